@@ -1,0 +1,240 @@
+"""Python front of the CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, ``__graft_entry__.smoke()`` and
+bench.py's cpu_baseline / ``--impl reference`` legs may import this package.
+The product path (paper_2201_07498_b200) never imports it and shares no code
+with it. Arithmetic lives in oracle.c (plain single-threaded fp64 C, every
+function citing PAPER.md); this file only marshals arrays and strings the C
+steps together in the paper's order (Lanczos, then Jacobi on
+T, then the Ritz projection 𝒱V).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.c")
+
+# breakdown thresholds tau per storage dtype (reading Q7)
+TAU = {"f64": 1e-12, "f32": 1e-6, "bf16": 1e-3}
+_DT = {"f64": 0, "f32": 1, "bf16": 2}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc: -O2, no -ffast-math (IEEE semantics kept),
+    single-threaded, no vector intrinsics."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
+                               "-shared", "-std=c11", "-o", _SO + ".tmp", _SRC, "-lm"])
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+_lib = None
+P = ctypes.c_void_p
+I64, I32, U64, D = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        sig = {
+            "orc_coo_to_csr": (I64, [I64, I64, P, P, P, P, P, P]),
+            "orc_is_symmetric": (ctypes.c_int, [I64, P, P, P]),
+            "orc_partition": (ctypes.c_int, [I64, P, I32, P]),
+            "orc_layout": (I64, [I64, P, P, P, I32, P, I32, ctypes.c_int, P, P, P]),
+            "orc_v1": (None, [U64, I64, P]),
+            "orc_spmv": (None, [I64, P, P, P, P, P]),
+            "orc_lanczos": (I64, [I64, P, P, P, P, I32, I32, D, P, P, P, P]),
+            "orc_jacobi": (ctypes.c_int, [I32, P, P, P, I32, P]),
+            "orc_select": (I32, [I32, P, I32, P]),
+            "orc_ritz": (None, [I64, I32, P, P, I32, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+# ---------------------------------------------------------------------------
+def coo_to_csr(n, row, col, val):
+    """O1: canonical CSR (rows grouped, columns sorted, duplicates summed in input order)."""
+    row, col, val = _c(row, np.int64), _c(col, np.int32), _c(val, np.float64)
+    nnz = len(val)
+    rp = np.zeros(n + 1, np.int64)
+    c = np.zeros(max(nnz, 1), np.int32)
+    v = np.zeros(max(nnz, 1), np.float64)
+    k = _load().orc_coo_to_csr(n, nnz, _p(row), _p(col), _p(val), _p(rp), _p(c), _p(v))
+    if k < 0:
+        raise ValueError(f"oracle coo_to_csr: error {-k}")
+    return rp, c[:k].copy(), v[:k].copy()
+
+
+def canonicalize_csr(n, rowptr, col, val):
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rowptr))
+    return coo_to_csr(n, rows, col, val)
+
+
+def is_symmetric(n, rowptr, col, val) -> bool:
+    rowptr, col, val = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    return bool(_load().orc_is_symmetric(n, _p(rowptr), _p(col), _p(val)))
+
+
+def partition(rowptr, G: int) -> np.ndarray:
+    """O2: rule P boundaries b[0..G]."""
+    rowptr = _c(rowptr, np.int64)
+    n = len(rowptr) - 1
+    b = np.zeros(G + 1, np.int64)
+    if _load().orc_partition(n, _p(rowptr), G, _p(b)) != 0:
+        raise ValueError("oracle partition: invalid G")
+    return b
+
+
+def layout(rowptr, col, val, G: int, b, g: int, dtype: str = "f64"):
+    """O2: per-partition local CSR (rebased rowptr, padded-remapped columns,
+    values rounded to dtype, returned as f64) and n_pad."""
+    rowptr, col, val, b = (_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64),
+                           _c(b, np.int64))
+    n = len(rowptr) - 1
+    ng = int(b[g + 1] - b[g])
+    zg = int(rowptr[b[g + 1]] - rowptr[b[g]])
+    lrp = np.zeros(ng + 1, np.int64)
+    lc = np.zeros(max(zg, 1), np.int32)
+    lv = np.zeros(max(zg, 1), np.float64)
+    npad = _load().orc_layout(n, _p(rowptr), _p(col), _p(val), G, _p(b), g, _DT[dtype],
+                              _p(lrp), _p(lc), _p(lv))
+    return lrp, lc[:zg].copy(), lv[:zg].copy(), int(npad)
+
+
+def v1(seed: int, n: int) -> np.ndarray:
+    """O3: unnormalised start vector u_r = 2 U(h3(seed, 0x7631, r)) - 1."""
+    u = np.zeros(n, np.float64)
+    _load().orc_v1(seed, n, _p(u))
+    return u
+
+
+def spmv(rowptr, col, val, x) -> np.ndarray:
+    rowptr, col, val, x = (_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64),
+                           _c(x, np.float64))
+    n = len(rowptr) - 1
+    y = np.zeros(n, np.float64)
+    _load().orc_spmv(n, _p(rowptr), _p(col), _p(val), _p(x), _p(y))
+    return y
+
+
+@dataclass
+class LanczosOut:
+    alpha: np.ndarray      # alpha_1..alpha_m'
+    beta: np.ndarray       # beta_1(=0)..beta_{m'+1}
+    V: np.ndarray | None   # (m', n)
+    m_found: int
+    breakdown: bool
+
+
+def lanczos(rowptr, col, val, v1vec, m: int, reorth: int = 1, tau: float = 1e-12,
+            keep_V: bool = True) -> LanczosOut:
+    rowptr, col, val, v1vec = (_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64),
+                               _c(v1vec, np.float64))
+    n = len(rowptr) - 1
+    alpha = np.zeros(m, np.float64)
+    beta = np.zeros(m + 1, np.float64)
+    V = np.zeros((m, n), np.float64) if keep_V else None
+    bd = np.zeros(1, np.int32)
+    mf = _load().orc_lanczos(n, _p(rowptr), _p(col), _p(val), _p(v1vec), m, reorth, tau,
+                             _p(alpha), _p(beta), _p(V) if keep_V else None, _p(bd))
+    if mf < 0:
+        raise MemoryError("oracle lanczos: out of memory")
+    return LanczosOut(alpha[:mf].copy(), beta[:mf + 1].copy(),
+                      V[:mf].copy() if keep_V else None, int(mf), bool(bd[0]))
+
+
+def tridiag_dense(alpha, beta) -> np.ndarray:
+    """O6: T = tridiag(beta_2..beta_m'; alpha_1..alpha_m'; beta_2..beta_m') (reading Q1)."""
+    mm = len(alpha)
+    T = np.diag(np.asarray(alpha, np.float64))
+    for k in range(1, mm):
+        T[k - 1, k] = T[k, k - 1] = beta[k]
+    return T
+
+
+def jacobi(A, max_sweeps: int = 50):
+    """O7: cyclic Jacobi; returns (theta, S (columns = eigenvectors), sweeps, converged)."""
+    A = np.array(A, dtype=np.float64, order="C", copy=True)
+    mm = A.shape[0]
+    theta = np.zeros(mm, np.float64)
+    S = np.zeros((mm, mm), np.float64)
+    sw = np.zeros(1, np.int32)
+    conv = _load().orc_jacobi(mm, _p(A), _p(theta), _p(S), max_sweeps, _p(sw))
+    return theta, S, int(sw[0]), bool(conv)
+
+
+def select(theta, K: int) -> np.ndarray:
+    """O8: indices of the top-K by (-|theta|, -theta)."""
+    theta = _c(theta, np.float64)
+    idx = np.zeros(max(K, 1), np.int32)
+    k = _load().orc_select(len(theta), _p(theta), K, _p(idx))
+    return idx[:k].copy()
+
+
+def ritz(V, S, idx) -> np.ndarray:
+    """O9: normalised, sign-fixed Ritz vectors (K, n)."""
+    V = _c(V, np.float64)
+    S = _c(S, np.float64)
+    idx = _c(idx, np.int32)
+    mm, n = V.shape
+    K = len(idx)
+    Y = np.zeros((K, n), np.float64)
+    _load().orc_ritz(n, mm, _p(V), _p(S), K, _p(idx), _p(Y))
+    return Y
+
+
+@dataclass
+class SolveOut:
+    eigenvalues: np.ndarray          # top-K' Ritz values, (-|θ|, -θ) order
+    eigenvectors: np.ndarray | None  # (K', n)
+    theta_all: np.ndarray            # all m' Ritz values (Jacobi order)
+    S: np.ndarray
+    idx: np.ndarray
+    lanczos: LanczosOut
+    jacobi_sweeps: int
+    jacobi_converged: bool
+    residual_est: np.ndarray         # |beta_{m'+1} s_{m',k}| for the selected k
+    extra: dict = field(default_factory=dict)
+
+
+def solve(rowptr, col, val, K: int, m: int | None = None, seed: int = 1, v1vec=None,
+          reorth: int = 1, tau: float = 1e-12, want_vectors: bool = True) -> SolveOut:
+    """The whole method in the paper's order:
+    O3 v1 -> O4-O6 Lanczos -> O7 Jacobi on T -> O8 select -> O9 Ritz."""
+    n = len(rowptr) - 1
+    if m is None:
+        m = K
+    if v1vec is None:
+        v1vec = v1(seed, n)
+    lz = lanczos(rowptr, col, val, v1vec, m, reorth, tau, keep_V=want_vectors)
+    T = tridiag_dense(lz.alpha, lz.beta)
+    theta, S, sw, conv = jacobi(T)
+    idx = select(theta, K)
+    evals = theta[idx]
+    Y = ritz(lz.V, S, idx) if want_vectors else None
+    mm = lz.m_found
+    rest = np.abs(lz.beta[mm] * S[mm - 1, idx]) if mm > 0 else np.zeros(0)
+    return SolveOut(evals, Y, theta, S, idx, lz, sw, conv, rest)

@@ -1,0 +1,395 @@
+"""Pins of the CPU oracle (oracle/) against things other than itself.
+
+Each test names the pin of DESIGN.md "Oracle pins" (P1..P10) it implements and
+the oracle step(s) it covers. These run on CPU (-m "not gpu").
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import oracle as O
+import synthgen as S
+
+
+def csr_of(a):
+    m = S.from_dense(a)
+    return m.rowptr, m.col, m.val
+
+
+def er_csr(n, samples, seed):
+    c = S.er_coo(n, samples, seed)
+    return O.coo_to_csr(n, c.row, c.col, c.val)
+
+
+def dense(n, rp, c, v):
+    return sp.csr_matrix((v, c, rp), shape=(n, n)).toarray()
+
+
+# ---------------------------------------------------------------- P10 (O1)
+def test_p10_coo_spec_examples(golden):
+    for ex in golden["coo"]:
+        e = np.array(ex["entries"], dtype=float).reshape(-1, 3)
+        rp, c, v = O.coo_to_csr(ex["n"], e[:, 0].astype(np.int64), e[:, 1].astype(np.int32),
+                                e[:, 2])
+        assert rp.tolist() == ex["rowptr"], ex["cite"]
+        assert c.tolist() == ex["col"], ex["cite"]
+        assert v.tolist() == ex["val"], ex["cite"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_p10_coo_duplicates_vs_dense_accumulation(seed):
+    """Duplicate summation == dense accumulation; round trip CSR->COO->CSR is the identity."""
+    rng = np.random.default_rng(seed)
+    n, nnz = 40, 600
+    r = rng.integers(0, n, nnz)
+    c = rng.integers(0, n, nnz).astype(np.int32)
+    v = rng.integers(-8, 9, nnz).astype(float) / 4  # exact sums in any order
+    rp, cc, vv = O.coo_to_csr(n, r, c, v)
+    d = np.zeros((n, n))
+    np.add.at(d, (r, c), v)
+    occupied = np.zeros((n, n), bool)
+    occupied[r, c] = True
+    assert np.array_equal(dense(n, rp, cc, vv), d)
+    assert len(vv) == occupied.sum()
+    for row in range(n):  # sorted, unique columns
+        cols = cc[rp[row]:rp[row + 1]]
+        assert np.all(np.diff(cols) > 0)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    rp2, c2, v2 = O.coo_to_csr(n, rows, cc, vv)
+    assert np.array_equal(rp2, rp) and np.array_equal(c2, cc) and np.array_equal(v2, vv)
+
+
+def test_p10_coo_rejects_out_of_range():
+    with pytest.raises(ValueError):
+        O.coo_to_csr(3, np.array([0, 3]), np.array([0, 0], np.int32), np.ones(2))
+    with pytest.raises(ValueError):
+        O.coo_to_csr(3, np.array([0, 1]), np.array([0, -1], np.int32), np.ones(2))
+
+
+def test_p10_symmetry_check():
+    rp, c, v = er_csr(200, 1000, 5)
+    assert O.is_symmetric(200, rp, c, v)
+    d = dense(200, rp, c, v)
+    assert np.array_equal(d, d.T)
+    v2 = v.copy()
+    k = np.nonzero(c != np.repeat(np.arange(200), np.diff(rp)))[0][0]
+    v2[k] = np.nextafter(v2[k], 10)  # one-ulp asymmetry
+    assert not O.is_symmetric(200, rp, c, v2)
+    # structural asymmetry: drop one off-diagonal entry
+    rows = np.repeat(np.arange(200), np.diff(rp))
+    keep = np.ones(len(v), bool)
+    keep[k] = False
+    rp3, c3, v3 = O.coo_to_csr(200, rows[keep], c[keep], v[keep])
+    assert not O.is_symmetric(200, rp3, c3, v3)
+
+
+# ---------------------------------------------------------------- P9 (O2)
+def brute_partition(rownnz, G):
+    n = len(rownnz)
+    pre = np.concatenate([[0], np.cumsum(rownnz)])
+    best = None
+    for cuts in itertools.combinations(range(1, n), G - 1):
+        b = (0,) + cuts + (n,)
+        load = max(pre[b[k + 1]] - pre[b[k]] for k in range(G))
+        key = (load, b)
+        if best is None or key < best:
+            best = key
+    return list(best[1])
+
+
+def test_p9_partition_spec_examples(golden):
+    for ex in golden["partition"]:
+        rp = np.concatenate([[0], np.cumsum(ex["row_nnz"])]).astype(np.int64)
+        assert O.partition(rp, ex["G"]).tolist() == ex["boundaries"], ex["cite"]
+
+
+def test_p9_partition_equals_brute_force():
+    rng = np.random.default_rng(7)
+    cases = 0
+    for _ in range(3000):
+        n = int(rng.integers(1, 10))
+        G = int(rng.integers(1, n + 1))
+        rownnz = rng.integers(0, 6, n) * (rng.random(n) > 0.3)
+        rp = np.concatenate([[0], np.cumsum(rownnz)]).astype(np.int64)
+        assert O.partition(rp, G).tolist() == brute_partition(rownnz, G), (rownnz, G)
+        cases += 1
+    assert cases == 3000
+
+
+def test_p9_partition_invalid():
+    with pytest.raises(ValueError):
+        O.partition(np.array([0, 1, 2]), 3)
+
+
+# ---------------------------------------------------------------- layout (O2)
+@pytest.mark.parametrize("G", [1, 2, 3, 5])
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+def test_layout_reassembles_matrix(G, dtype):
+    """Concatenated partitions, columns un-remapped, give back M (values rounded)."""
+    rp, c, v = er_csr(500, 3000, 11)
+    b = O.partition(rp, G)
+    npad_expect = int(math.ceil(max(np.diff(b)) / 64) * 64)
+    rows_all, cols_all, vals_all = [], [], []
+    for g in range(G):
+        lrp, lc, lv, npad = O.layout(rp, c, v, G, b, g, dtype)
+        assert npad == npad_expect
+        assert lrp[0] == 0 and len(lrp) == b[g + 1] - b[g] + 1
+        owner = lc // npad
+        local = lc % npad
+        assert np.all(local < np.diff(b)[owner])
+        rows_all.append(np.repeat(np.arange(b[g], b[g + 1]), np.diff(lrp)))
+        cols_all.append(b[owner] + local)
+        vals_all.append(lv)
+    assert np.array_equal(np.concatenate(rows_all), np.repeat(np.arange(500), np.diff(rp)))
+    assert np.array_equal(np.concatenate(cols_all), c)
+    lv = np.concatenate(vals_all)
+    if dtype == "f64":
+        assert np.array_equal(lv, v)
+    elif dtype == "f32":
+        assert np.array_equal(lv, v.astype(np.float32).astype(np.float64))
+    else:
+        check_bf16_rounding(v, lv)
+
+
+def check_bf16_rounding(x, r):
+    """r is x rounded to 8 significant bits, to nearest, ties to even (property pin)."""
+    nz = x != 0
+    e = np.floor(np.log2(np.abs(x[nz])))
+    ulp = 2.0 ** (e - 7)
+    q = r[nz] / ulp
+    assert np.all(q == np.round(q)), "not on the bf16 grid"
+    assert np.all(np.abs(r[nz] - x[nz]) <= ulp / 2 * (1 + 1e-15) + 2.0 ** (e - 8) * 0), "not nearest"
+    tie = np.abs(np.abs(r[nz] - x[nz]) - ulp / 2) == 0
+    assert np.all((q[tie] % 2) == 0), "tie not to even"
+
+
+def test_bf16_rounding_ties():
+    """Exact midpoints between bf16 neighbours round to the even mantissa."""
+    x = np.array([1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8), 1 + 2 ** -8 + 2 ** -30, 0.75])
+    rp = np.arange(len(x) + 1, dtype=np.int64)
+    c = np.arange(len(x), dtype=np.int32)
+    _, _, lv, _ = O.layout(rp, c, x, 1, np.array([0, len(x)]), 0, "bf16")
+    assert lv.tolist() == [1.0, 1 + 4 * 2 ** -8, -1.0, 1 + 2 * 2 ** -8, 0.75]
+
+
+# ---------------------------------------------------------------- O3 v1
+def splitmix_first(state):
+    m = (1 << 64) - 1
+    z = (state + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def test_v1_hash_pinned_to_splitmix64_vector(golden):
+    # the Python mix below is anchored by the published splitmix64 test vector ...
+    assert splitmix_first(0) == int(golden["splitmix64"]["state0_first_output"], 16)
+
+    def h3(s, a, b):
+        return splitmix_first(splitmix_first(splitmix_first(s) ^ a) ^ b)
+
+    # ... and the oracle's v1 entries equal it bit for bit (reading Q8)
+    for seed in (0, 1, 12345):
+        u = O.v1(seed, 50)
+        ref = [2.0 * ((h3(seed, 0x7631, r) >> 11) * 2.0 ** -53) - 1.0 for r in range(50)]
+        assert u.tolist() == ref
+    u = O.v1(3, 100000)
+    assert u.min() >= -1 and u.max() < 1 and abs(u.mean()) < 0.01
+
+
+# ---------------------------------------------------------------- SpMV (l.9)
+def test_spmv_vs_scipy():
+    rp, c, v = er_csr(700, 5000, 2)
+    x = np.random.default_rng(0).standard_normal(700)
+    y = O.spmv(rp, c, v, x)
+    yr = sp.csr_matrix((v, c, rp), shape=(700, 700)) @ x
+    assert np.allclose(y, yr, rtol=0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- P2 (O7)
+def test_p2_jacobi_spec_examples():
+    th, Sm, sw, conv = O.jacobi(np.array([[2.0, 1], [1, 2]]))
+    assert conv
+    order = np.argsort(-th)
+    assert np.allclose(th[order], [3, 1], atol=1e-15)
+    v3 = Sm[:, order[0]] * np.sign(Sm[0, order[0]])
+    v1 = Sm[:, order[1]] * np.sign(Sm[0, order[1]])
+    assert np.allclose(v3, [2 ** -0.5, 2 ** -0.5], atol=1e-15)
+    assert np.allclose(v1, [2 ** -0.5, -2 ** -0.5], atol=1e-15)
+    th, Sm, sw, conv = O.jacobi(np.eye(6))
+    assert conv and sw == 1 and np.array_equal(Sm, np.eye(6)) and np.array_equal(th, np.ones(6))
+
+
+@pytest.mark.parametrize("m", [2, 3, 8, 24, 64])
+def test_p2_jacobi_vs_eigh_and_invariants(m):
+    rng = np.random.default_rng(m)
+    for trial in range(3):
+        if trial == 0:  # random tridiagonal (the shape Lanczos produces)
+            A = np.diag(rng.standard_normal(m))
+            off = rng.random(m - 1) + 0.01
+            A += np.diag(off, 1) + np.diag(off, -1)
+        else:
+            B = rng.standard_normal((m, m))
+            A = (B + B.T) / 2
+        th, Sm, sw, conv = O.jacobi(A)
+        assert conv
+        ref = np.linalg.eigvalsh(A)
+        nrm = np.linalg.norm(A, 2)
+        assert np.allclose(np.sort(th), ref, rtol=0, atol=1e-13 * nrm)
+        assert abs(th.sum() - np.trace(A)) <= 1e-13 * nrm * m
+        assert np.abs(Sm.T @ Sm - np.eye(m)).max() <= 1e-13 * m
+        assert np.abs(A @ Sm - Sm * th).max() <= 1e-13 * nrm * m
+
+
+def test_p2_jacobi_sweep_cap():
+    rng = np.random.default_rng(1)
+    B = rng.standard_normal((20, 20))
+    th, Sm, sw, conv = O.jacobi(B + B.T, max_sweeps=1)
+    assert sw == 1 and not conv
+
+
+# ---------------------------------------------------------------- P3 (O4-O8)
+def test_p3_alpha1(golden):
+    ex = golden["alpha1_diag3210"]
+    rp, c, v = csr_of(np.diag(ex["diag"]).astype(float))
+    lz = O.lanczos(rp, c, v, np.array(ex["v1"]), 1)
+    assert lz.alpha[0] == ex["alpha1"], ex["cite"]
+
+
+def test_p3_identity_breakdown(golden):
+    ex = golden["identity4_breakdown"]
+    rp, c, v = csr_of(np.eye(ex["n"]))
+    r = O.solve(rp, c, v, K=4, m=4, seed=5)
+    assert r.lanczos.breakdown and r.lanczos.m_found == ex["m_found"], ex["cite"]
+    assert np.allclose(r.eigenvalues, [ex["eigenvalue"]], atol=1e-15)
+
+
+@pytest.mark.parametrize("key", ["two_by_two", "antidiag_tie", "diag54321_top2"])
+def test_p3_small_solves(golden, key):
+    ex = golden[key]
+    A = np.array(ex["A"], float) if "A" in ex else np.diag(ex["diag"]).astype(float)
+    rp, c, v = csr_of(A)
+    r = O.solve(rp, c, v, K=ex["K"], m=ex.get("m", ex["K"]), seed=3)
+    assert np.allclose(r.eigenvalues, ex["eigenvalues"], rtol=0, atol=1e-14), ex["cite"]
+
+
+def test_p3_orthogonalisation_example(golden):
+    """basis {e1}, v = e1 + e2 -> e2. Lanczos on diag(1,0,0) from
+    v1 = e1 makes v_nxt = M e1 - alpha_1 e1 = 0 -> breakdown; use the MGS step on
+    A = [[0,1,0],[1,0,0],[0,0,0]] with v1 = e1: y = e2, alpha_1 = 0, w = e2."""
+    A = np.array([[0.0, 1, 0], [1, 0, 0], [0, 0, 0]])
+    rp, c, v = csr_of(A)
+    lz = O.lanczos(rp, c, v, np.array([1.0, 0, 0]), 2)
+    assert lz.V[1].tolist() == golden["orth_e1"]["result"]
+
+
+# ---------------------------------------------------------------- P1 (O3-O7)
+@pytest.mark.parametrize("n,samples,seed", [(40, 100, 1), (120, 500, 2), (300, 900, 3)])
+def test_p1_full_dimension_lanczos_equals_eigh(n, samples, seed):
+    rp, c, v = er_csr(n, samples, seed)
+    A = dense(n, rp, c, v)
+    r = O.solve(rp, c, v, K=n, m=n, seed=seed)
+    ref = np.linalg.eigvalsh(A)
+    nrm = np.linalg.norm(A, 2)
+    mf = r.lanczos.m_found
+    if mf == n:
+        assert np.allclose(np.sort(r.theta_all), ref, rtol=0, atol=1e-10 * nrm)
+    else:  # invariant subspace hit: every Ritz value is an eigenvalue
+        d = np.abs(r.theta_all[:, None] - ref[None, :]).min(axis=1)
+        assert d.max() <= 1e-10 * nrm
+
+
+# ---------------------------------------------------------------- P4 (O3-O9)
+def test_p4_dirichlet_1M_closed_form():
+    """Dirichlet tridiag(-1,2,-1), n = 10^6, K = m = 16, v1 = sum of 16 spread sine
+    modes k_i = 58,823 i: the Krylov space is exactly their span, so the Ritz
+    values are the closed-form eigenvalues 2 - 2cos(pi k_i/(n+1))."""
+    n = 1_000_000
+    A = S.dirichlet(n)
+    j = np.arange(1, n + 1)
+    ks = 58_823 * np.arange(1, 17)
+    v1 = np.zeros(n)
+    for k in ks:
+        v1 += np.sin(np.pi * k * j / (n + 1))
+    r = O.solve(A.rowptr, A.col, A.val, K=16, m=16, v1vec=v1, tau=0.0, want_vectors=False)
+    lam = 2 - 2 * np.cos(np.pi * ks / (n + 1))
+    assert np.abs(np.sort(r.theta_all) - np.sort(lam)).max() <= 1e-13
+    assert r.lanczos.beta[16] <= 1e-8
+
+
+# ---------------------------------------------------------------- P5, P7 (O4-O10)
+@pytest.mark.parametrize("kind", ["dirichlet", "cycle"])
+def test_p5_kahan_bound_random_start(kind):
+    """Random v1: every Ritz value lies within its true residual of a closed-form
+    eigenvalue (min_k |theta - lambda_k| <= ||A y - theta y||)."""
+    n = 100_000
+    A = S.dirichlet(n) if kind == "dirichlet" else S.cycle_laplacian(n)
+    r = O.solve(A.rowptr, A.col, A.val, K=16, m=16, seed=9)
+    kk = np.arange(1, n + 1) if kind == "dirichlet" else np.arange(n)
+    lam = (2 - 2 * np.cos(np.pi * kk / (n + 1))) if kind == "dirichlet" else \
+        (2 - 2 * np.cos(2 * np.pi * kk / n))
+    lam = np.sort(lam)
+    for t, y in zip(r.eigenvalues, r.eigenvectors):
+        res = np.linalg.norm(O.spmv(A.rowptr, A.col, A.val, y) - t * y)
+        i = np.searchsorted(lam, t)
+        d = min(abs(lam[max(i - 1, 0)] - t), abs(lam[min(i, n - 1)] - t))
+        assert d <= res * (1 + 1e-9) + 1e-14
+
+
+@pytest.mark.parametrize("n", [6, 12, 13, 40, 64])
+def test_p6_cycle_breakdown_and_multiplicity(n):
+    """Cycle Laplacian: n//2+1 distinct eigenvalues 2-2cos(2 pi k/n); Lanczos from a
+    generic v1 breaks down at exactly i = n//2 + 1 and its Ritz values are those."""
+    A = S.cycle_laplacian(n)
+    r = O.solve(A.rowptr, A.col, A.val, K=n, m=n, seed=4)
+    distinct = np.unique(np.round(2 - 2 * np.cos(2 * np.pi * np.arange(n) / n), 12))
+    assert r.lanczos.breakdown
+    assert r.lanczos.m_found == n // 2 + 1 == len(distinct)
+    assert np.allclose(np.sort(r.theta_all), distinct, atol=1e-12)
+
+
+@pytest.mark.parametrize("m", [8, 24, 64])
+def test_p7_lanczos_invariants(m):
+    """Orthonormal basis, Lanczos relation, residual estimate = true residual,
+    trace(T) = sum(theta), theta inside the spectrum bounds."""
+    A = S.rmat(12, 40_000, 5)
+    n = A.n
+    rp, c, v = A.rowptr, A.col, A.val
+    r = O.solve(rp, c, v, K=8, m=m, seed=2)
+    lz = r.lanczos
+    V = lz.V
+    mf = lz.m_found
+    assert np.abs(V @ V.T - np.eye(mf)).max() <= 1e-13
+    M = sp.csr_matrix((v, c, rp), shape=(n, n))
+    T = O.tridiag_dense(lz.alpha, lz.beta)
+    AV = (M @ V.T)
+    # residual of the Lanczos relation, using the next direction w = beta_{m+1} v_{m+1}
+    R = AV - V.T @ T
+    nrmA = spla.norm(M, 2) if n < 3000 else abs(spla.eigsh(M, 1, which="LM")[0][0])
+    # all columns except the last satisfy the three-term relation exactly
+    assert np.abs(R[:, :-1]).max() <= 1e-12 * nrmA
+    assert abs(np.linalg.norm(R[:, -1]) - lz.beta[mf]) <= 1e-12 * nrmA
+    for k, (t, y) in enumerate(zip(r.eigenvalues, r.eigenvectors)):
+        true = np.linalg.norm(M @ y - t * y)
+        assert abs(true - r.residual_est[k]) <= 1e-12 * nrmA
+    assert abs(np.trace(T) - r.theta_all.sum()) <= 1e-12 * nrmA * m
+    assert np.all(np.abs(r.theta_all) <= nrmA * (1 + 1e-12))
+
+
+# ---------------------------------------------------------------- P8 (O4-O9)
+@pytest.mark.slow
+def test_p8_converged_pairs_match_arpack():
+    A = S.rmat(14, 120_000, 14)
+    n = A.n
+    M = sp.csr_matrix((A.val, A.col, A.rowptr), shape=(n, n))
+    r = O.solve(A.rowptr, A.col, A.val, K=8, m=64, seed=1)
+    ref = spla.eigsh(M, 8, which="LM", tol=1e-14)[0]
+    ref = ref[np.argsort(-np.abs(ref))]
+    nrm = abs(ref[0])
+    conv = r.residual_est <= 1e-10 * nrm
+    assert conv.sum() >= 4
+    assert np.allclose(r.eigenvalues[conv], ref[conv], rtol=1e-10, atol=0)
