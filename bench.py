@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py — Lanczos iter/s (and SpMV HBM GB/s, time-to-Top-K) of the hot path.
+
+Workload (default, BASELINE.json configs[2] "C3"): R-MAT power-law graph,
+n = 4,194,304, nnz ~ 61M, FDF (f32 storage, f64 compute), K = m = 24. One
+"step" = one full Top-K solve with the matrix resident in HBM: v1, 24 Lanczos
+iterations (SpMV + alpha, fused recurrence + reorth multi-dot, correction +
+beta), Jacobi on T, Ritz projection + normalisation.
+value = Lanczos iterations per second of the whole job (m * steps / time).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  (rows partitioned by nnz across ranks, NCCL allgather of v_i + scalars).
+
+The reference arm (--impl reference) times the CPU oracle (oracle/, fp64,
+single thread) on the same workload, one oracle Lanczos iteration per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_NOMINAL_GBS = 8000.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+WORKLOADS = {
+    "C3": dict(desc="R-MAT S=22 (n=4,194,304), 31,457,280 samples, Graph500 (a,b,c)=(.57,.19,.19), "
+                    "seed 22, symmetric, deduplicated, bf16-exact weights k/128",
+               K=24, m=24, storage="f32", compute="f64"),
+    "C3S": dict(desc="R-MAT S=16 (n=65,536), 491,520 samples, seed 16 (C3 shape, small)",
+                K=24, m=24, storage="f32", compute="f64"),
+}
+
+
+class ClockSampler:
+    """nvidia-smi sampler running DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_matrix(name: str):
+    import synthgen as S
+    return S.config_matrix(name)
+
+
+def spmv_bytes(nnz_g, n_g, n_x, s, sv):
+    """B_spmv = z_g (4 + s_v) + 4 (n_g + 1) + s n_x + s n_g."""
+    return nnz_g * (4 + sv) + 4 * (n_g + 1) + s * n_x + s * n_g
+
+
+def step_bytes(i, n_g, s):
+    """B_step(i) = (2i + 4) n_g s (fused recurrence + multi-dot, then correction)."""
+    return (2 * i + 4) * n_g * s
+
+
+def cpu_baseline(A, wl):
+    import oracle as O
+    t0 = time.perf_counter()
+    O.solve(A.rowptr, A.col, A.val, K=wl["K"], m=wl["m"], seed=1)
+    dt = time.perf_counter() - t0
+    return {"value": wl["m"] / dt, "unit": "iter/s", "cores": 1, "kind": "oracle",
+            "seconds": dt,
+            "sample": f"one full oracle solve of the same {wl['name']} matrix (v1 seed 1, m={wl['m']} "
+                      "Lanczos iterations with MGS reorth, Jacobi, Ritz), single-threaded fp64 C",
+            "host": host_info()}
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            info["mem_gb"] = round(int(f.readline().split()[1]) / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
+
+
+def run_reference(args, wl):
+    """--impl reference: the CPU oracle on the same workload, rank 0 only."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    A = make_matrix(wl["name"])
+    run = O.LanczosRun(A.rowptr, A.col, A.val, O.v1(1, A.n), wl["m"])
+    for _ in range(args.warmup):
+        run.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run.step()
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(wl, A, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} single oracle Lanczos iterations (SpMV + alpha + "
+                                       f"recurrence + MGS reorth, Alg. 1) on the full {wl['name']} matrix, "
+                                       f"cycling i = 1..{wl['m']}; Jacobi/Ritz excluded",
+                             "host": host_info()},
+            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "lanczos_iter_per_s"
+
+
+def config_of(wl, A, N):
+    return {"workload": wl["name"], "matrix": wl["desc"], "n": int(A.n), "nnz": int(A.nnz),
+            "K": wl["K"], "m": wl["m"],
+            "precision": "FDF" if (wl["storage"], wl["compute"]) == ("f32", "f64") else
+            f"{wl['storage']}-{wl['compute']}",
+            "vector_storage": wl["storage"], "value_storage": wl["storage"], "compute": wl["compute"],
+            "global_batch": 1, "parallelism": f"rows{N} (nnz-balanced row partition)",
+            "l2": "inputs larger than L2: matrix ~0.5 GB + basis 0.4 GB per solve vs 126 MB L2",
+            "step": "one full Top-K solve (v1, m Lanczos iterations, Jacobi, Ritz) with M resident"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=list(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload], name=args.workload)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    ws, rank, local = dist_env()
+    N = max(ws, 1)
+    if N != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if N > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2201_07498_b200 as T
+
+    A = make_matrix(wl["name"])
+    nid = None
+    if N > 1:
+        obj = [T.nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    kw = dict(storage=wl["storage"], compute=wl["compute"], m=wl["m"], device=local)
+    if N > 1:
+        kw.update(parts=N, rank=rank, world=N, nccl_id=nid)
+    h = T.TopkEig(A, wl["K"], profile=True, **kw)
+    rp, _, _, npad = h.layout(0)
+    n_g, nnz_g = len(rp) - 1, int(rp[-1])
+    K, m = wl["K"], wl["m"]
+    ev = torch.zeros(K, dtype=torch.float64, device="cuda")
+    Y = torch.zeros(K, max(n_g, 1), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.ExternalStream(h.stream)
+
+    for i in range(args.warmup):
+        h.solve_async(1 + i, ev.data_ptr(), Y.data_ptr(), "f32")
+        h.sync()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)  # let the sampler spin up before the timed region
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        h.solve_async(100 + i, ev.data_ptr(), Y.data_ptr(), "f32")
+    e1.record(stream)
+    info = h.sync()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kt = h.kernel_times()  # last solve of the timed region, events inside the graph
+    ms_step = ms / args.steps
+    value = m * args.steps / (ms / 1e3)
+
+    s = 4 if wl["storage"] == "f32" else 8 if wl["storage"] == "f64" else 2
+    sv = s
+    n_x = n_g if N == 1 else A.n
+    b_spmv = spmv_bytes(nnz_g, n_g, n_x, s, sv)
+    spmv_ms, spmv_n = kt["spmv"]
+    t_spmv = spmv_ms / max(spmv_n, 1)
+    spmv_gbs = b_spmv / (t_spmv * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    b_step_tot = sum(step_bytes(i, n_g, s) for i in range(1, m + 1))
+    stepcorr_ms = kt["step"][0] + kt["correct"][0]
+    kernels = {c: {"ms_total": round(v[0], 4), "launches": v[1]} for c, v in kt.items()}
+    kernels["spmv"]["gbs_algorithmic"] = round(spmv_gbs, 1)
+    kernels["step+correct"] = {"ms_total": round(stepcorr_ms, 4),
+                               "gbs_algorithmic": round(b_step_tot / (stepcorr_ms * 1e-3) / 1e9, 1)
+                               if stepcorr_ms > 0 else None}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                d = json.load(f)
+            if d.get("workload") == wl["name"] and d.get("n_gpus", 1) == N:
+                traffic = d.get("spmv_dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(T, A, wl, kw, args, N, rank, dist)
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu:
+        cpu = cpu_baseline(A, wl)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": N, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_of(wl, A, N),
+                "time_to_topk_ms": ms_step,
+                "spmv_hbm_gbs": spmv_gbs, "spmv_pct_of_8tbs": 100 * spmv_gbs / HBM_NOMINAL_GBS,
+                "roofline": {"kernel": "k_spmv (SpMV + alpha partial, Alg.1 l.9-10)", "bound": "hbm",
+                             "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
+                             "peak_source": peak_src, "traffic": traffic,
+                             "algorithmic_bytes_per_launch": b_spmv, "avg_launch_ms": t_spmv,
+                             "launches_timed": spmv_n},
+                "kernels": kernels,
+                "cpu_baseline": cpu,
+                "e2e": e2e,
+                "gpu_launches": int(info["gpu_launches"]) * args.steps,
+                "gpu_launches_per_step": int(info["gpu_launches"]),
+                "clocks": clocks,
+                "solve_info": {k: info[k] for k in ("k_found", "iterations", "breakdown", "jacobi_sweeps",
+                                                    "jacobi_converged")},
+                "paper_context": "paper (V100, fp32): 67x vs 104-thread ARPACK, 1.9x vs Alveo U280 FPGA "
+                                 "(PAPER.md:21,219); context only, not comparable"}
+        print(json.dumps(line), flush=True)
+    h.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(T, A, wl, kw, args, N, rank, dist):
+    """Same metric through the public API with host buffers: every step creates
+    the solver from the host CSR (H2D upload inside), solves, and copies the
+    eigenpairs back to host memory (D2H)."""
+    import torch
+    steps = max(1, min(args.e2e_steps, args.steps))
+    times = []
+    h2d = d2h = 0
+    for i in range(steps + 1):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        with T.TopkEig(A, wl["K"], check_symmetry=False, **kw) as h2:
+            r = h2.solve(seed=500 + i, vectors=True, vec_dtype="f32")
+            rp, _, _, _ = h2.layout(0) if i == 0 else (None, None, None, None)
+            if i == 0:
+                n_g, z_g = len(rp) - 1, int(rp[-1])
+                s = 4 if wl["storage"] == "f32" else 8
+                h2d = 4 * (n_g + 1) + z_g * (4 + s) + 16 * (z_g // 2048 + n_g // 2048 + 1) + 64
+                d2h = 8 * wl["K"] * 2 + 4 * wl["K"] * A.n
+        dt = time.perf_counter() - t0
+        if i > 0:  # first call warms the process (cudaMalloc pools, module load)
+            times.append(dt)
+    t = max(times)
+    if dist:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": wl["m"] / float(np.mean(times)) if not dist else wl["m"] / t, "unit": "iter/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "s_per_step": float(np.mean(times)),
+            "note": "create (host canonicalise + partition + layout + H2D, symmetry check skipped) "
+                    "+ solve + eigenvalues/eigenvectors (f32) D2H, wall clock"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,192 @@
+/*
+ * topk_eig.h — C ABI of the B200-native Top-K sparse eigensolver hot path
+ * (arXiv 2201.07498, "A Mixed Precision, Multi-GPU Design for Large-scale Top-K
+ * Sparse Eigenproblems").
+ *
+ * The library computes the K largest-magnitude eigenvalues ("the largest in
+ * modulo") and eigenvectors of a real symmetric sparse matrix M
+ * with the paper's two-phase method (Fig. 1):
+ *   phase 1  Lanczos, Algorithm 1: m iterations of
+ *            SpMV (l.9) + alpha (l.10) + three-term recurrence (l.11) +
+ *            full reorthogonalisation (l.12-18) + beta / normalise (l.6-7),
+ *            rows partitioned by nnz;
+ *   phase 2  Jacobi on the m x m tridiagonal T and the Ritz
+ *            projection 𝒱V.
+ * All steps run in hand-written sm_100a CUDA kernels owned by the handle.
+ * Arithmetic is fp64 inside every kernel with vectors stored in the storage
+ * dtype ("mixed precision": FDF = f32 storage, f64 compute).
+ *
+ * Conventions for every entry point
+ *   - Returns topk_status_t; no exception or signal crosses the ABI. On error a
+ *     message is available from topk_eig_last_error() (thread-local, valid until
+ *     the next call on the same thread).
+ *   - A CUDA or NCCL failure inside a handle makes it sticky: later calls on it
+ *     return TOPK_E_STATE. Destroy it.
+ *   - Pointers documented "host" must be host memory; "device" must be device
+ *     memory of the handle's device. Inputs are borrowed (read during the call
+ *     only); outputs are caller-owned buffers the library writes.
+ *   - One handle may be used by one thread at a time (thread-compatible).
+ *   - Breakdown (an exactly invariant Krylov subspace, beta ~ 0, reading Q7 of
+ *     DESIGN.md) is NOT an error: TOPK_OK with info.breakdown = 1 and
+ *     info.k_found < K; unused eigenvalue slots are NaN.
+ */
+#ifndef TOPK_EIG_H
+#define TOPK_EIG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct topk_eig_s *topk_eig_t; /* opaque; owns device memory, streams, graph, NCCL comm */
+
+typedef enum { TOPK_F64 = 0, TOPK_F32 = 1, TOPK_BF16 = 2 } topk_dtype_t;
+typedef enum { TOPK_CSR = 0, TOPK_COO = 1 } topk_format_t;
+
+typedef enum {
+    TOPK_OK = 0,
+    TOPK_E_INVALID = 1,       /* bad argument: K, m, n, dtype pair, null pointer, size          */
+    TOPK_E_STRUCTURE = 2,     /* row_ptr not monotone / wrong ends, index out of range          */
+    TOPK_E_NOT_SYMMETRIC = 3, /* symmetry check failed (structure or value bits)                */
+    TOPK_E_NOMEM = 4,         /* host or device allocation failed                               */
+    TOPK_E_CUDA = 5,          /* CUDA runtime error (handle becomes sticky)                     */
+    TOPK_E_NCCL = 6,          /* NCCL error (handle becomes sticky)                             */
+    TOPK_E_STATE = 7,         /* handle is sticky-failed or used out of order                   */
+    TOPK_E_NODEVICE = 8       /* no CUDA device / wrong architecture (the library never falls back to the CPU) */
+} topk_status_t;
+
+/* The input matrix M ("Input Matrix M"; stored as COO in the paper,
+ * PAPER.md:161). Borrowed during topk_eig_create only. Duplicated (row, col)
+ * entries are summed in input order; columns are sorted within rows. */
+typedef struct {
+    topk_format_t format;
+    int64_t n;              /* rows = cols; 1 <= n < 2^31                                        */
+    int64_t nnz;            /* entries supplied (before duplicate summation)                     */
+    const int64_t *row_ptr; /* CSR: host, n+1 entries, row_ptr[0]=0, non-decreasing, [n]=nnz      */
+    const int64_t *row_idx; /* COO: host, nnz row indices in [0,n)                               */
+    const int32_t *col_idx; /* host, nnz column indices in [0,n)                                 */
+    const void *values;     /* host, nnz values of values_dtype; NULL = pattern (all ones)       */
+    topk_dtype_t values_dtype; /* TOPK_F64 or TOPK_F32 (input representation)                 */
+} topk_matrix_t;
+
+/* Options. Zero-initialise, set struct_size = sizeof(topk_eig_opts_t), then set
+ * the fields you need; 0 selects the documented default. */
+typedef struct {
+    uint32_t struct_size;
+    int32_t krylov_dim;      /* m >= K Lanczos iterations; 0 -> K (the paper's "for i in 1, K", Alg.1 l.3) */
+    int32_t reorth;          /* 1 full classical Gram-Schmidt (default; Alg.1 l.12-18 as full reorth,
+                                reading Q3), 2 CGS twice, -1 none (paper's optional mode) */
+    int32_t num_parts;       /* G row partitions. Single process: G virtual ranks on
+                                one device ("loopback"). Multi-process: must equal world. 0 -> 1     */
+    int32_t device;          /* CUDA device ordinal of this process/handle                         */
+    int32_t check_symmetry;  /* 0 default -> check; -1 skip (caller guarantees M = M^T)            */
+    int32_t values_storage;  /* device dtype of matrix values; -1/0 default -> same as storage      */
+    int32_t use_graph;       /* 0 default -> capture the solve as one CUDA graph; -1 -> eager launches */
+    double breakdown_tol;    /* tau of reading Q7; 0 -> 1e-12 (f64), 1e-6 (f32), 1e-3 (bf16) storage */
+    /* multi-process (one process per GPU, NCCL over NVLink) */
+    int32_t rank;            /* this process's partition index g                                   */
+    int32_t world;           /* number of processes; 0/1 -> single process                         */
+    const void *nccl_id;     /* host, 128-byte ncclUniqueId from topk_eig_nccl_id() on rank 0     */
+    int32_t profile;         /* 1 -> bracket every kernel of part 0 with CUDA events (recorded inside
+                                the graph) so topk_eig_kernel_times() can report per-class device time */
+} topk_eig_opts_t;
+
+typedef struct {
+    int32_t k_found;          /* eigenpairs returned (= min(K, m') )                                */
+    int32_t iterations;       /* m' Lanczos iterations completed                                    */
+    int32_t breakdown;        /* 1 if Lanczos stopped early on beta <= tau * max(|alpha|, beta)      */
+    int32_t jacobi_sweeps;
+    int32_t jacobi_converged;
+    int32_t num_parts;
+    double beta_next;         /* beta_{m'+1} (reading Q6)                                           */
+    double ms_solve;          /* device time of the whole solve (CUDA events)                       */
+    int64_t bytes_model;      /* algorithmic HBM bytes of the solve on this part        */
+    int64_t gpu_launches;     /* kernels launched by the solve (this part)                          */
+} topk_eig_info_t;
+
+/* Create a solver for M, K eigenpairs, storage/compute precision pair.
+ *   storage : vector (and default value) storage dtype on the device
+ *   compute : arithmetic dtype inside the kernels; compute >= storage precision.
+ *             Supported (storage, compute): (F64,F64) "DDD", (F32,F64) "FDF",
+ *             (F32,F32) "FFF", (BF16,F64); values_storage BF16 with F32 vectors.
+ * Steps (DESIGN.md 8(a) rows a1-a4): canonicalise, check symmetry, partition by
+ * nnz (rule P, reading Q15), build the per-part layout, upload to HBM.
+ * Errors: TOPK_E_INVALID (K < 1, K > n, m < K, m > n, n >= 2^31, per-part nnz
+ * >= 2^31, bad dtype pair, NULL pointers), TOPK_E_STRUCTURE, TOPK_E_NOT_SYMMETRIC,
+ * TOPK_E_NOMEM, TOPK_E_CUDA, TOPK_E_NCCL, TOPK_E_NODEVICE. *out is NULL on error. */
+topk_status_t topk_eig_create(topk_eig_t *out, const topk_matrix_t *A, int32_t K,
+                              topk_dtype_t storage, topk_dtype_t compute,
+                              const topk_eig_opts_t *opts);
+
+/* Solve (DESIGN.md 8(a) rows a5-a15), host buffers.
+ *   seed        : start vector u_r = 2 U(h3(seed, 0x7631, r)) - 1 (reading Q8), used if v1 == NULL
+ *   v1          : host, NULL or n doubles: explicit start vector (normalised by the library)
+ *   eigenvalues : host, K doubles out, ordered by (-|lambda|, -lambda); NaN past k_found
+ *   eigenvectors: host, NULL or K*n out (vector k at [k*n, (k+1)*n)), dtype vec_dtype
+ *                 (TOPK_F64 or TOPK_F32); unit norm, sign <y_k, v_1> > 0 (reading Q12).
+ *                 Multi-process: each rank writes only its rows [b_g, b_{g+1}).
+ *   residual_est: host, NULL or K doubles out: |beta_{m'+1} s_{m',k}|
+ *   info        : host, NULL ok.
+ * Synchronises the handle's stream. */
+topk_status_t topk_eig_solve(topk_eig_t h, uint64_t seed, const double *v1, double *eigenvalues,
+                             void *eigenvectors, topk_dtype_t vec_dtype, double *residual_est,
+                             topk_eig_info_t *info);
+
+/* Asynchronous solve on the handle's stream with device-resident outputs (no
+ * host synchronisation): eigenvalues_dev (K doubles, device) and
+ * eigenvectors_dev (NULL or K * n_local values of vec_dtype, device, vector k at
+ * k * n_local) where n_local is this part's row count. Used for HBM-resident
+ * timing. Call topk_eig_sync() before reading results or info. */
+topk_status_t topk_eig_solve_async(topk_eig_t h, uint64_t seed, double *eigenvalues_dev,
+                                   void *eigenvectors_dev, topk_dtype_t vec_dtype);
+topk_status_t topk_eig_sync(topk_eig_t h, topk_eig_info_t *info);
+
+/* The handle's CUDA stream (cudaStream_t as void*), for event timing by callers. */
+void *topk_eig_stream(topk_eig_t h);
+
+void topk_eig_destroy(topk_eig_t h); /* NULL-safe; frees device memory, graph, comm */
+const char *topk_eig_last_error(void);
+
+/* 128-byte NCCL unique id for a multi-process create (call on rank 0, broadcast). */
+topk_status_t topk_eig_nccl_id(void *out128);
+
+/* ---- host-only planning (no device needed): rule-P partition and per-part layout
+ * (PAPER.md:125-128). Used by tests (CPU, gloo world_size 2) and by create. */
+/* boundaries: host, G+1 int64 out. */
+topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t G,
+                                      int64_t *boundaries);
+
+/* Per kernel class device time of the last solve (requires opts.profile = 1):
+ * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz, 6 ritz_norm.
+ * ms (host, 8 doubles): summed milliseconds; launches (host, 8 int32): launch counts.
+ * Events bracket each launch on the handle's stream (the stream the kernels run on). */
+topk_status_t topk_eig_kernel_times(topk_eig_t h, double *ms, int32_t *launches);
+
+/* ---- test/debug exports (same ABI; documented unstable) ---- */
+/* boundaries: host, G+1 int64 out */
+topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries);
+/* Part p (0 <= p < local parts) layout: rowptr host (n_p+1 int64), col host (z_p int32,
+ * remapped to the padded replica), val host (z_p doubles = stored values), n_pad out,
+ * sizes out (n_p, z_p). Any pointer may be NULL to query sizes only. */
+topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr, int32_t *col,
+                                     double *val, int64_t *n_pad, int64_t *n_rows,
+                                     int64_t *nnz);
+/* After a solve: alpha (m' doubles), beta (m'+1 doubles, beta[0] = 0), theta_all
+ * (m' doubles, Jacobi order), m_found out. Any pointer may be NULL. */
+topk_status_t topk_eig_export_tridiag(topk_eig_t h, double *alpha, double *beta,
+                                      double *theta_all, int32_t *m_found);
+/* After a solve: the stored Lanczos basis of part p as doubles: V[j * n_p + r] =
+ * s_j * u_j[r] for j < m'+1 (m'+1 columns when no breakdown), i.e. the
+ * normalised v_{j+1} (host, (m'+1) * n_p doubles). */
+topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32_t *ncols);
+/* One SpMV y = M x through the device kernel on part-local rows (x, y host, n
+ * doubles, global indexing; x is rounded to the storage dtype first, y is the
+ * fp64 row sums before storage rounding). */
+topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPK_EIG_H */

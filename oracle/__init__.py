@@ -54,6 +54,7 @@ def _load():
             "orc_v1": (None, [U64, I64, P]),
             "orc_spmv": (None, [I64, P, P, P, P, P]),
             "orc_lanczos": (I64, [I64, P, P, P, P, I32, I32, D, P, P, P, P]),
+            "orc_lanczos_iter": (ctypes.c_int, [I64, P, P, P, I32, I32, D, P, P, P, P, P, P]),
             "orc_jacobi": (ctypes.c_int, [I32, P, P, P, I32, P]),
             "orc_select": (I32, [I32, P, I32, P]),
             "orc_ritz": (None, [I64, I32, P, P, I32, P, P]),
@@ -164,6 +165,38 @@ def lanczos(rowptr, col, val, v1vec, m: int, reorth: int = 1, tau: float = 1e-12
         raise MemoryError("oracle lanczos: out of memory")
     return LanczosOut(alpha[:mf].copy(), beta[:mf + 1].copy(),
                       V[:mf].copy() if keep_V else None, int(mf), bool(bd[0]))
+
+
+class LanczosRun:
+    """Iteration-by-iteration driver over orc_lanczos_iter (the same arithmetic
+    as orc_lanczos); used to time bounded samples of the oracle. Restarts from
+    v1 after m iterations so the per-step reorth cost averages like a full solve."""
+
+    def __init__(self, rowptr, col, val, v1vec, m: int, reorth: int = 1, tau: float = 1e-12):
+        self.rp, self.c, self.v = (_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64))
+        self.n = len(self.rp) - 1
+        self.m, self.reorth, self.tau = m, reorth, tau
+        u = _c(v1vec, np.float64)
+        self.v1 = u / np.sqrt(np.add.accumulate(u * u)[-1])  # sequential sum, as in oracle.c
+        self.V = np.zeros((m, self.n))
+        self.vt = np.zeros(self.n)
+        self.vn = np.zeros(self.n)
+        self.alpha = np.zeros(m)
+        self.beta = np.zeros(m + 1)
+        self.ts = np.zeros(1)
+        self.i = 0
+
+    def step(self) -> int:
+        if self.i == self.m:
+            self.i = 0
+        if self.i == 0:
+            self.V[0] = self.v1
+            self.beta[0] = 0.0
+            self.ts[0] = 0.0
+        self.i += 1
+        return _load().orc_lanczos_iter(self.n, _p(self.rp), _p(self.c), _p(self.v), self.i,
+                                        self.reorth, self.tau, _p(self.V), _p(self.vt),
+                                        _p(self.vn), _p(self.alpha), _p(self.beta), _p(self.ts))
 
 
 def tridiag_dense(alpha, beta) -> np.ndarray:

@@ -214,6 +214,41 @@ static double dot(int64_t n, const double *a, const double *b) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* One iteration i (1-based) of Algorithm 1, l.5-18, on explicit state:
+ * Vw holds v_1..v_{i-1} (column-major, v_1 already normalised), vn holds v_nxt
+ * of iteration i-1, vt is scratch for v_tmp. Writes v_i, alpha_i, beta_i and the
+ * new v_nxt; *tscale is max(|alpha|, beta) so far (reading Q7). Returns 1 on
+ * breakdown (beta_i <= tau * tscale), else 0. orc_lanczos is this in a loop;
+ * bench.py's reference arm times single iterations of it. */
+int orc_lanczos_iter(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
+                     int32_t i, int32_t reorth, double tau, double *Vw, double *vt, double *vn,
+                     double *alpha, double *beta, double *tscale) {
+    double *vi = Vw + (size_t)(i - 1) * n;
+    if (i != 1) {                               /* l.5 */
+        double bi = sqrt(dot(n, vn, vn));       /* l.6 beta_i = ||v_nxt|| */
+        beta[i - 1] = bi;
+        if (bi <= tau * *tscale) return 1;
+        for (int64_t r = 0; r < n; ++r) vi[r] = vn[r] / bi; /* l.7 */
+        if (bi > *tscale) *tscale = bi;
+    }
+    orc_spmv(n, rowptr, col, val, vi, vt);          /* l.9 v_t = M v_i */
+    double ai = dot(n, vi, vt);                     /* l.10 alpha_i */
+    alpha[i - 1] = ai;
+    if (fabs(ai) > *tscale) *tscale = fabs(ai);
+    const double *vprev = (i > 1) ? Vw + (size_t)(i - 2) * n : NULL;
+    double bi = beta[i - 1];
+    for (int64_t r = 0; r < n; ++r)                 /* l.11 */
+        vn[r] = vt[r] - ai * vi[r] - (vprev ? bi * vprev[r] : 0.0);
+    if (reorth) {                                   /* l.12-18 (Q3) */
+        for (int32_t j = 1; j <= i; ++j) {
+            const double *vj = Vw + (size_t)(j - 1) * n;
+            double o = dot(n, vj, vn);
+            for (int64_t r = 0; r < n; ++r) vn[r] -= o * vj[r];
+        }
+    }
+    return 0;
+}
+
 /* O4-O6. Lanczos, Algorithm 1, m iterations (reading Q5:
  * m >= K; m = K is the paper's "for i in 1, K", l.3).
  *   v1     : start vector (normalised here, "L2-normalized")
@@ -247,28 +282,9 @@ int64_t orc_lanczos(int64_t n, const int64_t *rowptr, const int32_t *col, const 
     double tscale = 0.0;
     int64_t done = 0;
     for (int32_t i = 1; i <= m; ++i) {           /* l.3 */
-        double *vi = Vw + (size_t)(i - 1) * n;
-        if (i != 1) {                               /* l.5 */
-            double bi = sqrt(dot(n, vn, vn));       /* l.6 beta_i = ||v_nxt|| */
-            beta[i - 1] = bi;
-            if (bi <= tau * tscale) { *breakdown = 1; break; }
-            for (int64_t r = 0; r < n; ++r) vi[r] = vn[r] / bi; /* l.7 */
-            if (bi > tscale) tscale = bi;
-        }
-        orc_spmv(n, rowptr, col, val, vi, vt);          /* l.9 v_t = M v_i */
-        double ai = dot(n, vi, vt);                     /* l.10 alpha_i */
-        alpha[i - 1] = ai;
-        if (fabs(ai) > tscale) tscale = fabs(ai);
-        const double *vprev = (i > 1) ? Vw + (size_t)(i - 2) * n : NULL;
-        double bi = beta[i - 1];
-        for (int64_t r = 0; r < n; ++r)                 /* l.11 */
-            vn[r] = vt[r] - ai * vi[r] - (vprev ? bi * vprev[r] : 0.0);
-        if (reorth) {                                   /* l.12-18 (Q3) */
-            for (int32_t j = 1; j <= i; ++j) {
-                const double *vj = Vw + (size_t)(j - 1) * n;
-                double o = dot(n, vj, vn);
-                for (int64_t r = 0; r < n; ++r) vn[r] -= o * vj[r];
-            }
+        if (orc_lanczos_iter(n, rowptr, col, val, i, reorth, tau, Vw, vt, vn, alpha, beta, &tscale)) {
+            *breakdown = 1;
+            break;
         }
         done = i;
     }

@@ -1,0 +1,125 @@
+// device_common.cuh — storage/compute dtype plumbing, deterministic reductions,
+// last-block finalisation. sm_100a only.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace topk {
+
+using bf16 = __nv_bfloat16;
+
+// ---- storage dtype traits: vector width for 16-byte loads -------------------
+template <typename T> struct Vw;
+template <> struct Vw<double> { static constexpr int N = 2; };
+template <> struct Vw<float> { static constexpr int N = 4; };
+template <> struct Vw<bf16> { static constexpr int N = 8; };
+
+template <typename CT> __device__ __forceinline__ CT to_ct(double x) { return (CT)x; }
+template <typename CT> __device__ __forceinline__ CT cvt(double x) { return (CT)x; }
+template <typename CT> __device__ __forceinline__ CT cvt(float x) { return (CT)x; }
+template <typename CT> __device__ __forceinline__ CT cvt(bf16 x) { return (CT)__bfloat162float(x); }
+
+// round-to-nearest-even once on store (reading Q14)
+template <typename ST> __device__ __forceinline__ ST rnd(double x);
+template <> __device__ __forceinline__ double rnd<double>(double x) { return x; }
+template <> __device__ __forceinline__ float rnd<float>(double x) { return __double2float_rn(x); }
+template <> __device__ __forceinline__ bf16 rnd<bf16>(double x) { return __double2bfloat16(x); }
+template <typename ST> __device__ __forceinline__ ST rndf(float x);
+template <> __device__ __forceinline__ double rndf<double>(float x) { return (double)x; }
+template <> __device__ __forceinline__ float rndf<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 rndf<bf16>(float x) { return __float2bfloat16_rn(x); }
+template <typename ST, typename CT> __device__ __forceinline__ ST rnd_ct(CT x) {
+    if constexpr (sizeof(CT) == 8) return rnd<ST>((double)x);
+    else return rndf<ST>((float)x);
+}
+
+// 16-byte vector load/store of N = Vw<ST>::N storage elements, converted to CT.
+template <typename ST, typename CT>
+__device__ __forceinline__ void vload(const ST *__restrict__ p, CT (&o)[Vw<ST>::N]) {
+    uint4 raw = __ldg(reinterpret_cast<const uint4 *>(p));
+    const ST *e = reinterpret_cast<const ST *>(&raw);
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) o[q] = cvt<CT>(e[q]);
+}
+// streaming (evict-first) variant for data read once per kernel
+template <typename ST, typename CT>
+__device__ __forceinline__ void vload_cs(const ST *__restrict__ p, CT (&o)[Vw<ST>::N]) {
+    uint4 raw = __ldcs(reinterpret_cast<const uint4 *>(p));
+    const ST *e = reinterpret_cast<const ST *>(&raw);
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) o[q] = cvt<CT>(e[q]);
+}
+template <typename ST, typename CT>
+__device__ __forceinline__ void vstore(ST *__restrict__ p, const CT (&v)[Vw<ST>::N]) {
+    uint4 raw;
+    ST *e = reinterpret_cast<ST *>(&raw);
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) e[q] = rnd_ct<ST, CT>(v[q]);
+    *reinterpret_cast<uint4 *>(p) = raw;
+}
+// store rounded and return the rounded values in CT (what was stored)
+template <typename ST, typename CT>
+__device__ __forceinline__ void vstore_back(ST *__restrict__ p, CT (&v)[Vw<ST>::N]) {
+    uint4 raw;
+    ST *e = reinterpret_cast<ST *>(&raw);
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) {
+        e[q] = rnd_ct<ST, CT>(v[q]);
+        v[q] = cvt<CT>(e[q]);
+    }
+    *reinterpret_cast<uint4 *>(p) = raw;
+}
+
+// ---- deterministic reductions (fixed shuffle tree + fixed warp order) --------
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// Result valid in thread 0. `sm` needs NT/32 elements. Ends with a barrier.
+template <typename T, int NT> __device__ __forceinline__ T block_sum(T v, T *sm) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sm[w] = v;
+    __syncthreads();
+    T r = T(0);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) r += sm[i];
+    }
+    __syncthreads();
+    return r;
+}
+
+// Sum n values of a global array in fixed order using the whole block.
+// Result valid in thread 0.
+template <typename T, int NT>
+__device__ __forceinline__ T block_sum_array(const T *a, int n, int stride, T *sm) {
+    T s = T(0);
+    for (int i = threadIdx.x; i < n; i += NT) s += __ldcg(a + (size_t)i * stride);
+    return block_sum<T, NT>(s, sm);
+}
+
+// Classic threadfence "last block" pattern: every block publishes its partial,
+// then the block that arrives last (atomic ticket) reduces all partials in a
+// fixed order; it resets the ticket for the next launch (graph replays).
+__device__ __forceinline__ bool arrive_last(unsigned *counter, int *sflag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *sflag = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    const bool last = *sflag;
+    if (last) __threadfence();
+    return last;
+}
+
+// ---- counter-based start vector (reading Q8) ---------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+}  // namespace topk

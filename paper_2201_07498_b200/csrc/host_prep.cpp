@@ -1,0 +1,269 @@
+// host_prep.cpp — rows a1-a4 of the hot-path table: canonicalise
+// the input (COO as in the paper's Table I, or CSR), check
+// symmetry, partition rows by nnz, and lay out each partition
+// for the device (rows of M_g, replicated v_i).
+#include "host_prep.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace topk {
+
+static double load_value(const topk_matrix_t &A, int64_t k) {
+    if (!A.values) return 1.0;
+    if (A.values_dtype == TOPK_F32) return (double)((const float *)A.values)[k];
+    return ((const double *)A.values)[k];
+}
+
+// Sort one row's entries by column (stable: ties keep input order) and sum
+// duplicates in that order. Writes into col/val starting at `out`, returns count.
+static int64_t sort_row_sum(const int32_t *cin, const double *vin, int64_t len, int32_t *cout,
+                            double *vout, std::vector<int64_t> &perm) {
+    bool sorted_unique = true;
+    for (int64_t k = 1; k < len; ++k)
+        if (cin[k] <= cin[k - 1]) { sorted_unique = false; break; }
+    if (sorted_unique) {
+        std::memcpy(cout, cin, (size_t)len * sizeof(int32_t));
+        std::memcpy(vout, vin, (size_t)len * sizeof(double));
+        return len;
+    }
+    perm.resize((size_t)len);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return cin[a] < cin[b]; });
+    int64_t o = 0;
+    for (int64_t q = 0; q < len; ++q) {
+        int64_t k = perm[(size_t)q];
+        if (o > 0 && cout[o - 1] == cin[k]) {
+            vout[o - 1] += vin[k];
+        } else {
+            cout[o] = cin[k];
+            vout[o] = vin[k];
+            ++o;
+        }
+    }
+    return o;
+}
+
+topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
+    const int64_t n = A.n, nnz = A.nnz;
+    if (n < 1 || n >= (1ll << 31) || nnz < 0) { err = "n must be in [1, 2^31) and nnz >= 0"; return TOPK_E_INVALID; }
+    if (nnz > 0 && !A.col_idx) { err = "col_idx is NULL"; return TOPK_E_INVALID; }
+    if (A.values && A.values_dtype != TOPK_F64 && A.values_dtype != TOPK_F32) {
+        err = "values_dtype must be TOPK_F64 or TOPK_F32"; return TOPK_E_INVALID;
+    }
+    for (int64_t k = 0; k < nnz; ++k)
+        if (A.col_idx[k] < 0 || (int64_t)A.col_idx[k] >= n) { err = "column index out of range"; return TOPK_E_STRUCTURE; }
+
+    // Gather entries grouped by row, preserving input order inside a row.
+    std::vector<int64_t> start((size_t)n + 1, 0);
+    std::vector<int32_t> gcol((size_t)nnz);
+    std::vector<double> gval((size_t)nnz);
+    if (A.format == TOPK_CSR) {
+        if (!A.row_ptr) { err = "row_ptr is NULL"; return TOPK_E_INVALID; }
+        if (A.row_ptr[0] != 0 || A.row_ptr[n] != nnz) { err = "row_ptr[0] must be 0 and row_ptr[n] must be nnz"; return TOPK_E_STRUCTURE; }
+        for (int64_t r = 0; r < n; ++r)
+            if (A.row_ptr[r + 1] < A.row_ptr[r]) { err = "row_ptr is not non-decreasing"; return TOPK_E_STRUCTURE; }
+        std::memcpy(start.data(), A.row_ptr, (size_t)(n + 1) * sizeof(int64_t));
+        std::memcpy(gcol.data(), A.col_idx, (size_t)nnz * sizeof(int32_t));
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nnz; ++k) gval[(size_t)k] = load_value(A, k);
+    } else if (A.format == TOPK_COO) {
+        if (nnz > 0 && !A.row_idx) { err = "row_idx is NULL"; return TOPK_E_INVALID; }
+        for (int64_t k = 0; k < nnz; ++k)
+            if (A.row_idx[k] < 0 || A.row_idx[k] >= n) { err = "row index out of range"; return TOPK_E_STRUCTURE; }
+        for (int64_t k = 0; k < nnz; ++k) start[(size_t)A.row_idx[k] + 1]++;
+        std::partial_sum(start.begin(), start.end(), start.begin());
+        std::vector<int64_t> pos(start.begin(), start.end() - 1);
+        for (int64_t k = 0; k < nnz; ++k) {
+            int64_t p = pos[(size_t)A.row_idx[k]]++;
+            gcol[(size_t)p] = A.col_idx[k];
+            gval[(size_t)p] = load_value(A, k);
+        }
+    } else {
+        err = "unknown matrix format"; return TOPK_E_INVALID;
+    }
+
+    // Per row: stable sort by column, sum duplicates; then compact.
+    std::vector<int64_t> cnt((size_t)n, 0);
+    out.n = n;
+    out.col.resize((size_t)nnz);
+    out.val.resize((size_t)nnz);
+#pragma omp parallel
+    {
+        std::vector<int64_t> perm;
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t r = 0; r < n; ++r) {
+            int64_t b = start[(size_t)r], len = start[(size_t)r + 1] - b;
+            cnt[(size_t)r] = sort_row_sum(gcol.data() + b, gval.data() + b, len,
+                                          out.col.data() + b, out.val.data() + b, perm);
+        }
+    }
+    out.rowptr.assign((size_t)n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) out.rowptr[(size_t)r + 1] = out.rowptr[(size_t)r] + cnt[(size_t)r];
+    if (out.rowptr[(size_t)n] != nnz) {  // duplicates were merged: compact in place
+        for (int64_t r = 0; r < n; ++r) {
+            int64_t src = start[(size_t)r], dst = out.rowptr[(size_t)r];
+            if (src != dst) {
+                std::memmove(out.col.data() + dst, out.col.data() + src, (size_t)cnt[(size_t)r] * sizeof(int32_t));
+                std::memmove(out.val.data() + dst, out.val.data() + src, (size_t)cnt[(size_t)r] * sizeof(double));
+            }
+        }
+        out.col.resize((size_t)out.rowptr[(size_t)n]);
+        out.val.resize((size_t)out.rowptr[(size_t)n]);
+    }
+    return TOPK_OK;
+}
+
+bool is_symmetric(const Csr &m) {
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(| : bad)
+    for (int64_t r = 0; r < m.n; ++r) {
+        if (bad) continue;
+        for (int64_t k = m.rowptr[(size_t)r]; k < m.rowptr[(size_t)r + 1]; ++k) {
+            int32_t c = m.col[(size_t)k];
+            const int32_t *b = m.col.data() + m.rowptr[(size_t)c];
+            const int32_t *e = m.col.data() + m.rowptr[(size_t)c + 1];
+            const int32_t *p = std::lower_bound(b, e, (int32_t)r);
+            if (p == e || *p != (int32_t)r) { bad = 1; break; }
+            double x = m.val[(size_t)k], y = m.val[(size_t)(p - m.col.data())];
+            uint64_t xb, yb;
+            std::memcpy(&xb, &x, 8);
+            std::memcpy(&yb, &y, 8);
+            if (xb != yb) { bad = 1; break; }
+        }
+    }
+    return !bad;
+}
+
+// Number of parts a left-to-right greedy packing with bottleneck B needs,
+// jumping part by part with binary searches on the prefix sum rowptr.
+static int64_t parts_needed(const int64_t *rowptr, int64_t n, int64_t B, int64_t cap) {
+    int64_t s = 0, parts = 0;
+    while (s < n) {
+        ++parts;
+        if (parts > cap) return parts;
+        // last row index e (exclusive) with rowptr[e] - rowptr[s] <= B
+        const int64_t *p = std::upper_bound(rowptr + s, rowptr + n + 1, rowptr[s] + B);
+        int64_t e = (int64_t)(p - rowptr) - 1;
+        if (e <= s) return INT64_MAX;  // a single row exceeds B
+        s = e;
+    }
+    return parts;
+}
+
+topk_status_t partition_rule_p(const int64_t *rowptr, int64_t n, int32_t G, int64_t *b) {
+    if (G < 1 || n < G) return TOPK_E_INVALID;
+    int64_t maxrow = 0;
+    for (int64_t r = 0; r < n; ++r) maxrow = std::max(maxrow, rowptr[r + 1] - rowptr[r]);
+    int64_t lo = maxrow, hi = std::max(maxrow, rowptr[n]);
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (parts_needed(rowptr, n, mid, G) <= G) hi = mid; else lo = mid + 1;
+    }
+    const int64_t Bs = lo;
+    b[G] = n;
+    for (int32_t k = G - 1; k >= 1; --k) {
+        int64_t target = rowptr[b[k + 1]] - Bs;
+        int64_t j = (int64_t)(std::lower_bound(rowptr, rowptr + n + 1, target) - rowptr);
+        b[k] = std::max<int64_t>(j, k);
+    }
+    b[0] = 0;
+    return TOPK_OK;
+}
+
+int64_t padded_rows(const int64_t *b, int32_t G) {
+    int64_t mx = 0;
+    for (int32_t g = 0; g < G; ++g) mx = std::max(mx, b[g + 1] - b[g]);
+    return (mx + 63) / 64 * 64;
+}
+
+float round_f32(double x) { return (float)x; }
+
+uint16_t round_bf16_bits(double x) {
+    // f64 -> f32 with round-to-odd, then f32 -> bf16 round-to-nearest-even:
+    // exact single rounding because f32 keeps 16 more bits than bf16.
+    float f = (float)x;
+    if (std::isfinite(x) && (double)f != x) {
+        if (std::fabs((double)f) > std::fabs(x)) f = std::nextafter(f, 0.0f);
+        uint32_t fb;
+        std::memcpy(&fb, &f, 4);
+        fb |= 1u;
+        std::memcpy(&f, &fb, 4);
+    }
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) return (uint16_t)((u >> 16) | 0x40);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+double bf16_bits_to_double(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+static void build_tiles(const int32_t *rowptr, int64_t nrows, std::vector<Tile> &tiles,
+                        std::vector<LongRow> &longrows) {
+    tiles.clear();
+    longrows.clear();
+    int64_t r = 0;
+    while (r < nrows) {
+        int64_t len = rowptr[r + 1] - rowptr[r];
+        if (len > kTileNnz) {  // long row: fixed chunks
+            LongRow L;
+            L.row = (int32_t)r;
+            L.first_tile = (int32_t)tiles.size();
+            L.nchunks = (int32_t)((len + kTileNnz - 1) / kTileNnz);
+            L.pad = 0;
+            for (int32_t c = 0; c < L.nchunks; ++c)
+                tiles.push_back(Tile{(int32_t)r, (int32_t)(r + 1),
+                                     (int32_t)(rowptr[r] + (int64_t)c * kTileNnz),
+                                     (int32_t)longrows.size()});
+            longrows.push_back(L);
+            ++r;
+            continue;
+        }
+        int64_t s = r;
+        while (r < nrows && r - s < kTileRows) {
+            int64_t l = rowptr[r + 1] - rowptr[r];
+            if (l > kTileNnz) break;
+            if (rowptr[r + 1] - rowptr[s] > kTileNnz) break;
+            ++r;
+        }
+        tiles.push_back(Tile{(int32_t)s, (int32_t)r, rowptr[s], -1});
+    }
+}
+
+topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
+                         PartLayout &out, std::string &err) {
+    const int64_t r0 = b[g], r1 = b[g + 1];
+    const int64_t z0 = m.rowptr[(size_t)r0], z1 = m.rowptr[(size_t)r1];
+    if (z1 - z0 >= (1ll << 31) - kTileNnz) { err = "per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
+    if ((int64_t)G * npad >= (1ll << 31)) { err = "G * n_pad must be < 2^31"; return TOPK_E_INVALID; }
+    out.row0 = r0;
+    out.nrows = r1 - r0;
+    out.npad = npad;
+    out.rowptr.resize((size_t)(r1 - r0 + 1));
+    for (int64_t r = r0; r <= r1; ++r) out.rowptr[(size_t)(r - r0)] = (int32_t)(m.rowptr[(size_t)r] - z0);
+    out.col.resize((size_t)(z1 - z0));
+    out.val.assign(m.val.begin() + z0, m.val.begin() + z1);
+    // column remap c -> owner(c) * npad + (c - b[owner]) (owner by binary search on b)
+#pragma omp parallel for schedule(static)
+    for (int64_t k = z0; k < z1; ++k) {
+        int64_t c = m.col[(size_t)k];
+        int32_t owner = (int32_t)(std::upper_bound(b, b + G + 1, c) - b) - 1;
+        out.col[(size_t)(k - z0)] = (int32_t)(owner * npad + (c - b[owner]));
+    }
+    build_tiles(out.rowptr.data(), out.nrows, out.tiles, out.longrows);
+    return TOPK_OK;
+}
+
+}  // namespace topk

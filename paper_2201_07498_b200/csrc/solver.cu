@@ -1,0 +1,875 @@
+// solver.cu — orchestrator and C ABI (include/topk_eig.h).
+//
+// One handle = one process's view: either a single process driving G row
+// partitions on one device ("loopback": the G parts share the exchange buffers,
+// so every exchange is a no-op ordered on one stream), or one rank of a
+// multi-process NCCL job (one part per process, exchanges are in-place
+// ncclAllGather over NVLink). Both run the same kernels in the same order, so a
+// loopback-G solve and an NCCL-G solve are bitwise identical by construction.
+//
+// Per solve (DESIGN.md 8(a) a5-a15), all device-side, captured as ONE CUDA graph:
+//   k_v1 -> [exchange] -> for i in 1..m: k_spmv, [x], k_step, [x], k_correct, [x]
+//   -> k_jacobi -> k_ritz -> [x] -> k_ritz_norm
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_prep.h"
+#include "kernels.cuh"
+#include "topk_eig.h"
+
+using namespace topk;
+
+static thread_local std::string g_last_error;
+
+static topk_status_t fail(topk_status_t s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            throw CudaFail(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+        }                                                                                    \
+    } while (0)
+#define NCCL_TRY(expr)                                                                       \
+    do {                                                                                     \
+        ncclResult_t _r = (expr);                                                            \
+        if (_r != ncclSuccess) throw NcclFail(std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+struct CudaFail { std::string msg; explicit CudaFail(std::string m) : msg(std::move(m)) {} };
+struct NcclFail { std::string msg; explicit NcclFail(std::string m) : msg(std::move(m)) {} };
+
+static size_t dsize(topk_dtype_t t) { return t == TOPK_F64 ? 8 : t == TOPK_F32 ? 4 : 2; }
+
+struct SolveParams {
+    uint64_t seed;
+    int use_v1;
+    int out_dtype;
+    void *out_ptr;
+};
+
+struct Part {
+    int g = 0;
+    int64_t row0 = 0, nrows = 0, npad = 0, nnz = 0;
+    int ntiles = 0, nlong = 0;
+    int32_t *rowptr = nullptr, *col = nullptr;
+    void *val = nullptr;
+    Tile *tiles = nullptr;
+    LongRow *longrows = nullptr;
+    double *long_parts = nullptr, *alpha_long = nullptr;
+    unsigned *long_cnt = nullptr;
+    void *V = nullptr, *y = nullptr, *w = nullptr;
+    double *Y = nullptr;
+    void *out = nullptr;       // internal eigenvector output (K * nrows f64)
+    double *v1buf = nullptr;
+    double *y_dbg = nullptr;
+    double *slots = nullptr;
+    unsigned *counters = nullptr;  // [8]
+    char *state = nullptr;         // device state block
+    size_t state_bytes = 0;
+    LzState st{};
+    std::vector<char> hstate;      // host mirror
+};
+
+struct topk_eig_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0;
+    int K = 0, m = 0, G = 1, world = 1, rank = 0;
+    topk_dtype_t vs = TOPK_F64, ms = TOPK_F64, cs = TOPK_F64;
+    int reorth = 1;
+    double tau = 1e-12;
+    int use_graph = 1;
+    int nsm = 148;
+    int grid_spmv = 0, grid_stream = 0, grid_ritz = 0;
+    std::vector<int64_t> bounds;
+    std::vector<Part> parts;
+    Exch ex{};
+    char *exch_block = nullptr;
+    void *replica = nullptr;
+    SolveParams *dparams = nullptr, *hparams = nullptr;
+    double *jac_work = nullptr;
+    size_t jac_smem = 0;
+    int jac_threads = 32;
+    cudaGraphExec_t gexec = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ncclComm_t comm = nullptr;
+    bool sticky = false;
+    int64_t bytes_model = 0;
+    int64_t launches = 0;
+    int profile = 0;
+    bool capturing = false;
+    struct Prof { int cls; cudaEvent_t a, b; };
+    std::vector<Prof> prof;
+    size_t prof_next = 0;
+    void (*enqueue)(topk_eig_s *, bool) = nullptr;
+    void (*spmv_only)(topk_eig_s *, Part &) = nullptr;
+    std::vector<void *> allocs;
+
+    template <typename T> T *alloc(size_t count) {
+        void *p = nullptr;
+        size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+        CUDA_TRY(cudaMalloc(&p, bytes));
+        allocs.push_back(p);
+        CUDA_TRY(cudaMemsetAsync(p, 0, bytes, stream));
+        return reinterpret_cast<T *>(p);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// per-kernel-class event brackets (part 0 only); inside a capture they become
+// external event-record nodes of the graph
+static void prof_begin(topk_eig_s *h, const Part &p, int cls) {
+    if (!h->profile || &p != &h->parts[0]) return;
+    if (h->prof_next == h->prof.size()) {
+        topk_eig_s::Prof q{cls, nullptr, nullptr};
+        CUDA_TRY(cudaEventCreate(&q.a));
+        CUDA_TRY(cudaEventCreate(&q.b));
+        h->prof.push_back(q);
+    }
+    topk_eig_s::Prof &q = h->prof[h->prof_next];
+    q.cls = cls;
+    if (h->capturing) CUDA_TRY(cudaEventRecordWithFlags(q.a, h->stream, cudaEventRecordExternal));
+    else CUDA_TRY(cudaEventRecord(q.a, h->stream));
+}
+static void prof_end(topk_eig_s *h, const Part &p) {
+    if (!h->profile || &p != &h->parts[0]) return;
+    topk_eig_s::Prof &q = h->prof[h->prof_next++];
+    if (h->capturing) CUDA_TRY(cudaEventRecordWithFlags(q.b, h->stream, cudaEventRecordExternal));
+    else CUDA_TRY(cudaEventRecord(q.b, h->stream));
+}
+
+// ---------------------------------------------------------------------------
+// exchanges (no-ops in loopback: shared buffers on one stream)
+static void exch_vec_norm(topk_eig_s *h) {
+    if (!h->comm) return;
+    Part &p = h->parts[0];
+    size_t vb = (size_t)p.npad * dsize(h->vs);
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclAllGather((char *)h->replica + (size_t)h->rank * vb, h->replica, vb, ncclUint8, h->comm, h->stream));
+    NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
+    NCCL_TRY(ncclGroupEnd());
+}
+static void exch_norm(topk_eig_s *h) {
+    if (!h->comm) return;
+    NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
+}
+static void exch_alpha(topk_eig_s *h) {
+    if (!h->comm) return;
+    NCCL_TRY(ncclAllGather(h->ex.alpha_part + h->rank, h->ex.alpha_part, 1, ncclFloat64, h->comm, h->stream));
+}
+static void exch_h(topk_eig_s *h) {
+    if (!h->comm) return;
+    size_t ld = (size_t)h->m + 1;
+    NCCL_TRY(ncclAllGather(h->ex.hpart + h->rank * ld, h->ex.hpart, ld, ncclFloat64, h->comm, h->stream));
+}
+static void exch_ritz(topk_eig_s *h) {
+    if (!h->comm) return;
+    NCCL_TRY(ncclAllGather(h->ex.ritz_part + (size_t)h->rank * h->K, h->ex.ritz_part, h->K, ncclFloat64, h->comm, h->stream));
+}
+
+static void *rep_slot(topk_eig_s *h, Part &p) {
+    if (h->G == 1) return nullptr;
+    return (char *)h->replica + (size_t)p.g * p.npad * dsize(h->vs);
+}
+
+// ---------------------------------------------------------------------------
+template <typename VT, typename ST, typename CT>
+static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
+    SpmvArgs a;
+    a.rowptr = p.rowptr; a.col = p.col; a.val = p.val;
+    a.tiles = p.tiles; a.ntiles = p.ntiles;
+    a.longrows = p.longrows; a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
+    a.alpha_long = p.alpha_long; a.nlong = p.nlong;
+    const void *ucol = (const char *)p.V + (size_t)(it - 1) * p.npad * sizeof(ST);
+    a.x = (h->G == 1) ? ucol : h->replica;
+    a.ui = ucol;
+    a.y = p.y; a.y_dbg = y_dbg;
+    a.slots = p.slots; a.counter = p.counters + 1;
+    a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g;
+    prof_begin(h, p, 1);
+    k_spmv<VT, ST, CT><<<h->grid_spmv, kNT, 0, h->stream>>>(a, it);
+    CUDA_TRY(cudaGetLastError());
+    prof_end(h, p);
+    h->launches++;
+}
+
+template <typename ST, typename CT>
+static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
+    StepArgs a;
+    a.y = p.y; a.w = p.w; a.V = p.V;
+    a.vout = (char *)p.V + (size_t)it * p.npad * sizeof(ST);
+    a.rep_slot = (mode == 1) ? rep_slot(h, p) : nullptr;
+    a.npad = p.npad; a.ld = h->m + 1;
+    a.slots = p.slots; a.counter = p.counters + 2;
+    a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.mode = mode;
+    const int cols = it;
+    prof_begin(h, p, 2);
+    if (cols <= 8) k_step<ST, CT, 8><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
+    else if (cols <= 16) k_step<ST, CT, 16><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
+    else k_step<ST, CT, 32><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
+    CUDA_TRY(cudaGetLastError());
+    prof_end(h, p);
+    h->launches++;
+}
+
+template <typename ST, typename CT>
+static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
+    CorrArgs a;
+    a.w = p.w; a.V = p.V; a.rep_slot = rep_slot(h, p);
+    a.npad = p.npad; a.ld = h->m + 1;
+    a.slots = p.slots; a.counter = p.counters + 3;
+    a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
+    size_t smem = (size_t)(h->m + 1) * sizeof(double);
+    prof_begin(h, p, 3);
+    k_correct<ST, CT><<<h->grid_stream, kNT, smem, h->stream>>>(a, it);
+    CUDA_TRY(cudaGetLastError());
+    prof_end(h, p);
+    h->launches++;
+}
+
+template <typename VT, typename ST, typename CT>
+static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
+    // a5: v1
+    for (Part &p : h->parts) {
+        V1Args a;
+        a.u0 = p.V; a.rep_slot = rep_slot(h, p);
+        a.seed = &h->dparams->seed; a.use_v1 = &h->dparams->use_v1; a.v1 = p.v1buf;
+        a.row0 = p.row0; a.nrows = p.nrows; a.npad = p.npad;
+        a.slots = p.slots; a.counter = p.counters + 0;
+        a.st = p.st; a.ex = h->ex; a.g = p.g;
+        prof_begin(h, p, 0);
+        k_v1<ST, CT><<<h->grid_stream, kNT, 0, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+    exch_vec_norm(h);
+    for (int it = 1; it <= h->m; ++it) {
+        for (Part &p : h->parts) launch_spmv<VT, ST, CT>(h, p, it, nullptr);
+        exch_alpha(h);
+        if (h->reorth < 0) {
+            for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 1);
+            exch_vec_norm(h);
+            continue;
+        }
+        for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 0);
+        exch_h(h);
+        for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, -1);
+        if (h->reorth == 2) {
+            exch_norm(h);
+            for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 2);
+            exch_h(h);
+            for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it);
+        }
+        exch_vec_norm(h);
+    }
+    // a12-a13: Jacobi (redundant on every part, identical inputs)
+    for (Part &p : h->parts) {
+        JacArgs a;
+        a.st = p.st; a.ex = h->ex; a.G = h->G; a.m = h->m; a.K = h->K; a.max_sweeps = 50;
+        a.work = h->jac_work ? h->jac_work + (size_t)(&p - &h->parts[0]) * 2 * (h->m + 2) * (h->m + 2) + 0 : nullptr;
+        a.use_smem = h->jac_work ? 0 : 1;
+        prof_begin(h, p, 4);
+        k_jacobi<<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+    if (!want_vectors) return;
+    // a14: Ritz projection + normalisation
+    for (Part &p : h->parts) {
+        RitzArgs a;
+        a.V = p.V; a.Y = p.Y; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K;
+        a.slots = p.slots; a.counter = p.counters + 4;
+        a.st = p.st; a.ex = h->ex; a.g = p.g;
+        size_t smem = (size_t)h->m * h->K * sizeof(double);
+        prof_begin(h, p, 5);
+        if (h->K <= 8) k_ritz<ST, CT, 8><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
+        else if (h->K <= 16) k_ritz<ST, CT, 16><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
+        else k_ritz<ST, CT, 32><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+    exch_ritz(h);
+    for (Part &p : h->parts) {
+        RitzNormArgs a;
+        a.Y = p.Y; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K; a.G = h->G;
+        a.k_found = p.st.k_found; a.ritz_part = h->ex.ritz_part;
+        a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) + offsetof(SolveParams, out_ptr));
+        a.out_dtype = &h->dparams->out_dtype;
+        prof_begin(h, p, 6);
+        k_ritz_norm<<<h->grid_stream, kNT, 0, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+}
+
+template <typename VT, typename ST, typename CT>
+static void spmv_only(topk_eig_s *h, Part &p) {
+    launch_spmv<VT, ST, CT>(h, p, 1, p.y_dbg);
+}
+
+template <typename VT, typename ST, typename CT>
+static void set_kernels(topk_eig_s *h) {
+    h->enqueue = &enqueue_solve<VT, ST, CT>;
+    h->spmv_only = &spmv_only<VT, ST, CT>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT>, kNT, 0);
+    h->grid_spmv = h->nsm * std::max(1, occ);
+    int occ2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, 32>, kNT, 0);
+    h->grid_stream = h->nsm * std::max(1, std::min(occ2, 4));
+    h->grid_ritz = h->nsm * 2;
+    CUDA_TRY(cudaFuncSetAttribute(k_correct<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+}
+
+static bool select_kernels(topk_eig_s *h) {
+    using d = double;
+    using f = float;
+    if (h->ms == TOPK_F64 && h->vs == TOPK_F64 && h->cs == TOPK_F64) { set_kernels<d, d, d>(h); return true; }
+    if (h->ms == TOPK_F32 && h->vs == TOPK_F32 && h->cs == TOPK_F64) { set_kernels<f, f, d>(h); return true; }
+    if (h->ms == TOPK_F32 && h->vs == TOPK_F32 && h->cs == TOPK_F32) { set_kernels<f, f, f>(h); return true; }
+    if (h->ms == TOPK_BF16 && h->vs == TOPK_F32 && h->cs == TOPK_F64) { set_kernels<bf16, f, d>(h); return true; }
+    if (h->ms == TOPK_BF16 && h->vs == TOPK_BF16 && h->cs == TOPK_F64) { set_kernels<bf16, bf16, d>(h); return true; }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+static void carve_state(topk_eig_s *h, Part &p) {
+    const int m = h->m, K = h->K;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
+    size_t o_int = take(8 * sizeof(int));
+    size_t o_ts = take(sizeof(double));
+    size_t o_alpha = take((size_t)m * 8), o_beta = take((size_t)(m + 2) * 8), o_scale = take((size_t)(m + 1) * 8);
+    size_t o_theta = take((size_t)m * 8), o_evals = take((size_t)K * 8), o_resid = take((size_t)K * 8);
+    size_t o_coef = take((size_t)m * K * 8);
+    p.state_bytes = off;
+    p.state = h->alloc<char>(off);
+    p.hstate.assign(off, 0);
+    char *b = p.state;
+    int *ints = reinterpret_cast<int *>(b + o_int);
+    p.st.done = ints + 0;
+    p.st.m_found = ints + 1;
+    p.st.k_found = ints + 2;
+    p.st.jac_sweeps = ints + 3;
+    p.st.jac_conv = ints + 4;
+    p.st.tscale = reinterpret_cast<double *>(b + o_ts);
+    p.st.alpha = reinterpret_cast<double *>(b + o_alpha);
+    p.st.beta = reinterpret_cast<double *>(b + o_beta);
+    p.st.scale = reinterpret_cast<double *>(b + o_scale);
+    p.st.theta_all = reinterpret_cast<double *>(b + o_theta);
+    p.st.evals = reinterpret_cast<double *>(b + o_evals);
+    p.st.resid = reinterpret_cast<double *>(b + o_resid);
+    p.st.coefS = reinterpret_cast<double *>(b + o_coef);
+    p.st.tau = h->tau;
+}
+
+template <typename T> static T hget(const Part &p, const void *devptr) {
+    T v;
+    std::memcpy(&v, p.hstate.data() + ((const char *)devptr - p.state), sizeof(T));
+    return v;
+}
+static const double *hptr(const Part &p, const double *devptr) {
+    return reinterpret_cast<const double *>(p.hstate.data() + ((const char *)devptr - p.state));
+}
+
+static void upload_values(topk_eig_s *h, Part &p, const PartLayout &L) {
+    const size_t z = L.val.size();
+    if (h->ms == TOPK_F64) {
+        CUDA_TRY(cudaMemcpy(p.val, L.val.data(), z * 8, cudaMemcpyHostToDevice));
+    } else if (h->ms == TOPK_F32) {
+        std::vector<float> t(z);
+        for (size_t k = 0; k < z; ++k) t[k] = round_f32(L.val[k]);
+        CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 4, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<uint16_t> t(z);
+        for (size_t k = 0; k < z; ++k) t[k] = round_bf16_bits(L.val[k]);
+        CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 2, cudaMemcpyHostToDevice));
+    }
+}
+
+static int64_t model_bytes(topk_eig_s *h, const Part &p) {
+    // B_spmv = z(4+s_v) + 4(n_g+1) + s n_x + s n_g; B_step(i) = (2i+4) n_g s;
+    // Ritz: (m + 3K) n_g s. Per part, whole solve.
+    const int64_t s = (int64_t)dsize(h->vs), sv = (int64_t)dsize(h->ms);
+    const int64_t nx = (h->G == 1) ? p.nrows : h->n;
+    int64_t b = 0;
+    for (int i = 1; i <= h->m; ++i) {
+        b += p.nnz * (4 + sv) + 4 * (p.nrows + 1) + s * nx + s * p.nrows;
+        b += (h->reorth < 0) ? 4 * p.nrows * s : (2 * i + 4) * p.nrows * s;
+    }
+    b += (int64_t)(h->m + 3 * h->K) * p.nrows * s;
+    return b;
+}
+
+static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_t K,
+                                 topk_dtype_t storage, topk_dtype_t compute,
+                                 const topk_eig_opts_t *opts) {
+    if (!out || !A) return fail(TOPK_E_INVALID, "out and A must be non-NULL");
+    *out = nullptr;
+    topk_eig_opts_t o{};
+    if (opts) std::memcpy(&o, opts, std::min<size_t>(sizeof(o), opts->struct_size ? opts->struct_size : sizeof(o)));
+    const int64_t n = A->n;
+    if (n < 1 || n >= (1ll << 31)) return fail(TOPK_E_INVALID, "n must be in [1, 2^31)");
+    const int m = o.krylov_dim > 0 ? o.krylov_dim : K;
+    if (K < 1 || K > n || K > 256) return fail(TOPK_E_INVALID, "K must be in [1, min(n, 256)]");
+    if (m < K || m > n || m > 1024) return fail(TOPK_E_INVALID, "krylov_dim must be in [K, min(n, 1024)]");
+    const int world = o.world > 1 ? o.world : 1;
+    const int G = o.num_parts > 0 ? o.num_parts : world;
+    if (world > 1 && (G != world || o.rank < 0 || o.rank >= world || !o.nccl_id))
+        return fail(TOPK_E_INVALID, "multi-process: num_parts must equal world, 0 <= rank < world, nccl_id non-NULL");
+    if (G < 1 || G > 64 || G > n) return fail(TOPK_E_INVALID, "num_parts must be in [1, min(n, 64)]");
+    topk_dtype_t ms = (o.values_storage > 0) ? (topk_dtype_t)o.values_storage : storage;
+    if (storage < TOPK_F64 || storage > TOPK_BF16 || compute < TOPK_F64 || compute > TOPK_F32 || ms < TOPK_F64 || ms > TOPK_BF16)
+        return fail(TOPK_E_INVALID, "bad dtype");
+
+    std::unique_ptr<topk_eig_s> h(new topk_eig_s());
+    h->n = n; h->K = K; h->m = m; h->G = G; h->world = world; h->rank = world > 1 ? o.rank : 0;
+    h->vs = storage; h->ms = ms; h->cs = compute;
+    h->reorth = o.reorth == 0 ? 1 : o.reorth;
+    if (h->reorth != 1 && h->reorth != 2 && h->reorth != -1) return fail(TOPK_E_INVALID, "reorth must be 1, 2 or -1");
+    h->tau = o.breakdown_tol > 0 ? o.breakdown_tol : (storage == TOPK_F64 ? 1e-12 : storage == TOPK_F32 ? 1e-6 : 1e-3);
+    if (compute == TOPK_F32 && storage == TOPK_F64) return fail(TOPK_E_INVALID, "compute must be at least as precise as storage");
+    h->use_graph = o.use_graph >= 0;
+    h->profile = o.profile > 0;
+    h->device = o.device;
+
+    // a1-a3 on the host
+    Csr csr;
+    std::string err;
+    topk_status_t s = canonicalize(*A, csr, err);
+    if (s != TOPK_OK) return fail(s, err);
+    if (o.check_symmetry >= 0 && !is_symmetric(csr)) return fail(TOPK_E_NOT_SYMMETRIC, "matrix is not symmetric");
+    h->bounds.resize((size_t)G + 1);
+    s = partition_rule_p(csr.rowptr.data(), n, G, h->bounds.data());
+    if (s != TOPK_OK) return fail(s, "partition failed");
+    const int64_t npad = padded_rows(h->bounds.data(), G);
+
+    // device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(TOPK_E_NODEVICE, "no CUDA device: this library runs only on sm_100 (B200); there is no CPU fallback");
+    if (h->device < 0 || h->device >= ndev) return fail(TOPK_E_INVALID, "bad device ordinal");
+    try {
+        CUDA_TRY(cudaSetDevice(h->device));
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, h->device));
+        if (prop.major != 10 || prop.minor != 0)
+            return fail(TOPK_E_NODEVICE, "device is not sm_100 (B200); this library is built for sm_100a only");
+        h->nsm = prop.multiProcessorCount;
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreate(&h->ev0));
+        CUDA_TRY(cudaEventCreate(&h->ev1));
+        if (!select_kernels(h.get())) return fail(TOPK_E_INVALID, "unsupported (values, storage, compute) dtype combination");
+
+        // exchange buffers (shared by the local parts)
+        h->ex.alpha_part = h->alloc<double>((size_t)G);
+        h->ex.norm_part = h->alloc<double>((size_t)G);
+        h->ex.hpart = h->alloc<double>((size_t)G * (m + 1));
+        h->ex.ritz_part = h->alloc<double>((size_t)G * K);
+        if (G > 1) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
+        h->ex.replica = h->replica;
+        const int nlocal = (world > 1) ? 1 : G;
+        h->dparams = h->alloc<SolveParams>(1 + (size_t)nlocal);
+        CUDA_TRY(cudaMallocHost(&h->hparams, sizeof(SolveParams) * (1 + nlocal)));
+        std::memset(h->hparams, 0, sizeof(SolveParams) * (1 + nlocal));
+        // Jacobi workspace
+        const int M = m + (m & 1);
+        size_t jbytes = (size_t)2 * M * M * 8 + (size_t)(M / 2 + 2) * 4 + (size_t)(M / 2 + 1) * 16 + 64;
+        h->jac_threads = (M <= 48) ? 32 : 256;
+        if (jbytes <= 200 * 1024) {
+            h->jac_smem = jbytes;
+            CUDA_TRY(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
+        } else {
+            h->jac_smem = 0;
+            h->jac_work = h->alloc<double>((size_t)nlocal * 2 * (m + 2) * (m + 2) + 1024);
+        }
+
+        h->parts.resize((size_t)nlocal);
+        for (int lp = 0; lp < nlocal; ++lp) {
+            Part &p = h->parts[(size_t)lp];
+            p.g = (world > 1) ? h->rank : lp;
+            PartLayout L;
+            s = build_part(csr, h->bounds.data(), G, p.g, npad, L, err);
+            if (s != TOPK_OK) return fail(s, err);
+            p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.col.size();
+            p.ntiles = (int)L.tiles.size(); p.nlong = (int)L.longrows.size();
+            p.rowptr = h->alloc<int32_t>(L.rowptr.size());
+            p.col = h->alloc<int32_t>(L.col.size());
+            p.val = h->alloc<char>(L.val.size() * dsize(ms));
+            p.tiles = h->alloc<Tile>(L.tiles.size());
+            p.longrows = h->alloc<LongRow>(L.longrows.size());
+            p.long_parts = h->alloc<double>(L.tiles.size());
+            p.long_cnt = h->alloc<unsigned>(L.longrows.size());
+            p.alpha_long = h->alloc<double>(L.longrows.size());
+            CUDA_TRY(cudaStreamSynchronize(h->stream));
+            CUDA_TRY(cudaMemcpy(p.rowptr, L.rowptr.data(), L.rowptr.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(p.col, L.col.data(), L.col.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.tiles.empty()) CUDA_TRY(cudaMemcpy(p.tiles, L.tiles.data(), L.tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+            if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
+            upload_values(h.get(), p, L);
+            const size_t vsz = dsize(storage);
+            p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
+            p.y = h->alloc<char>((size_t)npad * vsz);
+            p.w = h->alloc<char>((size_t)npad * vsz);
+            p.Y = h->alloc<double>((size_t)K * npad);
+            p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
+            p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
+            p.slots = h->alloc<double>((size_t)std::max(h->grid_spmv, std::max(h->grid_stream, h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
+            p.counters = h->alloc<unsigned>(8);
+            carve_state(h.get(), p);
+            h->bytes_model += model_bytes(h.get(), p);
+        }
+        if (world > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, o.nccl_id, sizeof(id));
+            NCCL_TRY(ncclCommInitRank(&h->comm, world, id, h->rank));
+        }
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+    } catch (CudaFail &e) {
+        return fail(TOPK_E_CUDA, e.msg);
+    } catch (NcclFail &e) {
+        return fail(TOPK_E_NCCL, e.msg);
+    } catch (std::bad_alloc &) {
+        return fail(TOPK_E_NOMEM, "host allocation failed");
+    }
+    *out = h.release();
+    return TOPK_OK;
+}
+
+static void free_handle(topk_eig_s *h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->comm) ncclCommDestroy(h->comm);
+    for (void *p : h->allocs) cudaFree(p);
+    if (h->hparams) cudaFreeHost(h->hparams);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    for (auto &q : h->prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+// Enqueue one full solve on h->stream (graph replay or eager launches).
+static void enqueue(topk_eig_s *h, uint64_t seed, const double *v1_host, void *const *out_ptrs, int out_dtype) {
+    const int nl = (int)h->parts.size();
+    h->hparams[0].seed = seed;
+    h->hparams[0].use_v1 = v1_host ? 1 : 0;
+    h->hparams[0].out_dtype = out_dtype;
+    for (int lp = 0; lp < nl; ++lp) h->hparams[1 + lp].out_ptr = out_ptrs ? out_ptrs[lp] : nullptr;
+    CUDA_TRY(cudaMemcpyAsync(h->dparams, h->hparams, sizeof(SolveParams) * (1 + nl), cudaMemcpyHostToDevice, h->stream));
+    if (v1_host)
+        for (Part &p : h->parts)
+            CUDA_TRY(cudaMemcpyAsync(p.v1buf, v1_host + p.row0, (size_t)p.nrows * 8, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+    if (h->use_graph) {
+        if (!h->gexec) {
+            cudaGraph_t graph;
+            int64_t l0 = h->launches;
+            CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+            h->capturing = true;
+            h->prof_next = 0;
+            try {
+                h->enqueue(h, true);
+            } catch (...) {
+                h->capturing = false;
+                cudaStreamEndCapture(h->stream, &graph);
+                throw;
+            }
+            h->capturing = false;
+            CUDA_TRY(cudaStreamEndCapture(h->stream, &graph));
+            CUDA_TRY(cudaGraphInstantiate(&h->gexec, graph, 0));
+            CUDA_TRY(cudaGraphDestroy(graph));
+            h->launches = h->launches - l0;  // kernels per solve
+        }
+        CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+    } else {
+        int64_t l0 = h->launches;
+        h->prof_next = 0;
+        h->enqueue(h, true);
+        h->launches = h->launches - l0;
+    }
+    CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+    for (Part &p : h->parts)
+        CUDA_TRY(cudaMemcpyAsync(p.hstate.data(), p.state, p.state_bytes, cudaMemcpyDeviceToHost, h->stream));
+}
+
+static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
+    if (!info) return;
+    const Part &p = h->parts[0];
+    std::memset(info, 0, sizeof(*info));
+    info->iterations = hget<int>(p, p.st.m_found);
+    info->k_found = hget<int>(p, p.st.k_found);
+    info->breakdown = hget<int>(p, p.st.done);
+    info->jacobi_sweeps = hget<int>(p, p.st.jac_sweeps);
+    info->jacobi_converged = hget<int>(p, p.st.jac_conv);
+    info->num_parts = h->G;
+    info->beta_next = hptr(p, p.st.beta)[info->iterations];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    info->ms_solve = ms;
+    info->bytes_model = h->bytes_model;
+    info->gpu_launches = h->launches;
+}
+
+#define GUARD(h)                                                                   \
+    if (!(h)) return fail(TOPK_E_INVALID, "NULL handle");                          \
+    if ((h)->sticky) return fail(TOPK_E_STATE, "handle is in a failed state");    \
+    if (cudaSetDevice((h)->device) != cudaSuccess) return fail(TOPK_E_CUDA, "cudaSetDevice failed");
+
+#define CATCH(h)                                                                   \
+    catch (CudaFail & e) { (h)->sticky = true; return fail(TOPK_E_CUDA, e.msg); }  \
+    catch (NcclFail & e) { (h)->sticky = true; return fail(TOPK_E_NCCL, e.msg); }  \
+    catch (std::bad_alloc &) { return fail(TOPK_E_NOMEM, "host allocation failed"); }
+
+extern "C" {
+
+topk_status_t topk_eig_create(topk_eig_t *out, const topk_matrix_t *A, int32_t K, topk_dtype_t storage,
+                              topk_dtype_t compute, const topk_eig_opts_t *opts) {
+    try {
+        return create_impl(out, A, K, storage, compute, opts);
+    } catch (std::bad_alloc &) {
+        return fail(TOPK_E_NOMEM, "host allocation failed");
+    } catch (...) {
+        return fail(TOPK_E_INVALID, "unexpected exception in create");
+    }
+}
+
+topk_status_t topk_eig_solve(topk_eig_t h, uint64_t seed, const double *v1, double *eigenvalues, void *eigenvectors,
+                             topk_dtype_t vec_dtype, double *residual_est, topk_eig_info_t *info) {
+    GUARD(h);
+    if (!eigenvalues) return fail(TOPK_E_INVALID, "eigenvalues must be non-NULL");
+    if (eigenvectors && vec_dtype != TOPK_F64 && vec_dtype != TOPK_F32) return fail(TOPK_E_INVALID, "vec_dtype must be F64 or F32");
+    try {
+        std::vector<void *> outs;
+        for (Part &p : h->parts) outs.push_back(eigenvectors ? p.out : nullptr);
+        enqueue(h, seed, v1, outs.data(), vec_dtype == TOPK_F32 ? 1 : 0);
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        const Part &p0 = h->parts[0];
+        const int kf = hget<int>(p0, p0.st.k_found);
+        std::memcpy(eigenvalues, hptr(p0, p0.st.evals), (size_t)h->K * 8);
+        if (residual_est) std::memcpy(residual_est, hptr(p0, p0.st.resid), (size_t)h->K * 8);
+        if (eigenvectors) {
+            const size_t es = vec_dtype == TOPK_F32 ? 4 : 8;
+            for (Part &p : h->parts) {
+                if (p.nrows == 0 || kf == 0) continue;
+                CUDA_TRY(cudaMemcpy2DAsync((char *)eigenvectors + (size_t)p.row0 * es, (size_t)h->n * es, p.out,
+                                           (size_t)p.nrows * es, (size_t)p.nrows * es, (size_t)kf, cudaMemcpyDeviceToHost,
+                                           h->stream));
+            }
+            CUDA_TRY(cudaStreamSynchronize(h->stream));
+        }
+        fill_info(h, info);
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_solve_async(topk_eig_t h, uint64_t seed, double *eigenvalues_dev, void *eigenvectors_dev,
+                                   topk_dtype_t vec_dtype) {
+    GUARD(h);
+    if (h->parts.size() != 1 && eigenvectors_dev)
+        return fail(TOPK_E_INVALID, "solve_async with eigenvectors needs one local part (G = 1 or multi-process)");
+    try {
+        void *outs[1] = {eigenvectors_dev};
+        std::vector<void *> o(h->parts.size(), nullptr);
+        if (eigenvectors_dev) o[0] = outs[0];
+        enqueue(h, seed, nullptr, o.data(), vec_dtype == TOPK_F32 ? 1 : 0);
+        if (eigenvalues_dev)
+            CUDA_TRY(cudaMemcpyAsync(eigenvalues_dev, h->parts[0].st.evals, (size_t)h->K * 8, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_sync(topk_eig_t h, topk_eig_info_t *info) {
+    GUARD(h);
+    try {
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        fill_info(h, info);
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_kernel_times(topk_eig_t h, double *ms, int32_t *launches) {
+    GUARD(h);
+    if (!ms || !launches) return fail(TOPK_E_INVALID, "NULL argument");
+    if (!h->profile) return fail(TOPK_E_STATE, "create the handle with opts.profile = 1");
+    for (int c = 0; c < 8; ++c) { ms[c] = 0.0; launches[c] = 0; }
+    try {
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        for (size_t i = 0; i < h->prof_next && i < h->prof.size(); ++i) {
+            float t = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&t, h->prof[i].a, h->prof[i].b));
+            ms[h->prof[i].cls] += t;
+            launches[h->prof[i].cls] += 1;
+        }
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+void *topk_eig_stream(topk_eig_t h) { return h ? (void *)h->stream : nullptr; }
+
+void topk_eig_destroy(topk_eig_t h) { free_handle(h); }
+
+const char *topk_eig_last_error(void) { return g_last_error.c_str(); }
+
+topk_status_t topk_eig_nccl_id(void *out128) {
+    if (!out128) return fail(TOPK_E_INVALID, "NULL out");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(TOPK_E_NCCL, ncclGetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t G, int64_t *boundaries) {
+    if (!row_ptr || !boundaries || n < 1) return fail(TOPK_E_INVALID, "bad arguments");
+    for (int64_t r = 0; r < n; ++r)
+        if (row_ptr[r + 1] < row_ptr[r]) return fail(TOPK_E_STRUCTURE, "row_ptr not monotone");
+    topk_status_t s = partition_rule_p(row_ptr, n, G, boundaries);
+    if (s != TOPK_OK) return fail(s, "G must be in [1, n]");
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries) {
+    if (!h || !boundaries) return fail(TOPK_E_INVALID, "NULL argument");
+    std::memcpy(boundaries, h->bounds.data(), h->bounds.size() * 8);
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr, int32_t *col, double *val,
+                                     int64_t *n_pad, int64_t *n_rows, int64_t *nnz) {
+    GUARD(h);
+    if (part < 0 || part >= (int)h->parts.size()) return fail(TOPK_E_INVALID, "bad part");
+    Part &p = h->parts[(size_t)part];
+    if (n_pad) *n_pad = p.npad;
+    if (n_rows) *n_rows = p.nrows;
+    if (nnz) *nnz = p.nnz;
+    try {
+        if (rowptr) {
+            std::vector<int32_t> t((size_t)p.nrows + 1);
+            CUDA_TRY(cudaMemcpy(t.data(), p.rowptr, t.size() * 4, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < t.size(); ++i) rowptr[i] = t[i];
+        }
+        if (col) CUDA_TRY(cudaMemcpy(col, p.col, (size_t)p.nnz * 4, cudaMemcpyDeviceToHost));
+        if (val) {
+            const size_t z = (size_t)p.nnz;
+            if (h->ms == TOPK_F64) {
+                CUDA_TRY(cudaMemcpy(val, p.val, z * 8, cudaMemcpyDeviceToHost));
+            } else if (h->ms == TOPK_F32) {
+                std::vector<float> t(z);
+                CUDA_TRY(cudaMemcpy(t.data(), p.val, z * 4, cudaMemcpyDeviceToHost));
+                for (size_t k = 0; k < z; ++k) val[k] = t[k];
+            } else {
+                std::vector<uint16_t> t(z);
+                CUDA_TRY(cudaMemcpy(t.data(), p.val, z * 2, cudaMemcpyDeviceToHost));
+                for (size_t k = 0; k < z; ++k) val[k] = bf16_bits_to_double(t[k]);
+            }
+        }
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_export_tridiag(topk_eig_t h, double *alpha, double *beta, double *theta_all,
+                                      int32_t *m_found) {
+    GUARD(h);
+    const Part &p = h->parts[0];
+    const int mm = hget<int>(p, p.st.m_found);
+    if (m_found) *m_found = mm;
+    if (alpha) std::memcpy(alpha, hptr(p, p.st.alpha), (size_t)mm * 8);
+    if (beta) std::memcpy(beta, hptr(p, p.st.beta), (size_t)(mm + 1) * 8);
+    if (theta_all) std::memcpy(theta_all, hptr(p, p.st.theta_all), (size_t)mm * 8);
+    return TOPK_OK;
+}
+
+static double to_double_elem(const char *base, size_t idx, topk_dtype_t t) {
+    if (t == TOPK_F64) return reinterpret_cast<const double *>(base)[idx];
+    if (t == TOPK_F32) return reinterpret_cast<const float *>(base)[idx];
+    return bf16_bits_to_double(reinterpret_cast<const uint16_t *>(base)[idx]);
+}
+
+topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32_t *ncols) {
+    GUARD(h);
+    if (part < 0 || part >= (int)h->parts.size()) return fail(TOPK_E_INVALID, "bad part");
+    Part &p = h->parts[(size_t)part];
+    const int mm = hget<int>(p, p.st.m_found);
+    const int brk = hget<int>(p, p.st.done);
+    const int nc = brk ? mm : mm + 1;
+    if (ncols) *ncols = nc;
+    if (!V) return TOPK_OK;
+    try {
+        const size_t es = dsize(h->vs);
+        std::vector<char> t((size_t)nc * p.npad * es);
+        CUDA_TRY(cudaMemcpy(t.data(), p.V, t.size(), cudaMemcpyDeviceToHost));
+        const double *sc = hptr(p, p.st.scale);
+        const double *bt = hptr(p, p.st.beta);
+        for (int j = 0; j < nc; ++j) {
+            const double s = (j < mm) ? sc[j] : 1.0 / bt[mm];
+            for (int64_t r = 0; r < p.nrows; ++r)
+                V[(size_t)j * p.nrows + r] = s * to_double_elem(t.data(), (size_t)j * p.npad + r, h->vs);
+        }
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
+    GUARD(h);
+    if (!x || !y) return fail(TOPK_E_INVALID, "NULL argument");
+    try {
+        const size_t es = dsize(h->vs);
+        // x rounded to the storage dtype into V column 0 (and the replica)
+        std::vector<double> norm((size_t)h->G, 0.0);
+        norm[0] = 1.0;  // sum of partials = 1 -> s_1 = 1
+        CUDA_TRY(cudaMemcpyAsync(h->ex.norm_part, norm.data(), norm.size() * 8, cudaMemcpyHostToDevice, h->stream));
+        for (Part &p : h->parts) {
+            std::vector<char> buf((size_t)p.npad * es, 0);
+            for (int64_t r = 0; r < p.nrows; ++r) {
+                const double v = x[p.row0 + r];
+                if (h->vs == TOPK_F64) reinterpret_cast<double *>(buf.data())[r] = v;
+                else if (h->vs == TOPK_F32) reinterpret_cast<float *>(buf.data())[r] = round_f32(v);
+                else reinterpret_cast<uint16_t *>(buf.data())[r] = round_bf16_bits(v);
+            }
+            CUDA_TRY(cudaMemcpy(p.V, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+            if (h->G > 1 && h->comm == nullptr)
+                CUDA_TRY(cudaMemcpy(rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
+            if (h->comm) CUDA_TRY(cudaMemcpy(rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemsetAsync(p.st.done, 0, sizeof(int), h->stream));
+            CUDA_TRY(cudaMemsetAsync(p.st.tscale, 0, sizeof(double), h->stream));
+            if (!p.y_dbg) p.y_dbg = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
+        }
+        if (h->comm) exch_vec_norm(h);
+        for (Part &p : h->parts) h->spmv_only(h, p);
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        for (Part &p : h->parts)
+            CUDA_TRY(cudaMemcpy(y + p.row0, p.y_dbg, (size_t)p.nrows * 8, cudaMemcpyDeviceToHost));
+    }
+    CATCH(h)
+    return TOPK_OK;
+}
+
+}  // extern "C"
