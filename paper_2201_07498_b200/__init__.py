@@ -75,6 +75,7 @@ _SIGS = {
     "topk_eig_last_error": (ctypes.c_char_p, []),
     "topk_eig_nccl_id": (_S, [_P]),
     "topk_eig_plan_partition": (_S, [_P, _I64, _I32, _P]),
+    "topk_eig_plan_layout": (_S, [_P, _I32, _I32, _S, _S, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "topk_eig_export_partition": (_S, [_P, _P]),
     "topk_eig_export_layout": (_S, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "topk_eig_export_tridiag": (_S, [_P, _P, _P, _P, _P]),
@@ -110,6 +111,50 @@ def plan_partition(rowptr, G: int) -> np.ndarray:
     return b
 
 
+def _matrix(A, keep: list) -> "_Matrix":
+    mat = _Matrix()
+    mat.n = int(A.n)
+    if hasattr(A, "rowptr"):
+        rp = np.ascontiguousarray(A.rowptr, dtype=np.int64)
+        keep.append(rp)
+        mat.format, mat.row_ptr = 0, rp.ctypes.data
+        mat.nnz = int(rp[-1])
+    else:
+        ri = np.ascontiguousarray(A.row, dtype=np.int64)
+        keep.append(ri)
+        mat.format, mat.row_idx = 1, ri.ctypes.data
+        mat.nnz = len(ri)
+    col = np.ascontiguousarray(A.col, dtype=np.int32)
+    keep.append(col)
+    mat.col_idx = col.ctypes.data
+    if A.val is not None:
+        val = np.ascontiguousarray(A.val)
+        if val.dtype not in (np.float64, np.float32):
+            val = val.astype(np.float64)
+        keep.append(val)
+        mat.values = val.ctypes.data
+        mat.values_dtype = DTYPES["f32"] if val.dtype == np.float32 else DTYPES["f64"]
+    return mat
+
+
+def plan_layout(A, G: int, g: int, storage: str = "f64", values_storage: str | None = None):
+    """Host-only layout of part g of G (no device): (rowptr, col, val, n_pad, tiles, perm)."""
+    keep = []
+    mat = _matrix(A, keep)
+    npad, nr, nz, nt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    st, vs = DTYPES[storage], DTYPES[values_storage or storage]
+    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, ctypes.byref(npad), ctypes.byref(nr),
+                                     ctypes.byref(nz), ctypes.byref(nt), None, None, None, None, None))
+    rp = np.zeros(nr.value + 1, np.int64)
+    c = np.zeros(max(nz.value, 1), np.int32)
+    v = np.zeros(max(nz.value, 1), np.float64)
+    t = np.zeros((max(nt.value, 1), 4), np.int32)
+    pm = np.zeros(max(nr.value, 1), np.int32)
+    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, None, None, None, None,
+                                     _ptr(rp), _ptr(c), _ptr(v), _ptr(t), _ptr(pm)))
+    return rp, c[:nz.value], v[:nz.value], npad.value, t[:nt.value], pm[:nr.value]
+
+
 @dataclass
 class Result:
     eigenvalues: np.ndarray
@@ -133,29 +178,8 @@ class TopkEig:
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
-        mat = _Matrix()
-        mat.n = self.n
         keep = []
-        if hasattr(A, "rowptr"):
-            rp = np.ascontiguousarray(A.rowptr, dtype=np.int64)
-            keep.append(rp)
-            mat.format, mat.row_ptr = 0, rp.ctypes.data
-            mat.nnz = int(rp[-1])
-        else:
-            ri = np.ascontiguousarray(A.row, dtype=np.int64)
-            keep.append(ri)
-            mat.format, mat.row_idx = 1, ri.ctypes.data
-            mat.nnz = len(ri)
-        col = np.ascontiguousarray(A.col, dtype=np.int32)
-        keep.append(col)
-        mat.col_idx = col.ctypes.data
-        if A.val is not None:
-            val = np.ascontiguousarray(A.val)
-            if val.dtype not in (np.float64, np.float32):
-                val = val.astype(np.float64)
-            keep.append(val)
-            mat.values = val.ctypes.data
-            mat.values_dtype = DTYPES["f32"] if val.dtype == np.float32 else DTYPES["f64"]
+        mat = _matrix(A, keep)
         o = _Opts()
         o.struct_size = ctypes.sizeof(_Opts)
         o.krylov_dim = int(m or 0)
@@ -201,7 +225,7 @@ class TopkEig:
         _check(_lib.topk_eig_sync(self._h, ctypes.byref(info)))
         return info.as_dict()
 
-    KERNEL_CLASSES = ("v1", "spmv", "step", "correct", "jacobi", "ritz", "ritz_norm")
+    KERNEL_CLASSES = ("v1", "spmv", "step", "correct", "jacobi", "ritz_norms", "ritz_out")
 
     def kernel_times(self) -> dict:
         """{class: (total ms, launches)} of the last solve (profile=True)."""

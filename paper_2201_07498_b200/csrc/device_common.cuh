@@ -71,6 +71,72 @@ __device__ __forceinline__ void vstore_back(ST *__restrict__ p, CT (&v)[Vw<ST>::
     *reinterpret_cast<uint4 *>(p) = raw;
 }
 
+// round to the storage dtype and back (the value vstore_back would store)
+template <typename ST, typename CT>
+__device__ __forceinline__ void round_back(CT (&v)[Vw<ST>::N]) {
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) v[q] = cvt<CT>(rnd_ct<ST, CT>(v[q]));
+}
+
+// ---- L1 cache-policy loads (read-only path) ----------------------------------
+// stream: data read exactly once per kernel (matrix col/val) must not displace
+// the x values kept in L1 -> L1::no_allocate. Gathers: hot columns evict-last,
+// the rest no_allocate (SpMV).
+__device__ __forceinline__ int4 ld_stream(const int4 *p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2 *p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+template <typename T> __device__ __forceinline__ T ld_keep(const T *p);
+template <typename T> __device__ __forceinline__ T ld_noalloc(const T *p);
+template <> __device__ __forceinline__ float ld_keep<float>(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+template <> __device__ __forceinline__ float ld_noalloc<float>(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+template <> __device__ __forceinline__ double ld_keep<double>(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <> __device__ __forceinline__ double ld_noalloc<double>(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <> __device__ __forceinline__ bf16 ld_keep<bf16>(const bf16 *p) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::evict_last.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    return __ushort_as_bfloat16(v);
+}
+template <> __device__ __forceinline__ bf16 ld_noalloc<bf16>(const bf16 *p) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    return __ushort_as_bfloat16(v);
+}
+
 // ---- deterministic reductions (fixed shuffle tree + fixed warp order) --------
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -104,14 +170,17 @@ __device__ __forceinline__ T block_sum_array(const T *a, int n, int stride, T *s
 // Classic threadfence "last block" pattern: every block publishes its partial,
 // then the block that arrives last (atomic ticket) reduces all partials in a
 // fixed order; it resets the ticket for the next launch (graph replays).
-__device__ __forceinline__ bool arrive_last(unsigned *counter, int *sflag) {
+__device__ __forceinline__ bool arrive_last_n(unsigned *counter, unsigned nblocks, int *sflag) {
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *sflag = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    if (threadIdx.x == 0) *sflag = (atomicAdd(counter, 1u) == nblocks - 1);
     __syncthreads();
     const bool last = *sflag;
     if (last) __threadfence();
     return last;
+}
+__device__ __forceinline__ bool arrive_last(unsigned *counter, int *sflag) {
+    return arrive_last_n(counter, gridDim.x, sflag);
 }
 
 // ---- counter-based start vector (reading Q8) ---------------------------------

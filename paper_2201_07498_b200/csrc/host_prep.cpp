@@ -57,13 +57,41 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
     if (A.values && A.values_dtype != TOPK_F64 && A.values_dtype != TOPK_F32) {
         err = "values_dtype must be TOPK_F64 or TOPK_F32"; return TOPK_E_INVALID;
     }
+    int bad_col = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad_col)
     for (int64_t k = 0; k < nnz; ++k)
-        if (A.col_idx[k] < 0 || (int64_t)A.col_idx[k] >= n) { err = "column index out of range"; return TOPK_E_STRUCTURE; }
+        if (A.col_idx[k] < 0 || (int64_t)A.col_idx[k] >= n) bad_col = 1;
+    if (bad_col) { err = "column index out of range"; return TOPK_E_STRUCTURE; }
+    if (A.format == TOPK_CSR) {
+        if (!A.row_ptr) { err = "row_ptr is NULL"; return TOPK_E_INVALID; }
+        if (A.row_ptr[0] != 0 || A.row_ptr[n] != nnz) { err = "row_ptr[0] must be 0 and row_ptr[n] must be nnz"; return TOPK_E_STRUCTURE; }
+        for (int64_t r = 0; r < n; ++r)
+            if (A.row_ptr[r + 1] < A.row_ptr[r]) { err = "row_ptr is not non-decreasing"; return TOPK_E_STRUCTURE; }
+        // fast path: columns already strictly increasing in every row (canonical
+        // input) -> one parallel copy, no regrouping
+        int unsorted = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : unsorted)
+        for (int64_t r = 0; r < n; ++r)
+            for (int64_t k = A.row_ptr[r] + 1; k < A.row_ptr[r + 1]; ++k)
+                if (A.col_idx[k] <= A.col_idx[k - 1]) { unsorted = 1; break; }
+        if (!unsorted) {
+            out.n = n;
+            out.rowptr.assign(A.row_ptr, A.row_ptr + n + 1);
+            out.col.resize((size_t)nnz);
+            out.val.resize((size_t)nnz);
+#pragma omp parallel for schedule(static)
+            for (int64_t k = 0; k < nnz; ++k) {
+                out.col[(size_t)k] = A.col_idx[k];
+                out.val[(size_t)k] = load_value(A, k);
+            }
+            return TOPK_OK;
+        }
+    }
 
     // Gather entries grouped by row, preserving input order inside a row.
     std::vector<int64_t> start((size_t)n + 1, 0);
-    std::vector<int32_t> gcol((size_t)nnz);
-    std::vector<double> gval((size_t)nnz);
+    hvec<int32_t> gcol((size_t)nnz);
+    hvec<double> gval((size_t)nnz);
     if (A.format == TOPK_CSR) {
         if (!A.row_ptr) { err = "row_ptr is NULL"; return TOPK_E_INVALID; }
         if (A.row_ptr[0] != 0 || A.row_ptr[n] != nnz) { err = "row_ptr[0] must be 0 and row_ptr[n] must be nnz"; return TOPK_E_STRUCTURE; }
@@ -210,40 +238,111 @@ double bf16_bits_to_double(uint16_t b) {
     return (double)f;
 }
 
-static void build_tiles(const int32_t *rowptr, int64_t nrows, std::vector<Tile> &tiles,
-                        std::vector<LongRow> &longrows) {
-    tiles.clear();
-    longrows.clear();
-    int64_t r = 0;
-    while (r < nrows) {
-        int64_t len = rowptr[r + 1] - rowptr[r];
-        if (len > kTileNnz) {  // long row: fixed chunks
-            LongRow L;
-            L.row = (int32_t)r;
-            L.first_tile = (int32_t)tiles.size();
-            L.nchunks = (int32_t)((len + kTileNnz - 1) / kTileNnz);
-            L.pad = 0;
-            for (int32_t c = 0; c < L.nchunks; ++c)
-                tiles.push_back(Tile{(int32_t)r, (int32_t)(r + 1),
-                                     (int32_t)(rowptr[r] + (int64_t)c * kTileNnz),
-                                     (int32_t)longrows.size()});
-            longrows.push_back(L);
-            ++r;
+static void build_tiles(const int32_t *rowptr, int64_t nrows, PartLayout &L) {
+    L.tiles.clear();
+    L.longrows.clear();
+    L.nzrow.clear();
+    const int64_t z = rowptr[nrows];
+    L.endbits.assign((size_t)(z / 32 + 2), 0u);
+    for (int64_t r = 0; r < nrows; ++r)
+        if (rowptr[r + 1] > rowptr[r]) {
+            const int64_t e = rowptr[r + 1] - 1;
+            L.endbits[(size_t)(e >> 5)] |= 1u << (e & 31);
+            L.nzrow.push_back((int32_t)r);
+        }
+    const int64_t nz_rows = (int64_t)L.nzrow.size();
+    int64_t j = 0;  // index into nzrow
+    while (j < nz_rows) {
+        const int32_t r = L.nzrow[(size_t)j];
+        const int64_t len = rowptr[r + 1] - rowptr[r];
+        if (len > kTileNnz) {  // long row: fixed chunks, finished by the last-arriving chunk
+            LongRow lr;
+            lr.row = r;
+            lr.first_tile = (int32_t)L.tiles.size();
+            lr.nchunks = (int32_t)((len + kTileNnz - 1) / kTileNnz);
+            lr.pad = 0;
+            for (int32_t c = 0; c < lr.nchunks; ++c) {
+                const int64_t b = rowptr[r] + (int64_t)c * kTileNnz;
+                L.tiles.push_back(Tile{(int32_t)b, (int32_t)std::min<int64_t>(kTileNnz, rowptr[r + 1] - b),
+                                       (int32_t)j, (int32_t)L.longrows.size()});
+            }
+            L.longrows.push_back(lr);
+            ++j;
             continue;
         }
-        int64_t s = r;
-        while (r < nrows && r - s < kTileRows) {
-            int64_t l = rowptr[r + 1] - rowptr[r];
-            if (l > kTileNnz) break;
-            if (rowptr[r + 1] - rowptr[s] > kTileNnz) break;
-            ++r;
+        const int64_t j0 = j, zb = rowptr[r];
+        while (j < nz_rows) {
+            const int32_t q = L.nzrow[(size_t)j];
+            if (rowptr[q + 1] - rowptr[q] > kTileNnz) break;
+            if (rowptr[q + 1] - zb > kTileNnz) break;
+            ++j;
         }
-        tiles.push_back(Tile{(int32_t)s, (int32_t)r, rowptr[s], -1});
+        const int32_t last = L.nzrow[(size_t)j - 1];
+        L.tiles.push_back(Tile{(int32_t)zb, (int32_t)(rowptr[last + 1] - zb), (int32_t)j0, -1});
     }
 }
 
+std::vector<uint8_t> hot_columns(const Csr &m, int64_t H) {
+    const int64_t n = m.n;
+    std::vector<uint8_t> hot((size_t)n, 0);
+    if (H <= 0) return hot;
+    auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
+    std::vector<int64_t> idx;  // non-empty rows only: an empty row is never hot
+    idx.reserve((size_t)n);
+    for (int64_t r = 0; r < n; ++r)
+        if (deg(r) > 0) idx.push_back(r);
+    H = std::min<int64_t>(H, (int64_t)idx.size());
+    if (H <= 0) return hot;
+    std::nth_element(idx.begin(), idx.begin() + (H - 1), idx.end(), [&](int64_t a, int64_t b) {
+        const int64_t da = deg(a), db = deg(b);
+        return da != db ? da > db : a < b;
+    });
+    for (int64_t i = 0; i < H; ++i) hot[(size_t)idx[(size_t)i]] = 1;
+    return hot;
+}
+
+int64_t hot_count(int64_t n, int storage_bytes) {
+    return std::min<int64_t>(n, kHotBytes / std::max(1, storage_bytes));
+}
+
+void hub_first_order(const Csr &m, const int64_t *b, int32_t G, const uint8_t *hot,
+                     std::vector<int32_t> &pos) {
+    pos.assign((size_t)m.n, 0);
+    auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t q = 0; q < G; ++q) {
+        std::vector<int64_t> hr;
+        for (int64_t r = b[q]; r < b[q + 1]; ++r)
+            if (hot && hot[(size_t)r]) hr.push_back(r);
+        std::sort(hr.begin(), hr.end(), [&](int64_t x, int64_t y) {
+            const int64_t dx = deg(x), dy = deg(y);
+            return dx != dy ? dx > dy : x < y;
+        });
+        int32_t p = 0;
+        for (int64_t r : hr) pos[(size_t)r] = p++;
+        for (int64_t r = b[q]; r < b[q + 1]; ++r)
+            if (!(hot && hot[(size_t)r]) && deg(r) > 0) pos[(size_t)r] = p++;
+        for (int64_t r = b[q]; r < b[q + 1]; ++r)
+            if (deg(r) == 0) pos[(size_t)r] = p++;
+    }
+}
+
+std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const uint8_t *hot,
+                                const int32_t *pos) {
+    std::vector<int32_t> cm((size_t)n);
+    for (int32_t q = 0; q < G; ++q) {
+#pragma omp parallel for schedule(static)
+        for (int64_t c = b[q]; c < b[q + 1]; ++c) {
+            uint32_t cc = (uint32_t)(q * npad + pos[(size_t)c]);
+            if (hot && hot[(size_t)c]) cc |= kHotBit;
+            cm[(size_t)c] = (int32_t)cc;
+        }
+    }
+    return cm;
+}
+
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
-                         PartLayout &out, std::string &err) {
+                         const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
     const int64_t r0 = b[g], r1 = b[g + 1];
     const int64_t z0 = m.rowptr[(size_t)r0], z1 = m.rowptr[(size_t)r1];
     if (z1 - z0 >= (1ll << 31) - kTileNnz) { err = "per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
@@ -251,18 +350,29 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     out.row0 = r0;
     out.nrows = r1 - r0;
     out.npad = npad;
-    out.rowptr.resize((size_t)(r1 - r0 + 1));
-    for (int64_t r = r0; r <= r1; ++r) out.rowptr[(size_t)(r - r0)] = (int32_t)(m.rowptr[(size_t)r] - z0);
-    out.col.resize((size_t)(z1 - z0));
-    out.val.assign(m.val.begin() + z0, m.val.begin() + z1);
-    // column remap c -> owner(c) * npad + (c - b[owner]) (owner by binary search on b)
-#pragma omp parallel for schedule(static)
-    for (int64_t k = z0; k < z1; ++k) {
-        int64_t c = m.col[(size_t)k];
-        int32_t owner = (int32_t)(std::upper_bound(b, b + G + 1, c) - b) - 1;
-        out.col[(size_t)(k - z0)] = (int32_t)(owner * npad + (c - b[owner]));
+    const int64_t ng = r1 - r0;
+    out.perm.assign((size_t)ng, 0);
+    for (int64_t r = r0; r < r1; ++r) out.perm[(size_t)pos[(size_t)r]] = (int32_t)(r - r0);
+    out.rowptr.resize((size_t)(ng + 1));
+    out.rowptr[0] = 0;
+    for (int64_t p = 0; p < ng; ++p) {
+        const int64_t r = r0 + out.perm[(size_t)p];
+        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + (int32_t)(m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]);
     }
-    build_tiles(out.rowptr.data(), out.nrows, out.tiles, out.longrows);
+    out.col.resize((size_t)(z1 - z0));
+    out.val.resize((size_t)(z1 - z0));
+    // rows in hub-first order; entries of a row keep their (column-sorted) input
+    // order; column c -> owner(c) * npad + pos[c] (+ bit 31 if hot)
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t p = 0; p < ng; ++p) {
+        const int64_t r = r0 + out.perm[(size_t)p];
+        int64_t o = out.rowptr[(size_t)p];
+        for (int64_t k = m.rowptr[(size_t)r]; k < m.rowptr[(size_t)r + 1]; ++k, ++o) {
+            out.col[(size_t)o] = colmap[(size_t)m.col[(size_t)k]];
+            out.val[(size_t)o] = m.val[(size_t)k];
+        }
+    }
+    build_tiles(out.rowptr.data(), out.nrows, out);
     return TOPK_OK;
 }
 

@@ -25,6 +25,8 @@
 namespace topk {
 
 constexpr int kNT = 256;  // threads per block for the streaming kernels
+constexpr int kRitzKB = 8;  // Ritz outputs per thread
+constexpr int kStepJB = 8;  // basis columns per multi-dot pass of k_step
 
 struct LzState {
     double *alpha;      // [m]     alpha_1..alpha_m
@@ -87,7 +89,8 @@ struct V1Args {
     void *rep_slot;        // replica slot g or nullptr
     const uint64_t *seed;  // device param
     const int *use_v1;     // device param
-    const double *v1;      // device, n_g doubles (if *use_v1)
+    const double *v1;      // device, n_g doubles in original row order (if *use_v1)
+    const int32_t *perm;   // position -> part-local original row (hub-first order)
     int64_t row0, nrows, npad;
     double *slots;
     unsigned *counter;
@@ -118,9 +121,10 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
             const int64_t r = v * VW + q;
             double x = 0.0;
             if (r < a.nrows) {
-                if (use_v1) x = a.v1[r];
+                const int32_t orow = __ldg(a.perm + r);
+                if (use_v1) x = a.v1[orow];
                 else {
-                    uint64_t h = mix64(hs ^ (uint64_t)(a.row0 + r));
+                    uint64_t h = mix64(hs ^ (uint64_t)(a.row0 + orow));
                     x = 2.0 * ((double)(h >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
                 }
             }
@@ -143,15 +147,24 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// a7: SpMV + alpha partial (Alg.1 l.9-10). nnz-tiled: a packed tile holds whole
-// rows with <= kTileNnz nonzeros; each of 256 threads owns 8 consecutive
-// nonzeros; products go to shared memory, a block-wide segmented scan sums rows
-// (balanced regardless of the power-law row lengths); rows longer than a tile
-// are split into chunks finished by the last-arriving chunk block.
+// a7: SpMV + alpha partial (Alg.1 l.9-10), warp-per-tile segmented reduction.
+// A warp owns a tile of whole non-empty rows (<= kTileNnz nonzeros) and walks
+// it in rounds of 256 nonzeros: lane l holds 8 consecutive nonzeros (two
+// 16-byte col loads, vector value loads, all L1::no_allocate streaming; the
+// next round's columns and row-end bits are prefetched while the current round
+// gathers). x is gathered through L1: hot columns (bit 31, the hub-first
+// prefix of every slot) evict-last, the rest no_allocate. Products in the
+// compute dtype; a lane-serial + warp-wide segmented scan over the row-end
+// bitmask gives the row sums. Non-empty rows occupy positions [0, n_nonempty)
+// in order, so the j-th row end of a tile is row end_begin + j. Rows longer
+// than kTileNnz are chunked; the last-arriving chunk warp sums the chunk
+// partials in chunk order. Epilogue: y_r = s_i * sum (deferred normalisation),
+// stored once rounded, and the alpha partial sum_r y_r * v_i[r].
+// Deterministic: fixed shuffle trees and fixed orders everywhere.
 struct SpmvArgs {
-    const int32_t *rowptr;
     const int32_t *col;
     const void *val;
+    const uint32_t *endbits;
     const Tile *tiles;
     int ntiles;
     const LongRow *longrows;
@@ -170,152 +183,197 @@ struct SpmvArgs {
     int G, g;
 };
 
-__device__ __forceinline__ int padi(int e) { return e + (e >> 3); }
+// 8 consecutive matrix values (32-byte aligned group) converted to CT
+template <typename VT, typename CT> struct Val8;
+template <typename CT> struct Val8<float, CT> {
+    static __device__ __forceinline__ void load(const float *p, CT (&o)[8]) {
+        const float4 a = ld_stream(reinterpret_cast<const float4 *>(p));
+        const float4 b = ld_stream(reinterpret_cast<const float4 *>(p) + 1);
+        o[0] = (CT)a.x; o[1] = (CT)a.y; o[2] = (CT)a.z; o[3] = (CT)a.w;
+        o[4] = (CT)b.x; o[5] = (CT)b.y; o[6] = (CT)b.z; o[7] = (CT)b.w;
+    }
+};
+template <typename CT> struct Val8<double, CT> {
+    static __device__ __forceinline__ void load(const double *p, CT (&o)[8]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 a = ld_stream(reinterpret_cast<const double2 *>(p) + q);
+            o[2 * q] = (CT)a.x;
+            o[2 * q + 1] = (CT)a.y;
+        }
+    }
+};
+template <typename CT> struct Val8<bf16, CT> {
+    static __device__ __forceinline__ void load(const bf16 *p, CT (&o)[8]) {
+        const int4 v = ld_stream(reinterpret_cast<const int4 *>(p));
+        const bf16 *e = reinterpret_cast<const bf16 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = cvt<CT>(e[q]);
+    }
+};
+
+// x[c] for a remapped column entry: bit 31 set = hot column (kept in L1).
+template <typename ST, typename CT>
+__device__ __forceinline__ CT gather_x(const ST *__restrict__ x, int c) {
+    if (c < 0) return cvt<CT>(ld_keep<ST>(x + (c & 0x7FFFFFFF)));
+    return cvt<CT>(ld_noalloc<ST>(x + c));
+}
 
 template <typename VT, typename ST, typename CT>
-__global__ void __launch_bounds__(kNT) k_spmv(SpmvArgs a, int it) {
-    constexpr int IPT = kTileNnz / kNT;  // 8
-    __shared__ CT prod[kTileNnz + kTileNnz / 8];
-    __shared__ __align__(16) uint8_t flags[kTileNnz];
-    __shared__ int32_t rp[kTileRows + 1];
-    __shared__ CT wv[kNT / 32];
-    __shared__ int wf[kNT / 32];
+__global__ void __launch_bounds__(kNT, 4) k_spmv(SpmvArgs a, int it) {
+    constexpr int EPL = 8, RND = 32 * EPL;  // nonzeros per lane / per warp round
     __shared__ CT red[kNT / 32];
+    __shared__ double redd[kNT / 32];
     __shared__ int sflag;
 
     double sd;
     if (!lz_prologue(it, a.st, a.ex, a.G, sd)) return;
     const CT s = (CT)sd;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int gwarp = (int)((blockIdx.x * kNT + threadIdx.x) >> 5);
+    const int nwarps = (int)(gridDim.x * (kNT / 32));
     const VT *__restrict__ val = reinterpret_cast<const VT *>(a.val);
     const ST *__restrict__ x = reinterpret_cast<const ST *>(a.x);
     const ST *__restrict__ ui = reinterpret_cast<const ST *>(a.ui);
     ST *__restrict__ y = reinterpret_cast<ST *>(a.y);
     CT alpha_acc = CT(0);
 
-    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        const Tile T = a.tiles[t];
-        if (T.long_id < 0) {
-            const int rb = T.row_begin, nr = T.row_end - T.row_begin, nzb = T.nz_begin;
-            const int cnt = __ldg(a.rowptr + T.row_end) - nzb;
-            // issue the streaming loads of this tile's nonzeros first (MLP)
-            int32_t c[IPT];
-            VT v[IPT];
-#pragma unroll
-            for (int j = 0; j < IPT; ++j) {
-                const int k = j * kNT + tid;
-                if (k < cnt) {
-                    c[j] = __ldcs(a.col + nzb + k);
-                    v[j] = __ldcs(val + nzb + k);
+    for (int t = gwarp; t < a.ntiles; t += nwarps) {
+        const int4 T = __ldg(reinterpret_cast<const int4 *>(a.tiles) + t);
+        const int zb = T.x, zend = T.x + T.y;
+        const int z8 = zb & ~7;
+        if (T.w < 0) {
+            CT carry = CT(0);
+            int jrow = T.z;
+            // prefetch of round 0: columns + row-end bits
+            int k0 = z8 + EPL * lane;
+            int4 ca = make_int4(0, 0, 0, 0), cb = ca;
+            unsigned wb = 0u;
+            if (k0 < zend) {
+                ca = ld_stream(reinterpret_cast<const int4 *>(a.col + k0));
+                cb = ld_stream(reinterpret_cast<const int4 *>(a.col + k0) + 1);
+                wb = __ldg(a.endbits + (k0 >> 5));
+            }
+            for (int base = z8; base < zend; base += RND) {
+                const int cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+                const int kc = k0;
+                const unsigned wcur = wb;
+                k0 += RND;
+                if (k0 < zend) {  // next round's columns in flight during this round's gathers
+                    ca = ld_stream(reinterpret_cast<const int4 *>(a.col + k0));
+                    cb = ld_stream(reinterpret_cast<const int4 *>(a.col + k0) + 1);
+                    wb = __ldg(a.endbits + (k0 >> 5));
                 }
-            }
-            for (int q = tid; q <= nr; q += kNT) rp[q] = __ldg(a.rowptr + rb + q) - nzb;
-            *reinterpret_cast<uint2 *>(&flags[tid * IPT]) = make_uint2(0u, 0u);
+                // valid-element mask of this lane's 8 slots: [zb, zend) intersect [kc, kc + 8)
+                const int lo = max(zb - kc, 0), hi = min(zend - kc, EPL);
+                const unsigned valid = (hi > lo) ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+                CT p[8];
 #pragma unroll
-            for (int j = 0; j < IPT; ++j) {
-                const int k = j * kNT + tid;
-                if (k < cnt) prod[padi(k)] = cvt<CT>(v[j]) * cvt<CT>(__ldg(x + c[j]));
-            }
-            __syncthreads();
-            for (int q = tid; q < nr; q += kNT)
-                if (rp[q] < rp[q + 1]) flags[rp[q]] = 1;
-            __syncthreads();
-            // per-thread segmented inclusive scan over its 8 elements
-            const int e0 = tid * IPT;
-            CT run = CT(0);
-            int any = 0, first = IPT;
-            const uint2 fl = *reinterpret_cast<const uint2 *>(&flags[e0]);
-            const uint8_t *fb = reinterpret_cast<const uint8_t *>(&fl);
+                for (int e = 0; e < 8; ++e) p[e] = CT(0);
+                if (valid) {
+                    CT v8[8];
+                    Val8<VT, CT>::load(val + kc, v8);
 #pragma unroll
-            for (int q = 0; q < IPT; ++q) {
-                const int e = e0 + q;
-                if (e < cnt) {
-                    const CT pv = prod[padi(e)];
-                    if (fb[q]) {
-                        run = pv;
-                        if (!any) { any = 1; first = q; }
-                    } else {
-                        run += pv;
+                    for (int e = 0; e < 8; ++e)
+                        if ((valid >> e) & 1u) p[e] = v8[e] * gather_x<ST, CT>(x, cc[e]);
+                }
+                const unsigned fb = (wcur >> (kc & 31)) & valid & 0xFFu;
+                // lane-serial segment sums
+                CT part[8], run = CT(0), head = CT(0);
+                bool seen = false;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    run += p[e];
+                    part[e] = run;
+                    if ((fb >> e) & 1u) {
+                        if (!seen) { head = run; seen = true; }
+                        run = CT(0);
                     }
-                    prod[padi(e)] = run;
                 }
-            }
-            // block-wide exclusive segmented scan of (any, run)
-            int f = any;
-            CT sv = run;
+                // inclusive segmented scan of the open tails across lanes
+                CT v = (lane == 0 && !seen) ? carry + run : run;
+                int f = seen;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int fu = __shfl_up_sync(0xffffffffu, f, o);
-                const CT vu = __shfl_up_sync(0xffffffffu, sv, o);
-                if (lane >= o) {
-                    if (!f) sv = vu + sv;
-                    f |= fu;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const CT vu = __shfl_up_sync(0xffffffffu, v, o);
+                    const int fu = __shfl_up_sync(0xffffffffu, f, o);
+                    if (lane >= o) {
+                        if (!f) v = vu + v;
+                        f |= fu;
+                    }
                 }
-            }
-            if (lane == 31) { wf[wid] = f; wv[wid] = sv; }
-            int fe = __shfl_up_sync(0xffffffffu, f, 1);
-            CT ve = __shfl_up_sync(0xffffffffu, sv, 1);
-            if (lane == 0) { fe = 0; ve = CT(0); }
-            __syncthreads();
-            CT pv = CT(0);
-            int pf = 0;
-            for (int w = 0; w < wid; ++w) {  // prefix over previous warps, fixed order
-                if (wf[w]) { pv = wv[w]; pf = 1; } else { pv = pv + wv[w]; }
-            }
-            const CT carry = fe ? ve : pv + ve;
-            (void)pf;
-            if (tid > 0) {
+                CT cin = __shfl_up_sync(0xffffffffu, v, 1);
+                if (lane == 0) cin = carry;
+                carry = __shfl_sync(0xffffffffu, v, 31);
+                // rank of this lane's row ends within the tile (ne <= 8)
+                const unsigned ne = __popc(fb);
+                const unsigned b0 = __ballot_sync(0xffffffffu, ne & 1u);
+                const unsigned b1 = __ballot_sync(0xffffffffu, ne & 2u);
+                const unsigned b2 = __ballot_sync(0xffffffffu, ne & 4u);
+                const unsigned b3 = __ballot_sync(0xffffffffu, ne & 8u);
+                int row = jrow + __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask) +
+                          8 * __popc(b3 & lt_mask);
+                jrow += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
+                if (fb) {
+                    bool first = true;
 #pragma unroll
-                for (int q = 0; q < IPT; ++q) {
-                    const int e = e0 + q;
-                    if (q < first && e < cnt) prod[padi(e)] = carry + prod[padi(e)];
+                    for (int e = 0; e < 8; ++e) {
+                        if ((fb >> e) & 1u) {
+                            const CT tot = first ? cin + head : part[e];
+                            first = false;
+                            const CT yv = s * tot;
+                            y[row] = rnd_ct<ST, CT>(yv);
+                            alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
+                            if (a.y_dbg) a.y_dbg[row] = (double)tot;
+                            ++row;
+                        }
+                    }
                 }
             }
-            __syncthreads();
-            for (int q = tid; q < nr; q += kNT) {
-                const int e = rp[q + 1] - 1;
-                const CT sum = (rp[q] <= e) ? prod[padi(e)] : CT(0);
-                const CT yv = s * sum;
-                y[rb + q] = rnd_ct<ST, CT>(yv);
-                alpha_acc += yv * (s * cvt<CT>(ui[rb + q]));
-                if (a.y_dbg) a.y_dbg[rb + q] = (double)sum;
-            }
-            __syncthreads();
         } else {
-            const LongRow L = a.longrows[T.long_id];
-            const int r = T.row_begin, nzb = T.nz_begin;
-            const int cnt = min(kTileNnz, __ldg(a.rowptr + r + 1) - nzb);
+            // chunk of a long row: warp partial, last-arriving chunk finishes the row
             CT part = CT(0);
+            for (int base = z8; base < zend; base += RND) {
+                const int kc = base + EPL * lane;
+                const int lo = max(zb - kc, 0), hi = min(zend - kc, EPL);
+                if (hi > lo) {
+                    const unsigned valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+                    const int4 ca = ld_stream(reinterpret_cast<const int4 *>(a.col + kc));
+                    const int4 cb = ld_stream(reinterpret_cast<const int4 *>(a.col + kc) + 1);
+                    const int cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+                    CT v8[8];
+                    Val8<VT, CT>::load(val + kc, v8);
 #pragma unroll
-            for (int j = 0; j < IPT; ++j) {
-                const int k = j * kNT + tid;
-                if (k < cnt) part += cvt<CT>(__ldcs(val + nzb + k)) * cvt<CT>(__ldg(x + __ldcs(a.col + nzb + k)));
+                    for (int e = 0; e < 8; ++e)
+                        if ((valid >> e) & 1u) part += v8[e] * gather_x<ST, CT>(x, cc[e]);
+                }
             }
-            part = block_sum<CT, kNT>(part, red);
-            if (tid == 0) {
+            part = warp_sum(part);
+            if (lane == 0) {
+                const LongRow L = a.longrows[T.w];
                 a.long_parts[t] = (double)part;
                 __threadfence();
-                const unsigned prev = atomicAdd(a.long_cnt + T.long_id, 1u);
+                const unsigned prev = atomicAdd(a.long_cnt + T.w, 1u);
                 if (prev == (unsigned)L.nchunks - 1) {
                     __threadfence();
                     CT sum = CT(0);
                     for (int q = 0; q < L.nchunks; ++q) sum += (CT)__ldcg(a.long_parts + L.first_tile + q);
                     const CT yv = s * sum;
-                    y[r] = rnd_ct<ST, CT>(yv);
-                    a.alpha_long[T.long_id] = (double)(yv * (s * cvt<CT>(ui[r])));
-                    if (a.y_dbg) a.y_dbg[r] = (double)sum;
-                    a.long_cnt[T.long_id] = 0u;
+                    y[L.row] = rnd_ct<ST, CT>(yv);
+                    a.alpha_long[T.w] = (double)(yv * (s * cvt<CT>(ui[L.row])));
+                    if (a.y_dbg) a.y_dbg[L.row] = (double)sum;
+                    a.long_cnt[T.w] = 0u;
                 }
             }
         }
     }
     const CT tot = block_sum<CT, kNT>(alpha_acc, red);
-    if (tid == 0) a.slots[blockIdx.x] = (double)tot;
+    if (threadIdx.x == 0) a.slots[blockIdx.x] = (double)tot;
     if (arrive_last(a.counter, &sflag)) {
-        double* rd = reinterpret_cast<double *>(prod);
-        const double s1 = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, rd);
-        const double s2 = block_sum_array<double, kNT>(a.alpha_long, a.nlong, 1, rd);
-        if (tid == 0) {
+        const double s1 = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, redd);
+        const double s2 = block_sum_array<double, kNT>(a.alpha_long, a.nlong, 1, redd);
+        if (threadIdx.x == 0) {
             a.ex.alpha_part[a.g] = s1 + s2;
             *a.counter = 0u;
         }
@@ -343,7 +401,7 @@ struct StepArgs {
 };
 
 template <typename ST, typename CT, int JB>
-__global__ void __launch_bounds__(kNT) k_step(StepArgs a, int it) {
+__global__ void __launch_bounds__(kNT, 4) k_step(StepArgs a, int it) {
     constexpr int VW = Vw<ST>::N;
     __shared__ CT part[kNT / 32][JB];
     __shared__ CT red[kNT / 32];
@@ -397,22 +455,33 @@ __global__ void __launch_bounds__(kNT) k_step(StepArgs a, int it) {
         return;
     }
 
-    for (int j0 = 0; j0 < it; j0 += JB) {
+    // Multi-dot h_j = u_j . w: the block's threads form NG column groups of LPG
+    // lanes; group g takes columns j0 + g*JB .. +JB-1 for the SAME rows, so one
+    // pass over the rows streams every basis column from DRAM once (y, u_i,
+    // u_{i-1}, w are re-read by the other groups from L1/L2) while each thread
+    // keeps only JB accumulators. Passes over further column blocks (it > NG*JB)
+    // read the stored w.
+    constexpr int NG = 4, LPG = kNT / NG;
+    const int grp = tid / LPG, gl = tid - grp * LPG;
+    for (int jb0 = 0; jb0 < it; jb0 += NG * JB) {
+        const int j0 = jb0 + grp * JB;
         CT acc[JB];
 #pragma unroll
         for (int q = 0; q < JB; ++q) acc[q] = CT(0);
-        for (int64_t v = (int64_t)blockIdx.x * kNT + tid; v < nvec; v += (int64_t)gridDim.x * kNT) {
+        for (int64_t v = (int64_t)blockIdx.x * LPG + gl; v < nvec; v += (int64_t)gridDim.x * LPG) {
             CT w[VW];
             if (a.mode == 2) {
                 vload<ST, CT>(src2 + v * VW, w);
-            } else if (j0 == 0) {
+            } else if (jb0 == 0) {
                 CT yy[VW], u1[VW], u0[VW];
                 vload<ST, CT>(yv + v * VW, yy);
                 vload<ST, CT>(ucur + v * VW, u1);
                 if (it > 1) vload<ST, CT>(uprev + v * VW, u0);
 #pragma unroll
                 for (int q = 0; q < VW; ++q) w[q] = yy[q] - c1 * u1[q] - (it > 1 ? c2 * u0[q] : CT(0));
-                vstore_back<ST, CT>(wv + v * VW, w);  // w rounded once; dots use what was stored
+                // w rounded once; every group dots with the rounded (stored) value
+                if (grp == 0) vstore_back<ST, CT>(wv + v * VW, w);
+                else round_back<ST, CT>(w);
             } else {
                 vload<ST, CT>(wv + v * VW, w);
             }
@@ -435,11 +504,13 @@ __global__ void __launch_bounds__(kNT) k_step(StepArgs a, int it) {
             if (lane == 0) part[wid][q] = r;
         }
         __syncthreads();
-        if (tid < JB && j0 + tid < it) {
+        if (tid < NG * JB && jb0 + tid < it) {  // column jb0 + tid = group tid / JB, slot tid % JB
+            constexpr int WPG = LPG / 32;
+            const int g2 = tid / JB, q = tid - g2 * JB;
             CT r = CT(0);
 #pragma unroll
-            for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][tid];
-            a.slots[(size_t)blockIdx.x * a.ld + j0 + tid] = (double)r;
+            for (int w8 = 0; w8 < WPG; ++w8) r += part[g2 * WPG + w8][q];
+            a.slots[(size_t)blockIdx.x * a.ld + jb0 + tid] = (double)r;
         }
         __syncthreads();
     }
@@ -495,10 +566,28 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     ST *dst = V + (size_t)it * a.npad;
     const int64_t nvec = a.npad / VW;
     CT nrm = CT(0);
-    for (int64_t v = (int64_t)blockIdx.x * kNT + tid; v < nvec; v += (int64_t)gridDim.x * kNT) {
+    // rows are walked in DESCENDING order: k_step just streamed the same basis
+    // columns in ascending order, so the most recently read ones are still L2-resident
+    for (int64_t vv = (int64_t)blockIdx.x * kNT + tid; vv < nvec; vv += (int64_t)gridDim.x * kNT) {
+        const int64_t v = nvec - 1 - vv;
         CT acc[VW];
         vload<ST, CT>(src + v * VW, acc);
-        for (int j = 0; j < it; ++j) {
+        // basis columns in blocks of 8: all loads of a block are issued before
+        // the subtractions (memory-level parallelism); subtraction order stays j
+        // ascending
+        int j = 0;
+        for (; j + 8 <= it; j += 8) {
+            CT u[8][VW];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) vload<ST, CT>(V + (size_t)(j + q) * a.npad + v * VW, u[q]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const CT cj = coef[j + q];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) acc[e] -= cj * u[q][e];
+            }
+        }
+        for (; j < it; ++j) {
             CT u[VW];
             vload<ST, CT>(V + (size_t)j * a.npad + v * VW, u);
             const CT cj = coef[j];
@@ -519,22 +608,37 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
 }
 
 // ---------------------------------------------------------------------------
-// a12-a13: Jacobi on T in one block, parallel (round-robin
-// tournament) ordering of the same rotations as the oracle's cyclic ordering;
-// same negligibility rule (|t_pq| <= eps sqrt|t_pp t_qq| or <= eps^2 ||T||_F);
-// then top-K by (-|theta|, -theta) and the sign convention s_1k > 0.
+// a12-a13: Jacobi on T in one CTA: parallel (round-robin
+// tournament) ordering of the oracle's rotations (reading Q10) with the same
+// stable tangent t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta =
+// (t_qq - t_pp) / (2 t_pq), evaluated division-free as
+//   r = sqrt(d^2 + 4 t_pq^2), d = t_qq - t_pp, D = |d| + r,
+//   c = D / sqrt(D^2 + 4 t_pq^2),  s = sgn(zeta) 2 |t_pq| / sqrt(D^2 + 4 t_pq^2)
+// (c = 1/sqrt(1+t^2), s = t c with t = sgn(zeta) 2|t_pq| / D), the same
+// negligibility rule (|t_pq| <= eps sqrt|t_pp t_qq| or <= eps^2 ||T||_F, tested
+// squared), stop at a rotation-free sweep or max_sweeps. The M/2 rotations of
+// a round are disjoint, so T <- J^T T J is applied as independent 2x2 blocks
+// (pair k rows, pair l columns) and S <- S J as independent column pairs: one
+// barrier-separated phase per round. Then top-K by (-|theta|, -theta) and the
+// sign convention S[0,k] > 0 (reading Q12). T and S use a power-of-two leading
+// dimension LD >= M (shifts instead of divisions).
 struct JacArgs {
     LzState st;
     Exch ex;
     int G, m, K, max_sweeps;
-    double *work;  // global fallback workspace (2 * M * M doubles) or nullptr
-    int use_smem;
+    double *work;  // global workspace when T, S do not fit in shared memory
+    int ld_log2;   // LD = 1 << ld_log2 >= m + (m & 1)
+    int hl_log2;   // 1 << hl_log2 >= (m + (m & 1)) / 2
 };
 
 __device__ __forceinline__ int rr_player(int pos, int round, int M) {
-    return pos == 0 ? 0 : 1 + (pos - 1 + round) % (M - 1);
+    if (pos == 0) return 0;
+    int x = pos - 1 + round;
+    if (x >= M - 1) x -= M - 1;
+    return 1 + x;
 }
 
+template <bool kSmem>
 __global__ void k_jacobi(JacArgs a) {
     extern __shared__ double jsm[];
     __shared__ int s_rot;
@@ -549,12 +653,14 @@ __global__ void k_jacobi(JacArgs a) {
     }
     __syncthreads();
     const int M = mm + (mm & 1);
-    double *T = a.use_smem ? jsm : a.work;
-    double *S = T + (size_t)M * M;
-    int *rot = reinterpret_cast<int *>(S + (size_t)M * M);           // [M/2]
-    double *cs = reinterpret_cast<double *>(rot + ((M / 2 + 1) & ~1));  // [M/2][2]
-    for (int i = tid; i < M * M; i += nt) {
-        const int r = i / M, c = i % M;
+    const int LS = a.ld_log2, LD = 1 << LS, HS = a.hl_log2, HD = 1 << HS;
+    double *T = kSmem ? jsm : a.work;
+    double *S = T + (size_t)M * LD;
+    double *cs = S + (size_t)M * LD;                      // [M/2][2]
+    int *pq = reinterpret_cast<int *>(cs + (size_t)M);    // [M/2][2]
+    int *rot = pq + M;                                    // [M/2]
+    for (int i = tid; i < M * LD; i += nt) {
+        const int r = i >> LS, c = i & (LD - 1);
         double t = 0.0;
         if (r < mm && c < mm) {
             if (r == c) t = st.alpha[r];
@@ -565,71 +671,78 @@ __global__ void k_jacobi(JacArgs a) {
     }
     __syncthreads();
     if (tid == 0) {
-        double f = 0.0;
-        for (int i = 0; i < M * M; ++i) f += T[i] * T[i];
+        double f = 0.0;  // ||T||_F in the oracle's summation order (row-major)
+        for (int r = 0; r < mm; ++r)
+            for (int c = 0; c < mm; ++c) f += T[(r << LS) + c] * T[(r << LS) + c];
         s_fro = sqrt(f);
     }
     __syncthreads();
     const double eps = 2.220446049250313e-16;
-    const double fro = s_fro;
+    const double fro2 = (eps * eps * s_fro) * (eps * eps * s_fro);
     int sweeps = 0, conv = (M < 2) ? 1 : 0;
     const int half = M / 2;
     while (!conv && sweeps < a.max_sweeps) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int round = 0; round < M - 1; ++round) {
+            // phase A: the rotation of every pair of this round
             for (int k = tid; k < half; k += nt) {
                 int p = rr_player(k, round, M), q = rr_player(M - 1 - k, round, M);
-                if (p > q) { int t = p; p = q; q = t; }
+                if (p > q) { const int t = p; p = q; q = t; }
+                pq[2 * k] = p;
+                pq[2 * k + 1] = q;
                 int doit = 0;
+                double c = 1.0, sn = 0.0;
                 if (q < mm) {
-                    const double apq = T[p * M + q], app = T[p * M + p], aqq = T[q * M + q];
-                    if (fabs(apq) <= eps * sqrt(fabs(app * aqq)) || fabs(apq) <= eps * eps * fro) {
-                        T[p * M + q] = 0.0;
-                        T[q * M + p] = 0.0;
-                    } else {
-                        const double zeta = (aqq - app) / (2.0 * apq);
-                        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                        const double c = 1.0 / sqrt(1.0 + t * t);
-                        cs[2 * k] = c;
-                        cs[2 * k + 1] = t * c;
+                    const double apq = T[(p << LS) + q], app = T[(p << LS) + p], aqq = T[(q << LS) + q];
+                    const double a2 = apq * apq;
+                    if (!(a2 <= eps * eps * fabs(app * aqq) || a2 <= fro2)) {
+                        const double d = aqq - app;
+                        const bool zpos = (d == 0.0) || ((d > 0.0) == (apq > 0.0));
+                        const double x = d * d + 4.0 * a2;
+                        const double D = fabs(d) + x * rsqrt(x);
+                        const double ih = rsqrt(D * D + 4.0 * a2);
+                        c = D * ih;
+                        sn = (zpos ? 2.0 : -2.0) * fabs(apq) * ih;
                         doit = 1;
                         s_rot = 1;
                     }
                 }
+                cs[2 * k] = c;
+                cs[2 * k + 1] = sn;
                 rot[k] = doit;
             }
             __syncthreads();
-            for (int i = tid; i < half * M; i += nt) {  // T <- T J, S <- S J (columns p, q)
-                const int k = i / M, r = i % M;
-                if (!rot[k]) continue;
-                int p = rr_player(k, round, M), q = rr_player(M - 1 - k, round, M);
-                if (p > q) { int t = p; p = q; q = t; }
-                const double c = cs[2 * k], s = cs[2 * k + 1];
-                const double tp = T[r * M + p], tq = T[r * M + q];
-                T[r * M + p] = c * tp - s * tq;
-                T[r * M + q] = s * tp + c * tq;
-                const double sp = S[r * M + p], sq = S[r * M + q];
-                S[r * M + p] = c * sp - s * sq;
-                S[r * M + q] = s * sp + c * sq;
+            // phase B1: T <- J^T T J as 2x2 blocks (rows of pair k, columns of pair l)
+            for (int i = tid; i < (half << HS); i += nt) {
+                const int k = i >> HS, l = i & (HD - 1);
+                if (l >= half || !(rot[k] | rot[l])) continue;
+                const int pk = pq[2 * k], qk = pq[2 * k + 1], pl = pq[2 * l], ql = pq[2 * l + 1];
+                const double ck = cs[2 * k], sk = cs[2 * k + 1], cl = cs[2 * l], sl = cs[2 * l + 1];
+                double *r0 = T + (pk << LS), *r1 = T + (qk << LS);
+                const double b00 = r0[pl], b01 = r0[ql], b10 = r1[pl], b11 = r1[ql];
+                const double e00 = cl * b00 - sl * b01, e01 = sl * b00 + cl * b01;  // columns (T J)
+                const double e10 = cl * b10 - sl * b11, e11 = sl * b10 + cl * b11;
+                r0[pl] = ck * e00 - sk * e10;                                      // rows (J^T .)
+                r1[pl] = sk * e00 + ck * e10;
+                if (k == l && rot[k]) {
+                    r0[ql] = 0.0;
+                    r1[pl] = 0.0;
+                } else {
+                    r0[ql] = ck * e01 - sk * e11;
+                }
+                r1[ql] = sk * e01 + ck * e11;
             }
-            __syncthreads();
-            for (int i = tid; i < half * M; i += nt) {  // T <- J^T T (rows p, q)
-                const int k = i / M, col = i % M;
-                if (!rot[k]) continue;
-                int p = rr_player(k, round, M), q = rr_player(M - 1 - k, round, M);
-                if (p > q) { int t = p; p = q; q = t; }
-                const double c = cs[2 * k], s = cs[2 * k + 1];
-                const double tp = T[p * M + col], tq = T[q * M + col];
-                T[p * M + col] = c * tp - s * tq;
-                T[q * M + col] = s * tp + c * tq;
-            }
-            __syncthreads();
-            for (int k = tid; k < half; k += nt) {
-                if (!rot[k]) continue;
-                int p = rr_player(k, round, M), q = rr_player(M - 1 - k, round, M);
-                T[p * M + q] = 0.0;
-                T[q * M + p] = 0.0;
+            // phase B2: S <- S J (columns p, q), row r
+            for (int i = tid; i < (half << LS); i += nt) {
+                const int k = i >> LS, r = i & (LD - 1);
+                if (r >= mm || !rot[k]) continue;
+                const int p = pq[2 * k], q = pq[2 * k + 1];
+                const double c = cs[2 * k], sn = cs[2 * k + 1];
+                double *Sr = S + (r << LS);
+                const double sp = Sr[p], sq = Sr[q];
+                Sr[p] = c * sp - sn * sq;
+                Sr[q] = sn * sp + c * sq;
             }
             __syncthreads();
         }
@@ -641,11 +754,11 @@ __global__ void k_jacobi(JacArgs a) {
     const int K = a.K;
     const int kf = K < mm ? K : mm;
     for (int c = tid; c < mm; c += nt) {
-        const double tc = T[c * M + c];
+        const double tc = T[(c << LS) + c];
         st.theta_all[c] = tc;
         int rank = 0;
         for (int d = 0; d < mm; ++d) {
-            const double td = T[d * M + d];
+            const double td = T[(d << LS) + d];
             const bool before = (fabs(td) != fabs(tc)) ? (fabs(td) > fabs(tc))
                                 : (td != tc) ? (td > tc) : (d < c);
             rank += before;
@@ -653,12 +766,12 @@ __global__ void k_jacobi(JacArgs a) {
         if (rank < kf) {
             double sg = 1.0;
             for (int j = 0; j < mm; ++j) {
-                const double sj = S[j * M + c];
+                const double sj = S[(j << LS) + c];
                 if (sj != 0.0) { sg = sj > 0.0 ? 1.0 : -1.0; break; }
             }
             st.evals[rank] = tc;
-            for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[j * M + c] * st.scale[j];
-            st.resid[rank] = fabs(st.beta[mm] * S[(mm - 1) * M + c]);
+            for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[(j << LS) + c] * st.scale[j];
+            st.resid[rank] = fabs(st.beta[mm] * S[((mm - 1) << LS) + c]);
         }
     }
     for (int k = kf + tid; k < K; k += nt) {
@@ -673,108 +786,140 @@ __global__ void k_jacobi(JacArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// a14: Ritz projection Y = V S_K ("𝒱V") with fp64 accumulation,
-// per-block squared-norm partials; k_ritz_norm scales to unit norm.
+// a14: Ritz projection y_k = sum_j S[j,k] v_j ("the eigenvectors of
+// M are given by 𝒱V"), fp64 accumulation, then y_k / ||y_k|| (reading Q12).
+// Two streaming passes over the stored basis; no fp64 Y is materialised:
+//   pass 0: recompute y_k row by row, per-block partials of ||y_k||^2 ->
+//           ex.ritz_part[g][k] (last-arriving block per output group, fixed order)
+//   pass 1: recompute y_k, scale by 1/||y_k|| (norms summed over parts in rank
+//           order) and store once, in the output dtype, to the caller's buffer
+//           in ORIGINAL row order (position p -> row perm[p]; hub-first order
+//           keeps all non-hot rows ascending, so the stores stay coalesced).
+// Thread = VW consecutive rows (one 16-byte load per basis column) x KB outputs;
+// block b = (row range b / ngroups, output group b % ngroups). coefS holds the sign
+// fix and the deferred normalisation s_j.
 struct RitzArgs {
     const void *V;
-    double *Y;        // [K][npad] unnormalised
     int64_t npad, nrows;
-    int K;
-    double *slots;    // [grid][K]
-    unsigned *counter;
+    int K, G, g;
+    double *slots;            // [gridDim.x][K]
+    unsigned *counter;        // [ceil(K / KB)]
     LzState st;
     Exch ex;
-    int g;
+    void *const *out_ptr;     // device param: output base (K vectors of nrows)
+    const int *out_dtype;     // device param: 0 f64, 1 f32
+    const int32_t *perm;      // position -> part-local original row (output order)
 };
 
 template <typename ST, typename CT, int KB>
-__global__ void __launch_bounds__(kNT) k_ritz(RitzArgs a) {
-    extern __shared__ double rsm[];  // coef[m' * K]
+__global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
+    constexpr int VW = Vw<ST>::N;
+    extern __shared__ double rsm[];  // coef[m'][KB]
     __shared__ CT part[kNT / 32][KB];
+    __shared__ double inv[KB];
     __shared__ int sflag;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int mm = *a.st.m_found, kf = *a.st.k_found, K = a.K;
+    // output group fastest: the ngroups blocks of one row range run together and
+    // share the basis reads through L2 (DRAM reads V once per pass)
+    const int ngroups = (K + KB - 1) / KB;
+    const int grp = (int)(blockIdx.x % (unsigned)ngroups);
+    const int rblk = (int)(blockIdx.x / (unsigned)ngroups), nrblk = (int)(gridDim.x / (unsigned)ngroups);
+    const int k0 = grp * KB;
+    if (k0 >= kf) return;
+    void *out = nullptr;
+    int dt = 0;
+    if (pass == 1) {
+        out = *a.out_ptr;
+        if (!out) return;
+        dt = *a.out_dtype;
+    }
     CT *coef = reinterpret_cast<CT *>(rsm);
-    for (int i = tid; i < mm * K; i += kNT) coef[i] = (CT)a.st.coefS[i];
+    for (int i = tid; i < mm * KB; i += kNT) {
+        const int j = i / KB, q = i - j * KB;
+        coef[i] = (k0 + q < kf) ? (CT)a.st.coefS[(size_t)j * K + k0 + q] : CT(0);
+    }
+    if (pass == 1 && tid < KB) {
+        double s = 0.0;
+        for (int q = 0; q < a.G; ++q) s += __ldcg(a.ex.ritz_part + (size_t)q * K + k0 + tid);
+        inv[tid] = (k0 + tid < kf) ? 1.0 / sqrt(s) : 0.0;
+    }
     __syncthreads();
     const ST *V = reinterpret_cast<const ST *>(a.V);
-    for (int k0 = 0; k0 < kf; k0 += KB) {
-        CT nrm[KB];
+    const int64_t nvec = (a.nrows + VW - 1) / VW;
+    CT nrm[KB];
 #pragma unroll
-        for (int q = 0; q < KB; ++q) nrm[q] = CT(0);
-        for (int64_t r = (int64_t)blockIdx.x * kNT + tid; r < a.nrows; r += (int64_t)gridDim.x * kNT) {
-            CT acc[KB];
+    for (int q = 0; q < KB; ++q) nrm[q] = CT(0);
+    for (int64_t v = (int64_t)rblk * kNT + tid; v < nvec; v += (int64_t)nrblk * kNT) {
+        CT acc[VW][KB];
 #pragma unroll
-            for (int q = 0; q < KB; ++q) acc[q] = CT(0);
-            for (int j = 0; j < mm; ++j) {
-                const CT u = cvt<CT>(V[(size_t)j * a.npad + r]);
-                const CT *cj = coef + (size_t)j * K + k0;
+        for (int e = 0; e < VW; ++e)
 #pragma unroll
-                for (int q = 0; q < KB; ++q)
-                    if (k0 + q < kf) acc[q] += cj[q] * u;
+            for (int q = 0; q < KB; ++q) acc[e][q] = CT(0);
+        for (int j = 0; j < mm; ++j) {
+            CT u[VW];
+            vload_cs<ST, CT>(V + (size_t)j * a.npad + v * VW, u);
+            const CT *cj = coef + j * KB;
+#pragma unroll
+            for (int q = 0; q < KB; ++q) {
+                const CT c = cj[q];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) acc[e][q] += c * u[e];
             }
+        }
+        if (pass == 0) {
 #pragma unroll
             for (int q = 0; q < KB; ++q)
-                if (k0 + q < kf) {
-                    a.Y[(size_t)(k0 + q) * a.npad + r] = (double)acc[q];
-                    nrm[q] += acc[q] * acc[q];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) nrm[q] += acc[e][q] * acc[e][q];
+        } else {
+            int32_t orow[VW];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) {
+                const int64_t r = v * VW + e;
+                orow[e] = (r < a.nrows) ? __ldg(a.perm + r) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < KB; ++q) {
+                if (k0 + q >= kf) break;
+                const double iv = inv[q];
+                const size_t base = (size_t)(k0 + q) * a.nrows;
+#pragma unroll
+                for (int e = 0; e < VW; ++e) {
+                    const int64_t r = v * VW + e;
+                    if (r < a.nrows) {
+                        const size_t o = base + (size_t)orow[e];
+                        const double yv = (double)acc[e][q] * iv;
+                        if (dt == 0) __stcs(reinterpret_cast<double *>(out) + o, yv);
+                        else __stcs(reinterpret_cast<float *>(out) + o, (float)yv);
+                    }
                 }
+            }
         }
-#pragma unroll
-        for (int q = 0; q < KB; ++q) {
-            const CT rr = warp_sum(nrm[q]);
-            if (lane == 0) part[wid][q] = rr;
-        }
-        __syncthreads();
-        if (tid < KB && k0 + tid < kf) {
-            CT rr = CT(0);
-#pragma unroll
-            for (int w8 = 0; w8 < kNT / 32; ++w8) rr += part[w8][tid];
-            a.slots[(size_t)blockIdx.x * K + k0 + tid] = (double)rr;
-        }
-        __syncthreads();
     }
-    if (arrive_last(a.counter, &sflag)) {
-        for (int k = wid; k < kf; k += kNT / 32) {
-            double rr = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) rr += __ldcg(a.slots + (size_t)b * K + k);
-            rr = warp_sum(rr);
-            if (lane == 0) a.ex.ritz_part[(size_t)a.g * K + k] = rr;
-        }
-        __syncthreads();
-        if (tid == 0) *a.counter = 0u;
-    }
-}
-
-struct RitzNormArgs {
-    const double *Y;
-    int64_t npad, nrows;
-    int K, G;
-    const int *k_found;
-    const double *ritz_part;  // [G][K]
-    void *const *out_ptr;     // device param: output base (K vectors of nrows)
-    const int *out_dtype;     // device param: 0 f64, 1 f32
-};
-
-__global__ void __launch_bounds__(kNT) k_ritz_norm(RitzNormArgs a) {
-    __shared__ double inv[256];
-    const int kf = *a.k_found;
-    void *out = *a.out_ptr;
-    if (!out) return;
-    for (int k = threadIdx.x; k < kf && k < 256; k += blockDim.x) {
-        double s = 0.0;
-        for (int q = 0; q < a.G; ++q) s += __ldcg(a.ritz_part + (size_t)q * a.K + k);
-        inv[k] = 1.0 / sqrt(s);
+    if (pass == 1) return;
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+        const CT rr = warp_sum(nrm[q]);
+        if (lane == 0) part[wid][q] = rr;
     }
     __syncthreads();
-    const int dt = *a.out_dtype;
-    const int64_t total = (int64_t)kf * a.nrows;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(i / a.nrows);
-        const int64_t r = i - (int64_t)k * a.nrows;
-        const double v = a.Y[(size_t)k * a.npad + r] * inv[k];
-        if (dt == 0) reinterpret_cast<double *>(out)[i] = v;
-        else reinterpret_cast<float *>(out)[i] = (float)v;
+    if (tid < KB && k0 + tid < kf) {
+        CT rr = CT(0);
+#pragma unroll
+        for (int w8 = 0; w8 < kNT / 32; ++w8) rr += part[w8][tid];
+        a.slots[(size_t)rblk * K + k0 + tid] = (double)rr;
+    }
+    if (arrive_last_n(a.counter + grp, (unsigned)nrblk, &sflag)) {
+        for (int q = wid; q < KB; q += kNT / 32) {
+            if (k0 + q >= kf) break;
+            double rr = 0.0;
+            for (int b = lane; b < nrblk; b += 32) rr += __ldcg(a.slots + (size_t)b * K + k0 + q);
+            rr = warp_sum(rr);
+            if (lane == 0) a.ex.ritz_part[(size_t)a.g * K + k0 + q] = rr;
+        }
+        __syncthreads();
+        if (tid == 0) a.counter[grp] = 0u;
     }
 }
 

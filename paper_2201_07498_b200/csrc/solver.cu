@@ -9,12 +9,14 @@
 //
 // Per solve (DESIGN.md 8(a) a5-a15), all device-side, captured as ONE CUDA graph:
 //   k_v1 -> [exchange] -> for i in 1..m: k_spmv, [x], k_step, [x], k_correct, [x]
-//   -> k_jacobi -> k_ritz -> [x] -> k_ritz_norm
+//   -> k_jacobi -> k_ritz(pass 0: norms) -> [x] -> k_ritz(pass 1: output)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -28,6 +30,24 @@
 using namespace topk;
 
 static thread_local std::string g_last_error;
+
+// TOPK_TRACE=1: stage timings of topk_eig_create on stderr (host-side profiling)
+struct StageClock {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0;
+    StageClock() {
+        const char *e = std::getenv("TOPK_TRACE");
+        on = e && e[0] == '1';
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[topk create] %-28s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 static topk_status_t fail(topk_status_t s, const std::string &msg) {
     g_last_error = msg;
@@ -63,14 +83,16 @@ struct Part {
     int g = 0;
     int64_t row0 = 0, nrows = 0, npad = 0, nnz = 0;
     int ntiles = 0, nlong = 0;
-    int32_t *rowptr = nullptr, *col = nullptr;
+    int32_t *col = nullptr, *perm = nullptr;
+    std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
+    uint32_t *endbits = nullptr;
+    std::vector<int32_t> h_rowptr;  // host copy (export_layout)
     void *val = nullptr;
     Tile *tiles = nullptr;
     LongRow *longrows = nullptr;
     double *long_parts = nullptr, *alpha_long = nullptr;
     unsigned *long_cnt = nullptr;
     void *V = nullptr, *y = nullptr, *w = nullptr;
-    double *Y = nullptr;
     void *out = nullptr;       // internal eigenvector output (K * nrows f64)
     double *v1buf = nullptr;
     double *y_dbg = nullptr;
@@ -100,7 +122,8 @@ struct topk_eig_s {
     void *replica = nullptr;
     SolveParams *dparams = nullptr, *hparams = nullptr;
     double *jac_work = nullptr;
-    size_t jac_smem = 0;
+    size_t jac_smem = 0, jac_bytes = 0;
+    int jac_ld_log2 = 0, jac_hl_log2 = 0;
     int jac_threads = 32;
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -188,7 +211,7 @@ static void *rep_slot(topk_eig_s *h, Part &p) {
 template <typename VT, typename ST, typename CT>
 static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     SpmvArgs a;
-    a.rowptr = p.rowptr; a.col = p.col; a.val = p.val;
+    a.col = p.col; a.val = p.val; a.endbits = p.endbits;
     a.tiles = p.tiles; a.ntiles = p.ntiles;
     a.longrows = p.longrows; a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
     a.alpha_long = p.alpha_long; a.nlong = p.nlong;
@@ -216,9 +239,8 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.mode = mode;
     const int cols = it;
     prof_begin(h, p, 2);
-    if (cols <= 8) k_step<ST, CT, 8><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
-    else if (cols <= 16) k_step<ST, CT, 16><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
-    else k_step<ST, CT, 32><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
+    (void)cols;
+    k_step<ST, CT, kStepJB><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -245,7 +267,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     for (Part &p : h->parts) {
         V1Args a;
         a.u0 = p.V; a.rep_slot = rep_slot(h, p);
-        a.seed = &h->dparams->seed; a.use_v1 = &h->dparams->use_v1; a.v1 = p.v1buf;
+        a.seed = &h->dparams->seed; a.use_v1 = &h->dparams->use_v1; a.v1 = p.v1buf; a.perm = p.perm;
         a.row0 = p.row0; a.nrows = p.nrows; a.npad = p.npad;
         a.slots = p.slots; a.counter = p.counters + 0;
         a.st = p.st; a.ex = h->ex; a.g = p.g;
@@ -279,42 +301,38 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     for (Part &p : h->parts) {
         JacArgs a;
         a.st = p.st; a.ex = h->ex; a.G = h->G; a.m = h->m; a.K = h->K; a.max_sweeps = 50;
-        a.work = h->jac_work ? h->jac_work + (size_t)(&p - &h->parts[0]) * 2 * (h->m + 2) * (h->m + 2) + 0 : nullptr;
-        a.use_smem = h->jac_work ? 0 : 1;
+        a.work = h->jac_work ? h->jac_work + (size_t)(&p - &h->parts[0]) * (h->jac_bytes / 8) : nullptr;
+        a.ld_log2 = h->jac_ld_log2;
+        a.hl_log2 = h->jac_hl_log2;
         prof_begin(h, p, 4);
-        k_jacobi<<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
+        if (h->jac_work) k_jacobi<false><<<1, h->jac_threads, 0, h->stream>>>(a);
+        else k_jacobi<true><<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
         CUDA_TRY(cudaGetLastError());
         prof_end(h, p);
         h->launches++;
     }
     if (!want_vectors) return;
-    // a14: Ritz projection + normalisation
-    for (Part &p : h->parts) {
-        RitzArgs a;
-        a.V = p.V; a.Y = p.Y; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K;
-        a.slots = p.slots; a.counter = p.counters + 4;
-        a.st = p.st; a.ex = h->ex; a.g = p.g;
-        size_t smem = (size_t)h->m * h->K * sizeof(double);
-        prof_begin(h, p, 5);
-        if (h->K <= 8) k_ritz<ST, CT, 8><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
-        else if (h->K <= 16) k_ritz<ST, CT, 16><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
-        else k_ritz<ST, CT, 32><<<h->grid_ritz, kNT, smem, h->stream>>>(a);
-        CUDA_TRY(cudaGetLastError());
-        prof_end(h, p);
-        h->launches++;
-    }
-    exch_ritz(h);
-    for (Part &p : h->parts) {
-        RitzNormArgs a;
-        a.Y = p.Y; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K; a.G = h->G;
-        a.k_found = p.st.k_found; a.ritz_part = h->ex.ritz_part;
-        a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) + offsetof(SolveParams, out_ptr));
-        a.out_dtype = &h->dparams->out_dtype;
-        prof_begin(h, p, 6);
-        k_ritz_norm<<<h->grid_stream, kNT, 0, h->stream>>>(a);
-        CUDA_TRY(cudaGetLastError());
-        prof_end(h, p);
-        h->launches++;
+    // a14: Ritz projection + normalisation, two streaming passes (norms, output)
+    for (int pass = 0; pass < 2; ++pass) {
+        for (Part &p : h->parts) {
+            RitzArgs a;
+            a.V = p.V; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K; a.G = h->G; a.g = p.g;
+            a.slots = p.slots; a.counter = p.counters + 8;
+            a.st = p.st; a.ex = h->ex;
+            a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) +
+                                        offsetof(SolveParams, out_ptr));
+            a.out_dtype = &h->dparams->out_dtype;
+            a.perm = p.perm;
+            const size_t smem = (size_t)h->m * kRitzKB * sizeof(double);
+            const unsigned ngroups = (unsigned)((h->K + kRitzKB - 1) / kRitzKB);
+            const dim3 grid((unsigned)h->grid_ritz * ngroups);
+            prof_begin(h, p, 5 + pass);
+            k_ritz<ST, CT, kRitzKB><<<grid, kNT, smem, h->stream>>>(a, pass);
+            CUDA_TRY(cudaGetLastError());
+            prof_end(h, p);
+            h->launches++;
+        }
+        if (pass == 0) exch_ritz(h);
     }
 }
 
@@ -328,16 +346,19 @@ static void set_kernels(topk_eig_s *h) {
     h->enqueue = &enqueue_solve<VT, ST, CT>;
     h->spmv_only = &spmv_only<VT, ST, CT>;
     int occ = 0;
+    // the SpMV uses (almost) no shared memory: give the whole unified L1 to the x gathers
+    CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT>, kNT, 0);
     h->grid_spmv = h->nsm * std::max(1, occ);
     int occ2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, 32>, kNT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
     h->grid_stream = h->nsm * std::max(1, std::min(occ2, 4));
-    h->grid_ritz = h->nsm * 2;
+    int occ3 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB>, kNT, (size_t)h->m * kRitzKB * 8);
+    h->grid_ritz = h->nsm * std::max(1, std::min(occ3, 2));
     CUDA_TRY(cudaFuncSetAttribute(k_correct<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 * kRitzKB * sizeof(double))));
 }
 
 static bool select_kernels(topk_eig_s *h) {
@@ -396,11 +417,13 @@ static void upload_values(topk_eig_s *h, Part &p, const PartLayout &L) {
     if (h->ms == TOPK_F64) {
         CUDA_TRY(cudaMemcpy(p.val, L.val.data(), z * 8, cudaMemcpyHostToDevice));
     } else if (h->ms == TOPK_F32) {
-        std::vector<float> t(z);
+        hvec<float> t(z);
+#pragma omp parallel for schedule(static)
         for (size_t k = 0; k < z; ++k) t[k] = round_f32(L.val[k]);
         CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 4, cudaMemcpyHostToDevice));
     } else {
-        std::vector<uint16_t> t(z);
+        hvec<uint16_t> t(z);
+#pragma omp parallel for schedule(static)
         for (size_t k = 0; k < z; ++k) t[k] = round_bf16_bits(L.val[k]);
         CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 2, cudaMemcpyHostToDevice));
     }
@@ -455,13 +478,21 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     // a1-a3 on the host
     Csr csr;
     std::string err;
+    StageClock clk;
     topk_status_t s = canonicalize(*A, csr, err);
     if (s != TOPK_OK) return fail(s, err);
+    clk.mark("canonicalize");
     if (o.check_symmetry >= 0 && !is_symmetric(csr)) return fail(TOPK_E_NOT_SYMMETRIC, "matrix is not symmetric");
+    clk.mark("symmetry check");
     h->bounds.resize((size_t)G + 1);
     s = partition_rule_p(csr.rowptr.data(), n, G, h->bounds.data());
     if (s != TOPK_OK) return fail(s, "partition failed");
     const int64_t npad = padded_rows(h->bounds.data(), G);
+    const std::vector<uint8_t> hot = hot_columns(csr, hot_count(n, (int)dsize(storage)));
+    std::vector<int32_t> pos;
+    hub_first_order(csr, h->bounds.data(), G, hot.data(), pos);
+    const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, hot.data(), pos.data());
+    clk.mark("partition + hot + order");
 
     // device
     int ndev = 0;
@@ -491,16 +522,23 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->dparams = h->alloc<SolveParams>(1 + (size_t)nlocal);
         CUDA_TRY(cudaMallocHost(&h->hparams, sizeof(SolveParams) * (1 + nlocal)));
         std::memset(h->hparams, 0, sizeof(SolveParams) * (1 + nlocal));
-        // Jacobi workspace
+        // Jacobi workspace: T and S with a power-of-two leading dimension, + rotations
         const int M = m + (m & 1);
-        size_t jbytes = (size_t)2 * M * M * 8 + (size_t)(M / 2 + 2) * 4 + (size_t)(M / 2 + 1) * 16 + 64;
-        h->jac_threads = (M <= 48) ? 32 : 256;
+        int ls = 0, hs = 0;
+        while ((1 << ls) < M) ++ls;
+        while ((1 << hs) < M / 2) ++hs;
+        h->jac_ld_log2 = ls;
+        h->jac_hl_log2 = hs;
+        const size_t jbytes = (size_t)2 * M * ((size_t)1 << ls) * 8 + (size_t)M * 8 + (size_t)M * 4 + (size_t)M * 2 + 64;
+        const int items = std::max((M / 2) << hs, (M / 2) << ls);
+        h->jac_threads = std::max(32, std::min(1024, (items + 31) / 32 * 32));
         if (jbytes <= 200 * 1024) {
             h->jac_smem = jbytes;
-            CUDA_TRY(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
+            CUDA_TRY(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
         } else {
             h->jac_smem = 0;
-            h->jac_work = h->alloc<double>((size_t)nlocal * 2 * (m + 2) * (m + 2) + 1024);
+            h->jac_bytes = (jbytes + 255) / 256 * 256;
+            h->jac_work = h->alloc<double>((size_t)nlocal * h->jac_bytes / 8);
         }
 
         h->parts.resize((size_t)nlocal);
@@ -508,33 +546,39 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             Part &p = h->parts[(size_t)lp];
             p.g = (world > 1) ? h->rank : lp;
             PartLayout L;
-            s = build_part(csr, h->bounds.data(), G, p.g, npad, L, err);
+            s = build_part(csr, h->bounds.data(), G, p.g, npad, pos.data(), colmap.data(), L, err);
             if (s != TOPK_OK) return fail(s, err);
+            clk.mark("build_part");
             p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.col.size();
             p.ntiles = (int)L.tiles.size(); p.nlong = (int)L.longrows.size();
-            p.rowptr = h->alloc<int32_t>(L.rowptr.size());
-            p.col = h->alloc<int32_t>(L.col.size());
-            p.val = h->alloc<char>(L.val.size() * dsize(ms));
+            // col/val padded by 128 entries: the SpMV issues aligned 4-wide loads
+            p.col = h->alloc<int32_t>(L.col.size() + 128);
+            p.val = h->alloc<char>((L.val.size() + 128) * dsize(ms));
+            p.endbits = h->alloc<uint32_t>(L.endbits.size());
+            p.h_rowptr = L.rowptr;
+            p.h_perm = L.perm;
+            p.perm = h->alloc<int32_t>(L.perm.size());
             p.tiles = h->alloc<Tile>(L.tiles.size());
             p.longrows = h->alloc<LongRow>(L.longrows.size());
             p.long_parts = h->alloc<double>(L.tiles.size());
             p.long_cnt = h->alloc<unsigned>(L.longrows.size());
             p.alpha_long = h->alloc<double>(L.longrows.size());
             CUDA_TRY(cudaStreamSynchronize(h->stream));
-            CUDA_TRY(cudaMemcpy(p.rowptr, L.rowptr.data(), L.rowptr.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(cudaMemcpy(p.endbits, L.endbits.data(), L.endbits.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.perm.empty()) CUDA_TRY(cudaMemcpy(p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemcpy(p.col, L.col.data(), L.col.size() * 4, cudaMemcpyHostToDevice));
             if (!L.tiles.empty()) CUDA_TRY(cudaMemcpy(p.tiles, L.tiles.data(), L.tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
             upload_values(h.get(), p, L);
+            clk.mark("upload (H2D)");
             const size_t vsz = dsize(storage);
             p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
             p.y = h->alloc<char>((size_t)npad * vsz);
             p.w = h->alloc<char>((size_t)npad * vsz);
-            p.Y = h->alloc<double>((size_t)K * npad);
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
             p.slots = h->alloc<double>((size_t)std::max(h->grid_spmv, std::max(h->grid_stream, h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
-            p.counters = h->alloc<unsigned>(8);
+            p.counters = h->alloc<unsigned>(8 + 64);
             carve_state(h.get(), p);
             h->bytes_model += model_bytes(h.get(), p);
         }
@@ -754,6 +798,55 @@ topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t
     return TOPK_OK;
 }
 
+topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g, topk_dtype_t storage,
+                                   topk_dtype_t values_storage, int64_t *n_pad, int64_t *n_rows, int64_t *nnz,
+                                   int64_t *ntiles, int64_t *rowptr, int32_t *col, double *val, int32_t *tiles,
+                                   int32_t *perm) {
+    if (!A) return fail(TOPK_E_INVALID, "A must be non-NULL");
+    if (G < 1 || G > 64 || g < 0 || g >= G) return fail(TOPK_E_INVALID, "need 1 <= G <= 64 and 0 <= g < G");
+    if (values_storage < TOPK_F64 || values_storage > TOPK_BF16 || storage < TOPK_F64 || storage > TOPK_BF16)
+        return fail(TOPK_E_INVALID, "bad dtype");
+    try {
+        Csr csr;
+        std::string err;
+        StageClock clk;
+        topk_status_t s = canonicalize(*A, csr, err);
+        if (s != TOPK_OK) return fail(s, err);
+        clk.mark("canonicalize");
+        if (G > csr.n) return fail(TOPK_E_INVALID, "G must be <= n");
+        std::vector<int64_t> b((size_t)G + 1);
+        s = partition_rule_p(csr.rowptr.data(), csr.n, G, b.data());
+        if (s != TOPK_OK) return fail(s, "partition failed");
+        const int64_t npad = padded_rows(b.data(), G);
+        PartLayout L;
+        const std::vector<uint8_t> hot = hot_columns(csr, hot_count(csr.n, (int)dsize(storage)));
+        std::vector<int32_t> pos;
+        hub_first_order(csr, b.data(), G, hot.data(), pos);
+        const std::vector<int32_t> colmap = column_map(csr.n, b.data(), G, npad, hot.data(), pos.data());
+        clk.mark("partition + hot + order");
+        s = build_part(csr, b.data(), G, g, npad, pos.data(), colmap.data(), L, err);
+        if (s != TOPK_OK) return fail(s, err);
+        clk.mark("build_part");
+        if (n_pad) *n_pad = npad;
+        if (n_rows) *n_rows = L.nrows;
+        if (nnz) *nnz = (int64_t)L.col.size();
+        if (ntiles) *ntiles = (int64_t)L.tiles.size();
+        if (rowptr)
+            for (size_t i = 0; i < L.rowptr.size(); ++i) rowptr[i] = L.rowptr[i];
+        if (col) std::memcpy(col, L.col.data(), L.col.size() * 4);
+        if (val)
+            for (size_t k = 0; k < L.val.size(); ++k)
+                val[k] = values_storage == TOPK_F64 ? L.val[k]
+                         : values_storage == TOPK_F32 ? (double)round_f32(L.val[k])
+                                                      : bf16_bits_to_double(round_bf16_bits(L.val[k]));
+        if (tiles) std::memcpy(tiles, L.tiles.data(), L.tiles.size() * sizeof(Tile));
+        if (perm) std::memcpy(perm, L.perm.data(), L.perm.size() * 4);
+    } catch (std::bad_alloc &) {
+        return fail(TOPK_E_NOMEM, "host allocation failed");
+    }
+    return TOPK_OK;
+}
+
 topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries) {
     if (!h || !boundaries) return fail(TOPK_E_INVALID, "NULL argument");
     std::memcpy(boundaries, h->bounds.data(), h->bounds.size() * 8);
@@ -769,11 +862,8 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
     if (n_rows) *n_rows = p.nrows;
     if (nnz) *nnz = p.nnz;
     try {
-        if (rowptr) {
-            std::vector<int32_t> t((size_t)p.nrows + 1);
-            CUDA_TRY(cudaMemcpy(t.data(), p.rowptr, t.size() * 4, cudaMemcpyDeviceToHost));
-            for (size_t i = 0; i < t.size(); ++i) rowptr[i] = t[i];
-        }
+        if (rowptr)
+            for (size_t i = 0; i < p.h_rowptr.size(); ++i) rowptr[i] = p.h_rowptr[i];
         if (col) CUDA_TRY(cudaMemcpy(col, p.col, (size_t)p.nnz * 4, cudaMemcpyDeviceToHost));
         if (val) {
             const size_t z = (size_t)p.nnz;
@@ -830,7 +920,7 @@ topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32
         for (int j = 0; j < nc; ++j) {
             const double s = (j < mm) ? sc[j] : 1.0 / bt[mm];
             for (int64_t r = 0; r < p.nrows; ++r)
-                V[(size_t)j * p.nrows + r] = s * to_double_elem(t.data(), (size_t)j * p.npad + r, h->vs);
+                V[(size_t)j * p.nrows + p.h_perm[(size_t)r]] = s * to_double_elem(t.data(), (size_t)j * p.npad + r, h->vs);
         }
     }
     CATCH(h)
@@ -849,7 +939,7 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
         for (Part &p : h->parts) {
             std::vector<char> buf((size_t)p.npad * es, 0);
             for (int64_t r = 0; r < p.nrows; ++r) {
-                const double v = x[p.row0 + r];
+                const double v = x[p.row0 + p.h_perm[(size_t)r]];
                 if (h->vs == TOPK_F64) reinterpret_cast<double *>(buf.data())[r] = v;
                 else if (h->vs == TOPK_F32) reinterpret_cast<float *>(buf.data())[r] = round_f32(v);
                 else reinterpret_cast<uint16_t *>(buf.data())[r] = round_bf16_bits(v);
@@ -865,8 +955,11 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
         if (h->comm) exch_vec_norm(h);
         for (Part &p : h->parts) h->spmv_only(h, p);
         CUDA_TRY(cudaStreamSynchronize(h->stream));
-        for (Part &p : h->parts)
-            CUDA_TRY(cudaMemcpy(y + p.row0, p.y_dbg, (size_t)p.nrows * 8, cudaMemcpyDeviceToHost));
+        for (Part &p : h->parts) {
+            std::vector<double> t((size_t)p.nrows);
+            CUDA_TRY(cudaMemcpy(t.data(), p.y_dbg, (size_t)p.nrows * 8, cudaMemcpyDeviceToHost));
+            for (int64_t r = 0; r < p.nrows; ++r) y[p.row0 + p.h_perm[(size_t)r]] = t[(size_t)r];
+        }
     }
     CATCH(h)
     return TOPK_OK;

@@ -12,6 +12,7 @@ from conftest import ROOT, has_gpu
 
 import oracle as O
 import synthgen as S
+import paper_2201_07498_b200 as T
 
 
 def header_symbols():
@@ -93,3 +94,45 @@ def test_create_argument_errors_precede_device():
     with pytest.raises(T.TopkError) as e:
         T.TopkEig(asym, 1, "f64", "f64")
     assert e.value.status == 3
+
+
+# ---------------------------------------------------------------- host layout (no device)
+@pytest.mark.parametrize("G", [1, 2, 3])
+@pytest.mark.parametrize("storage,dtype", [("f64", "f64"), ("f32", "f32"), ("f32", "bf16"), ("bf16", "bf16")])
+def test_plan_layout_bit_exact_vs_oracle(G, storage, dtype):
+    """Rows a3-a4: the library's host layout (what create
+    uploads) equals the oracle's, bit for bit: hub-first row order, remapped
+    columns with the hot bit, stored values and the SpMV tile table."""
+    A = S.rmat(13, 120_000, 5)  # long rows (> 1024 nnz) present
+    b = O.partition(A.rowptr, G)
+    for g in range(G):
+        rp, col, val, npad, tiles, perm = T.plan_layout(A, G, g, storage, dtype)
+        orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, b, g, dtype, storage=storage,
+                                                 with_perm=True)
+        assert npad == onpad
+        assert np.array_equal(perm, operm)
+        assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+        assert np.array_equal(val.view(np.uint64), oval.view(np.uint64))
+        assert np.array_equal(tiles, O.tiles(orp, 1024))
+
+
+def test_tile_table_properties():
+    """Every nonzero of every non-empty row is covered exactly once; packed
+    tiles hold whole rows and <= 1024 nonzeros; long rows are split in order."""
+    A = S.rmat(13, 120_000, 5)
+    rp = A.rowptr
+    t = O.tiles(rp, 1024)
+    nz_rows = np.flatnonzero(np.diff(rp) > 0)
+    cover = np.zeros(rp[-1], np.int32)
+    assert (t[:, 3] >= 0).any(), "fixture should contain long rows"
+    for zb, cnt, jb, lid in t:
+        assert 1 <= cnt <= 1024
+        cover[zb:zb + cnt] += 1
+        r = nz_rows[jb]
+        if lid < 0:
+            assert rp[r] == zb
+            end = zb + cnt
+            assert end in rp  # whole rows only
+        else:
+            assert rp[r] <= zb < rp[r + 1] and zb + cnt <= rp[r + 1]
+    assert (cover == 1).all()

@@ -72,7 +72,8 @@ def test_layout_bit_exact_c1(T, c1, G, dtype):
         assert np.array_equal(b, O.partition(csr.rowptr, G))
         for g in range(G):
             rp, col, val, npad = h.layout(g)
-            orp, ocol, oval, onpad = O.layout(csr.rowptr, csr.col, csr.val, G, b, g, dtype)
+            orp, ocol, oval, onpad = O.layout(csr.rowptr, csr.col, csr.val, G, b, g, dtype,
+                                              storage=dtype if dtype != "bf16" else "f32")
             assert npad == onpad
             assert np.array_equal(rp, orp)
             assert np.array_equal(col, ocol)
@@ -102,7 +103,9 @@ def test_spmv_parity(T, c1, c3s, name, storage, vals, G):
         y = h.debug_spmv(x)
     xr = x.astype(np.float32).astype(np.float64) if storage == "f32" else x
     if vals == "bf16":
-        _, _, vb, _ = O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16")
+        # bf16-rounded values in the original order (no hot rows -> identity row order)
+        _, _, vb, _ = O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16",
+                               hot=np.zeros(A.n, np.uint8))
         av = vb
     else:
         av = A.val if vals == "f64" else A.val.astype(np.float32).astype(np.float64)
@@ -176,7 +179,8 @@ def test_rmat_parity(T, c3s, K, m, storage, compute, vals):
     A = c3s
     av = A.val
     if vals == "bf16":  # generator weights are bf16-exact: the matrix is unchanged
-        assert np.array_equal(O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16")[2], A.val)
+        assert np.array_equal(O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16",
+                                       hot=np.zeros(A.n, np.uint8))[2], A.val)
     ref = O.solve(A.rowptr, A.col, av, K=K, m=m, seed=7, tau=O.TAU["f64"])
     r = T.solve(A, K, storage=storage, compute=compute, m=m, seed=7, values_storage=vals)
     th = T_all(T, A, K, storage, compute, m, 7, values_storage=vals)

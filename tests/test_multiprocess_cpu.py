@@ -1,0 +1,95 @@
+"""Host-side logic of the N > 1 path on CPU: two processes (torch.distributed,
+gloo, world_size 2) each plan their own part through the host-only C ABI
+(topk_eig_plan_partition / topk_eig_plan_layout), exactly what a rank does in
+topk_eig_create, and run the paper's per-iteration exchange protocol
+(replicated v_i, alpha / beta partial sums) with numpy on
+their layout. Checks: every rank derives the same boundaries; the parts'
+layouts equal the oracle's; the padded-slot allgather + remapped columns give
+the global SpMV; alpha and ||w||^2 summed from rank-ordered partials agree on
+both ranks bitwise and with the single-part value to rounding."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import synthgen as S
+
+WORLD = 2
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import paper_2201_07498_b200 as T
+        A = S.rmat(12, 40_000, 12)
+        G = WORLD
+        b = T.plan_partition(A.rowptr, G)
+        allb = [torch.zeros(G + 1, dtype=torch.int64) for _ in range(G)]
+        dist.all_gather(allb, torch.from_numpy(b))
+        same_b = all(np.array_equal(x.numpy(), b) for x in allb)
+        rp, col, val, npad, tiles, perm = T.plan_layout(A, G, rank, "f64")
+        orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, O.partition(A.rowptr, G), rank,
+                                                 "f64", with_perm=True)
+        layout_ok = (np.array_equal(rp, orp) and np.array_equal(col, ocol) and np.array_equal(val, oval)
+                     and npad == onpad and np.array_equal(perm, operm))
+        # replicated v_i: each rank publishes its padded slot
+        v = O.v1(7, A.n)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        slot = np.zeros(npad)
+        slot[: r1 - r0] = v[r0 + perm]  # part vectors live in hub-first position order
+        slots = [torch.zeros(npad, dtype=torch.float64) for _ in range(G)]
+        dist.all_gather(slots, torch.from_numpy(slot))
+        replica = torch.cat(slots).numpy()
+        # local SpMV on the remapped columns, then the alpha partial (Alg.1 l.9-10)
+        cidx = col & 0x7FFFFFFF  # strip the hot-column bit
+        y = np.array([np.dot(val[rp[r]:rp[r + 1]], replica[cidx[rp[r]:rp[r + 1]]]) for r in range(r1 - r0)])
+        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(G)]
+        vloc = v[r0 + perm]
+        dist.all_gather(parts, torch.tensor([np.dot(y, vloc)], dtype=torch.float64))
+        alpha = 0.0
+        for p in parts:  # rank order (reading Q16)
+            alpha += float(p[0])
+        w = y - alpha * vloc
+        nparts = [torch.zeros(1, dtype=torch.float64) for _ in range(G)]
+        dist.all_gather(nparts, torch.tensor([np.dot(w, w)], dtype=torch.float64))
+        wn = 0.0
+        for p in nparts:
+            wn += float(p[0])
+        yg = O.spmv(A.rowptr, A.col, A.val, v)
+        q.put((rank, same_b, layout_ok, y, alpha, wn, float(np.dot(yg, v)), yg[r0 + perm]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_plan_and_exchange_protocol():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda t: t[0])
+    for rank, same_b, layout_ok, y, alpha, wn, alpha_g, yg in out:
+        assert same_b, "ranks derived different partitions"
+        assert layout_ok, f"rank {rank} layout differs from the oracle's"
+        assert np.abs(y - yg).max() <= 1e-12 * max(1.0, np.abs(yg).max())
+        assert abs(alpha - alpha_g) <= 1e-12 * max(1.0, abs(alpha_g))
+    # scalars identical on every rank (rank-ordered sums of the same partials)
+    assert out[0][4] == out[1][4] and out[0][5] == out[1][5]

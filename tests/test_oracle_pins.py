@@ -129,30 +129,66 @@ def test_p9_partition_invalid():
 @pytest.mark.parametrize("G", [1, 2, 3, 5])
 @pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
 def test_layout_reassembles_matrix(G, dtype):
-    """Concatenated partitions, columns un-remapped, give back M (values rounded)."""
+    """Concatenated partitions, rows and columns mapped back through the
+    hub-first positions, give back M (values rounded)."""
     rp, c, v = er_csr(500, 3000, 11)
     b = O.partition(rp, G)
     npad_expect = int(math.ceil(max(np.diff(b)) / 64) * 64)
-    rows_all, cols_all, vals_all = [], [], []
-    for g in range(G):
-        lrp, lc, lv, npad = O.layout(rp, c, v, G, b, g, dtype)
+    hot = O.hot_columns(rp, 37)
+    parts = [O.layout(rp, c, v, G, b, g, dtype, hot=hot, with_perm=True) for g in range(G)]
+    perms = [pt[4] for pt in parts]
+    dense = np.zeros((500, 500))
+    np.add.at(dense, (np.repeat(np.arange(500), np.diff(rp)), c), v)
+    got = np.zeros((500, 500))
+    for g, (lrp, lc, lv, npad, perm) in enumerate(parts):
         assert npad == npad_expect
         assert lrp[0] == 0 and len(lrp) == b[g + 1] - b[g] + 1
-        owner = lc // npad
-        local = lc % npad
+        assert sorted(perm) == list(range(b[g + 1] - b[g]))
+        flag = lc < 0  # hot-column bit 31
+        lc = lc & 0x7FFFFFFF
+        owner, local = lc // npad, lc % npad
         assert np.all(local < np.diff(b)[owner])
-        rows_all.append(np.repeat(np.arange(b[g], b[g + 1]), np.diff(lrp)))
-        cols_all.append(b[owner] + local)
-        vals_all.append(lv)
-    assert np.array_equal(np.concatenate(rows_all), np.repeat(np.arange(500), np.diff(rp)))
-    assert np.array_equal(np.concatenate(cols_all), c)
-    lv = np.concatenate(vals_all)
+        gcol = np.array([b[o] + perms[o][q] for o, q in zip(owner, local)], np.int64)
+        assert np.array_equal(flag, hot[gcol].astype(bool))
+        grow = b[g] + np.repeat(perm, np.diff(lrp))
+        np.add.at(got, (grow, gcol), lv)
     if dtype == "f64":
-        assert np.array_equal(lv, v)
+        assert np.array_equal(got, dense)
     elif dtype == "f32":
-        assert np.array_equal(lv, v.astype(np.float32).astype(np.float64))
+        assert np.array_equal(got, dense.astype(np.float32).astype(np.float64))
     else:
-        check_bf16_rounding(v, lv)
+        nz = dense != 0
+        check_bf16_rounding(dense[nz], got[nz])
+
+
+def test_hub_first_positions_brute_force():
+    """Inside each part: hot rows first by (degree desc, index asc), then the
+    other rows ascending."""
+    rp, c, v = er_csr(300, 200, 3)
+    deg = np.diff(rp)
+    assert (deg == 0).any()
+    hot = O.hot_columns(rp, 23)
+    for G in (1, 2, 3):
+        b = O.partition(rp, G)
+        pos = O.positions(rp, G, b, hot)
+        for g in range(G):
+            rows = list(range(b[g], b[g + 1]))
+            order = sorted([r for r in rows if hot[r]], key=lambda r: (-deg[r], r)) + \
+                [r for r in rows if not hot[r] and deg[r] > 0] + [r for r in rows if deg[r] == 0]
+            assert [pos[r] for r in order] == list(range(len(rows)))
+
+
+def test_hot_columns_are_the_largest_degrees():
+    """Hot set = top-H non-empty columns by (degree desc, index asc), by brute force."""
+    rp, c, v = er_csr(500, 300, 11)
+    deg = np.diff(rp)
+    assert (deg == 0).any(), "fixture should contain empty rows"
+    for H in (0, 1, 17, 500):
+        hot = O.hot_columns(rp, H)
+        order = sorted([r for r in range(500) if deg[r] > 0], key=lambda r: (-deg[r], r))
+        expect = np.zeros(500, np.uint8)
+        expect[order[:H]] = 1
+        assert np.array_equal(hot, expect)
 
 
 def check_bf16_rounding(x, r):
