@@ -161,23 +161,26 @@ topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t
 /* Host-only per-part layout (rows a1, a3, a4 without a device): canonicalise A,
  * partition it by rule P into G parts and lay out part g exactly as
  * topk_eig_create uploads it for vector storage `storage` (the hot-row count
- * depends on it) and matrix values rounded to `values_storage`:
- *   rowptr (host, n_g+1 int64): rows in the part's hub-first order
- *   col    (host, z_g int32): column c -> owner(c) * n_pad + position of c in its
- *          owner's order, bit 31 set for hot columns
- *   val    (host, z_g doubles): stored values
- *   tiles  (host, 4 int32 per SpMV tile: nz_begin, cnt, end_begin, long_id)
- *   perm   (host, n_g int32): part-local original row at each position
- * Any output array may be NULL; n_pad, n_rows, nnz, ntiles (host int64 out, may
- * be NULL) give the sizes. Used by the multi-process CPU tests (each rank plans
- * its own part). Errors as in create. */
+ * depends on it) and matrix values rounded to `values_storage`.
+ *   sizes  (host, 9 int64 out): n_pad, n_rows, nnz, n_nonempty, nbig, nchunks,
+ *          nslices, nitems, nphys
+ *   logical CSR in degree order: rowptr (n_rows+1 int64), col (nnz int32 device
+ *          column entries: cold q*n_pad+pos, hot bit31|hot index), val (nnz
+ *          doubles = stored values), perm (n_rows int32: original part-local row
+ *          at each position)
+ *   physical SpMV format: pcol (nphys int32), pval (nphys doubles), chunks (4
+ *          int32 each: row, first, count, long id), sell (2 int32 per slice:
+ *          base, width), items (2 int32 per SELL work item: first, end slice)
+ * Every array pointer may be NULL. Used by the multi-process CPU tests (each
+ * rank plans its own part). Errors as in create. */
 topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g, topk_dtype_t storage,
-                                   topk_dtype_t values_storage, int64_t *n_pad, int64_t *n_rows,
-                                   int64_t *nnz, int64_t *ntiles, int64_t *rowptr, int32_t *col,
-                                   double *val, int32_t *tiles, int32_t *perm);
+                                   topk_dtype_t values_storage, int64_t *sizes, int64_t *rowptr,
+                                   int32_t *col, double *val, int32_t *perm, int32_t *pcol, double *pval,
+                                   int32_t *chunks, int32_t *sell, int32_t *items);
 
 /* Per kernel class device time of the last solve (requires opts.profile = 1):
- * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz pass 0 (norms), 6 ritz pass 1 (output).
+ * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz pass 0 (norms), 6 ritz pass 1 (output),
+ * 7 unpermute (output back to the original row order).
  * ms (host, 8 doubles): summed milliseconds; launches (host, 8 int32): launch counts.
  * Events bracket each launch on the handle's stream (the stream the kernels run on). */
 topk_status_t topk_eig_kernel_times(topk_eig_t h, double *ms, int32_t *launches);
@@ -185,10 +188,10 @@ topk_status_t topk_eig_kernel_times(topk_eig_t h, double *ms, int32_t *launches)
 /* ---- test/debug exports (same ABI; documented unstable) ---- */
 /* boundaries: host, G+1 int64 out */
 topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries);
-/* Part p (0 <= p < local parts) layout as uploaded: rowptr host (n_p+1 int64, hub-first
- * row order), col host (z_p int32, remapped to the padded replica + hot bit 31), val host
- * (z_p doubles = stored values), n_pad out, sizes out (n_p, z_p). Any pointer may be NULL
- * to query sizes only. */
+/* Part p (0 <= p < local parts) logical layout, reassembled from the uploaded physical
+ * arrays: rowptr host (n_p+1 int64, degree row order), col host (z_p int32 device column
+ * entries, see topk_eig_plan_layout), val host (z_p doubles = stored values), n_pad out,
+ * sizes out (n_p, z_p). Any pointer may be NULL to query sizes only. */
 topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr, int32_t *col,
                                      double *val, int64_t *n_pad, int64_t *n_rows,
                                      int64_t *nnz);

@@ -50,10 +50,8 @@ def _load():
             "orc_coo_to_csr": (I64, [I64, I64, P, P, P, P, P, P]),
             "orc_is_symmetric": (ctypes.c_int, [I64, P, P, P]),
             "orc_partition": (ctypes.c_int, [I64, P, I32, P]),
-            "orc_hot_columns": (ctypes.c_int, [I64, P, I64, P]),
-            "orc_positions": (ctypes.c_int, [I64, P, I32, P, P, P]),
-            "orc_layout": (I64, [I64, P, P, P, I32, P, I32, ctypes.c_int, P, P, P, P, P, P]),
-            "orc_tiles": (I64, [I64, P, I32, P]),
+            "orc_positions": (ctypes.c_int, [I64, P, I32, P, P]),
+            "orc_layout": (I64, [I64, P, P, P, I32, P, I32, ctypes.c_int, P, P, P, P, P]),
             "orc_v1": (None, [U64, I64, P]),
             "orc_spmv": (None, [I64, P, P, P, P, P]),
             "orc_lanczos": (I64, [I64, P, P, P, P, I32, I32, D, P, P, P, P]),
@@ -112,64 +110,33 @@ def partition(rowptr, G: int) -> np.ndarray:
     return b
 
 
-HOT_BYTES = 192 * 1024  # hot rows fill ~192 KB of x
-_SBYTES = {"f64": 8, "f32": 4, "bf16": 2}
-
-
-def hot_count(n: int, storage: str) -> int:
-    return min(n, HOT_BYTES // _SBYTES[storage])
-
-
-def hot_columns(rowptr, H: int) -> np.ndarray:
-    """Columns of the H largest degrees (ties: lower index), as a uint8 mask."""
-    rowptr = _c(rowptr, np.int64)
-    n = len(rowptr) - 1
-    hot = np.zeros(max(n, 1), np.uint8)
-    _load().orc_hot_columns(n, _p(rowptr), H, _p(hot))
-    return hot[:n]
-
-
-def positions(rowptr, G: int, b, hot) -> np.ndarray:
-    """Hub-first position of every row inside its part."""
-    rowptr, b, hot = _c(rowptr, np.int64), _c(b, np.int64), _c(hot, np.uint8)
+def positions(rowptr, G: int, b) -> np.ndarray:
+    """Degree-order position of every row inside its part."""
+    rowptr, b = _c(rowptr, np.int64), _c(b, np.int64)
     n = len(rowptr) - 1
     pos = np.zeros(max(n, 1), np.int32)
-    _load().orc_positions(n, _p(rowptr), G, _p(b), _p(hot), _p(pos))
+    _load().orc_positions(n, _p(rowptr), G, _p(b), _p(pos))
     return pos[:n]
 
 
-def layout(rowptr, col, val, G: int, b, g: int, dtype: str = "f64", storage: str | None = None,
-           hot=None, with_perm: bool = False):
-    """O2: per-partition local CSR (hub-first row order, rebased rowptr, padded-
-    remapped columns with the hot-column bit 31, values rounded to dtype,
-    returned as f64) and n_pad; storage = vector storage dtype (sets the hot
-    count; default dtype). with_perm: also return the position -> row map."""
+def layout(rowptr, col, val, G: int, b, g: int, dtype: str = "f64", with_perm: bool = False):
+    """O2: per-partition local CSR (degree row order, rebased rowptr, columns
+    remapped into the padded replica, values rounded to dtype, returned as f64)
+    and n_pad; with_perm: also return the position -> original row map."""
     rowptr, col, val, b = (_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64),
                            _c(b, np.int64))
     n = len(rowptr) - 1
-    if hot is None:
-        hot = hot_columns(rowptr, hot_count(n, storage or dtype))
-    hot = _c(hot, np.uint8)
-    pos = positions(rowptr, G, b, hot)
+    pos = positions(rowptr, G, b)
     ng = int(b[g + 1] - b[g])
     zg = int(rowptr[b[g + 1]] - rowptr[b[g]])
     lrp = np.zeros(ng + 1, np.int64)
     lc = np.zeros(max(zg, 1), np.int32)
     lv = np.zeros(max(zg, 1), np.float64)
     perm = np.zeros(max(ng, 1), np.int32)
-    npad = _load().orc_layout(n, _p(rowptr), _p(col), _p(val), G, _p(b), g, _DT[dtype], _p(hot),
-                              _p(pos), _p(lrp), _p(lc), _p(lv), _p(perm))
+    npad = _load().orc_layout(n, _p(rowptr), _p(col), _p(val), G, _p(b), g, _DT[dtype], _p(pos),
+                              _p(lrp), _p(lc), _p(lv), _p(perm))
     out = (lrp, lc[:zg].copy(), lv[:zg].copy(), int(npad))
     return out + (perm[:ng].copy(),) if with_perm else out
-
-
-def tiles(lrowptr, T: int = 1024) -> np.ndarray:
-    """O2 tile table of a part's local rowptr: int32 [ntiles, 4]."""
-    lrp = _c(lrowptr, np.int64)
-    nt = _load().orc_tiles(len(lrp) - 1, _p(lrp), T, None)
-    out = np.zeros((max(nt, 1), 4), np.int32)
-    _load().orc_tiles(len(lrp) - 1, _p(lrp), T, _p(out))
-    return out[:nt]
 
 
 def v1(seed: int, n: int) -> np.ndarray:

@@ -153,17 +153,13 @@ static double round_to_dtype(double x, int dtype) {
 }
 
 /* O2 (layout). Per-partition CSR of partition g (rows of M_g;
- * v_i replicated): rows of the part in hub-first order (orc_positions), local
+ * v_i replicated): rows of the part in degree order (orc_positions), local
  * rowptr rebased to 0; columns remapped into the padded replica
  * c' = g(c) * n_pad + pos[c] with n_pad = round_up(max_g n_g, 64) (SURVEY.md
- * 8(e) "v1 = padded"), bit 31 set for hot columns; values rounded to the
+ * 8(e) "v1 = padded"); values rounded to the
  * storage dtype (out_val receives the rounded values as f64, their exact
  * value); out_perm[p] = part-local original row at position p. */
-/* Hot-column flag (a layout hint, not a paper construct):
- * the H non-empty columns of largest degree (= row nnz, M symmetric), equal
- * degrees by lower index, carry bit 31 in the device column array. Plain
- * selection: sort all columns by (degree descending, index ascending), mark the
- * first H that are non-empty. */
+/* (degree-descending comparator shared by the layout functions below) */
 static const int64_t *g_deg_rowptr;
 static int cmp_deg_desc(const void *pa, const void *pb) {
     int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
@@ -171,52 +167,30 @@ static int cmp_deg_desc(const void *pa, const void *pb) {
     if (da != db) return da > db ? -1 : 1;
     return a < b ? -1 : (a > b ? 1 : 0);
 }
-int orc_hot_columns(int64_t n, const int64_t *rowptr, int64_t H, uint8_t *hot) {
-    int64_t *idx = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
-    if (!idx) return ORC_E_NOMEM;
-    for (int64_t i = 0; i < n; ++i) { idx[i] = i; hot[i] = 0; }
-    g_deg_rowptr = rowptr;
-    qsort(idx, (size_t)n, sizeof(int64_t), cmp_deg_desc);
-    /* empty rows (degree 0) sort last and are never hot */
-    for (int64_t i = 0; i < H && i < n && rowptr[idx[i] + 1] > rowptr[idx[i]]; ++i) hot[idx[i]] = 1;
-    free(idx);
-    return ORC_OK;
-}
 
-/* Hub-first local order (a layout choice, not a paper
- * construct): inside part q the hot rows come first, by (degree descending,
- * index ascending), then the other non-empty rows ascending, then the empty
- * rows ascending.
- * pos[r] = position of global row r inside its part. */
-int orc_positions(int64_t n, const int64_t *rowptr, int32_t G, const int64_t *b, const uint8_t *hot,
-                  int32_t *pos) {
+
+/* Degree order (a layout choice, not a paper construct):
+ * inside part q the rows are sorted by (degree descending, index ascending);
+ * empty rows therefore come last. pos[r] = position of global row r inside its
+ * part. */
+int orc_positions(int64_t n, const int64_t *rowptr, int32_t G, const int64_t *b, int32_t *pos) {
     (void)n;
     for (int32_t q = 0; q < G; ++q) {
-        int64_t nh = 0;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (hot[r]) ++nh;
-        int64_t *hr = (int64_t *)malloc((size_t)(nh > 0 ? nh : 1) * sizeof(int64_t));
-        if (!hr) return ORC_E_NOMEM;
-        int64_t k = 0;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (hot[r]) hr[k++] = r;
+        int64_t nr = b[q + 1] - b[q];
+        int64_t *rows = (int64_t *)malloc((size_t)(nr > 0 ? nr : 1) * sizeof(int64_t));
+        if (!rows) return ORC_E_NOMEM;
+        for (int64_t i = 0; i < nr; ++i) rows[i] = b[q] + i;
         g_deg_rowptr = rowptr;
-        qsort(hr, (size_t)nh, sizeof(int64_t), cmp_deg_desc);
-        int32_t p = 0;
-        for (int64_t i = 0; i < nh; ++i) pos[hr[i]] = p++;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (!hot[r] && rowptr[r + 1] > rowptr[r]) pos[r] = p++;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (rowptr[r + 1] == rowptr[r]) pos[r] = p++;
-        free(hr);
+        qsort(rows, (size_t)nr, sizeof(int64_t), cmp_deg_desc);
+        for (int64_t i = 0; i < nr; ++i) pos[rows[i]] = (int32_t)i;
+        free(rows);
     }
     return ORC_OK;
 }
 
 int64_t orc_layout(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
-                   int32_t G, const int64_t *b, int32_t g, int dtype, const uint8_t *hot,
-                   const int32_t *pos, int64_t *out_rowptr, int32_t *out_col, double *out_val,
-                   int32_t *out_perm) {
+                   int32_t G, const int64_t *b, int32_t g, int dtype, const int32_t *pos,
+                   int64_t *out_rowptr, int32_t *out_col, double *out_val, int32_t *out_perm) {
     (void)n;
     int64_t npad = 0;
     for (int32_t p = 0; p < G; ++p)
@@ -232,7 +206,6 @@ int64_t orc_layout(int64_t n, const int64_t *rowptr, const int32_t *col, const d
             int32_t owner = 0;
             while (!(c >= b[owner] && c < b[owner + 1])) ++owner;
             uint32_t cc = (uint32_t)(owner * npad + pos[c]);
-            if (hot[c]) cc |= 0x80000000u;
             out_col[o] = (int32_t)cc;
             out_val[o] = round_to_dtype(val[k], dtype);
         }
@@ -241,57 +214,6 @@ int64_t orc_layout(int64_t n, const int64_t *rowptr, const int32_t *col, const d
     return npad;
 }
 
-/* O2 (tile table; DESIGN.md section 2 "tiles", not a paper construct: the
- * SpMV work decomposition whose bit-exactness the parity contract checks).
- * Definition: walk the non-empty rows of the part in order. A row with more
- * than T nonzeros is a "long row" and becomes ceil(len/T) chunks of T
- * nonzeros (last chunk shorter), each its own tile. Otherwise a tile starts at
- * this row and takes following non-empty rows (empty rows are skipped, they
- * own no tile) as long as none of them is long and the tile's nonzeros stay
- * <= T. Tile record: {first nonzero, nonzero count, index of its first row in
- * the list of non-empty rows, long-row ordinal or -1}. Returns the count. */
-int64_t orc_tiles(int64_t nrows, const int64_t *lrowptr, int32_t T, int32_t *out4) {
-    int64_t ntiles = 0, nonempty_before = 0, nlong = 0;
-    int64_t r = 0;
-    while (r < nrows) {
-        int64_t len = lrowptr[r + 1] - lrowptr[r];
-        if (len == 0) { ++r; continue; }
-        if (len > T) {
-            for (int64_t c = 0; c * T < len; ++c) {
-                int64_t first = lrowptr[r] + c * T;
-                int64_t cnt = len - c * T < T ? len - c * T : T;
-                if (out4) {
-                    out4[4 * ntiles + 0] = (int32_t)first;
-                    out4[4 * ntiles + 1] = (int32_t)cnt;
-                    out4[4 * ntiles + 2] = (int32_t)nonempty_before;
-                    out4[4 * ntiles + 3] = (int32_t)nlong;
-                }
-                ++ntiles;
-            }
-            ++nlong;
-            ++nonempty_before;
-            ++r;
-            continue;
-        }
-        int64_t first = lrowptr[r], first_index = nonempty_before, total = 0;
-        while (r < nrows) {
-            int64_t l = lrowptr[r + 1] - lrowptr[r];
-            if (l == 0) { ++r; continue; }
-            if (l > T || total + l > T) break;
-            total += l;
-            ++nonempty_before;
-            ++r;
-        }
-        if (out4) {
-            out4[4 * ntiles + 0] = (int32_t)first;
-            out4[4 * ntiles + 1] = (int32_t)total;
-            out4[4 * ntiles + 2] = (int32_t)first_index;
-            out4[4 * ntiles + 3] = -1;
-        }
-        ++ntiles;
-    }
-    return ntiles;
-}
 
 /* ------------------------------------------------------------------------ */
 /* O3. Random start vector ("L2-normalized random vector v_1";

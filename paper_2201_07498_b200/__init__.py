@@ -75,7 +75,7 @@ _SIGS = {
     "topk_eig_last_error": (ctypes.c_char_p, []),
     "topk_eig_nccl_id": (_S, [_P]),
     "topk_eig_plan_partition": (_S, [_P, _I64, _I32, _P]),
-    "topk_eig_plan_layout": (_S, [_P, _I32, _I32, _S, _S, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "topk_eig_plan_layout": (_S, [_P, _I32, _I32, _S, _S, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "topk_eig_export_partition": (_S, [_P, _P]),
     "topk_eig_export_layout": (_S, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "topk_eig_export_tridiag": (_S, [_P, _P, _P, _P, _P]),
@@ -137,22 +137,29 @@ def _matrix(A, keep: list) -> "_Matrix":
     return mat
 
 
-def plan_layout(A, G: int, g: int, storage: str = "f64", values_storage: str | None = None):
-    """Host-only layout of part g of G (no device): (rowptr, col, val, n_pad, tiles, perm)."""
+def plan_layout(A, G: int, g: int, storage: str = "f64", values_storage: str | None = None) -> dict:
+    """Host-only layout of part g of G (no device): the logical CSR in degree
+    order (rowptr, col, val, perm, n_pad) and the SpMV physical format (pcol,
+    pval, chunks [nchunks, 4], sell [nslices, 2], items [nitems, 2], nbig,
+    nnonempty) -- exactly what topk_eig_create uploads."""
     keep = []
     mat = _matrix(A, keep)
-    npad, nr, nz, nt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     st, vs = DTYPES[storage], DTYPES[values_storage or storage]
-    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, ctypes.byref(npad), ctypes.byref(nr),
-                                     ctypes.byref(nz), ctypes.byref(nt), None, None, None, None, None))
-    rp = np.zeros(nr.value + 1, np.int64)
-    c = np.zeros(max(nz.value, 1), np.int32)
-    v = np.zeros(max(nz.value, 1), np.float64)
-    t = np.zeros((max(nt.value, 1), 4), np.int32)
-    pm = np.zeros(max(nr.value, 1), np.int32)
-    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, None, None, None, None,
-                                     _ptr(rp), _ptr(c), _ptr(v), _ptr(t), _ptr(pm)))
-    return rp, c[:nz.value], v[:nz.value], npad.value, t[:nt.value], pm[:nr.value]
+    sz = np.zeros(9, np.int64)
+    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, _ptr(sz), *([None] * 9)))
+    npad, nr, nz, nne, nbig, nch, nsl, nit, nph = (int(v) for v in sz)
+    out = dict(n_pad=npad, nnonempty=nne, nbig=nbig,
+               rowptr=np.zeros(nr + 1, np.int64), col=np.zeros(max(nz, 1), np.int32),
+               val=np.zeros(max(nz, 1)), perm=np.zeros(max(nr, 1), np.int32),
+               pcol=np.zeros(max(nph, 1), np.int32), pval=np.zeros(max(nph, 1)),
+               chunks=np.zeros((max(nch, 1), 4), np.int32), sell=np.zeros((max(nsl, 1), 2), np.int32),
+               items=np.zeros((max(nit, 1), 2), np.int32))
+    _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, None, *[_ptr(out[k]) for k in (
+        "rowptr", "col", "val", "perm", "pcol", "pval", "chunks", "sell", "items")]))
+    for k, m in (("col", nz), ("val", nz), ("perm", nr), ("pcol", nph), ("pval", nph), ("chunks", nch),
+                 ("sell", nsl), ("items", nit)):
+        out[k] = out[k][:m]
+    return out
 
 
 @dataclass
@@ -225,7 +232,7 @@ class TopkEig:
         _check(_lib.topk_eig_sync(self._h, ctypes.byref(info)))
         return info.as_dict()
 
-    KERNEL_CLASSES = ("v1", "spmv", "step", "correct", "jacobi", "ritz_norms", "ritz_out")
+    KERNEL_CLASSES = ("v1", "spmv", "step", "correct", "jacobi", "ritz_norms", "ritz_out", "unperm")
 
     def kernel_times(self) -> dict:
         """{class: (total ms, launches)} of the last solve (profile=True)."""

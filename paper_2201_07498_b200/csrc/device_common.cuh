@@ -80,8 +80,8 @@ __device__ __forceinline__ void round_back(CT (&v)[Vw<ST>::N]) {
 
 // ---- L1 cache-policy loads (read-only path) ----------------------------------
 // stream: data read exactly once per kernel (matrix col/val) must not displace
-// the x values kept in L1 -> L1::no_allocate. Gathers: hot columns evict-last,
-// the rest no_allocate (SpMV).
+// the x values kept in L1 -> L1::no_allocate; the SpMV gathers x with plain
+// (L1-allocating) __ldg, DESIGN.md section 7.
 __device__ __forceinline__ int4 ld_stream(const int4 *p) {
     int4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -104,32 +104,16 @@ __device__ __forceinline__ uint2 ld_stream(const uint2 *p) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
-template <typename T> __device__ __forceinline__ T ld_keep(const T *p);
 template <typename T> __device__ __forceinline__ T ld_noalloc(const T *p);
-template <> __device__ __forceinline__ float ld_keep<float>(const float *p) {
-    float v;
-    asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
 template <> __device__ __forceinline__ float ld_noalloc<float>(const float *p) {
     float v;
     asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-template <> __device__ __forceinline__ double ld_keep<double>(const double *p) {
-    double v;
-    asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 template <> __device__ __forceinline__ double ld_noalloc<double>(const double *p) {
     double v;
     asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
-}
-template <> __device__ __forceinline__ bf16 ld_keep<bf16>(const bf16 *p) {
-    unsigned short v;
-    asm volatile("ld.global.nc.L1::evict_last.b16 %0, [%1];" : "=h"(v) : "l"(p));
-    return __ushort_as_bfloat16(v);
 }
 template <> __device__ __forceinline__ bf16 ld_noalloc<bf16>(const bf16 *p) {
     unsigned short v;

@@ -238,105 +238,25 @@ double bf16_bits_to_double(uint16_t b) {
     return (double)f;
 }
 
-static void build_tiles(const int32_t *rowptr, int64_t nrows, PartLayout &L) {
-    L.tiles.clear();
-    L.longrows.clear();
-    L.nzrow.clear();
-    const int64_t z = rowptr[nrows];
-    L.endbits.assign((size_t)(z / 32 + 2), 0u);
-    for (int64_t r = 0; r < nrows; ++r)
-        if (rowptr[r + 1] > rowptr[r]) {
-            const int64_t e = rowptr[r + 1] - 1;
-            L.endbits[(size_t)(e >> 5)] |= 1u << (e & 31);
-            L.nzrow.push_back((int32_t)r);
-        }
-    const int64_t nz_rows = (int64_t)L.nzrow.size();
-    int64_t j = 0;  // index into nzrow
-    while (j < nz_rows) {
-        const int32_t r = L.nzrow[(size_t)j];
-        const int64_t len = rowptr[r + 1] - rowptr[r];
-        if (len > kTileNnz) {  // long row: fixed chunks, finished by the last-arriving chunk
-            LongRow lr;
-            lr.row = r;
-            lr.first_tile = (int32_t)L.tiles.size();
-            lr.nchunks = (int32_t)((len + kTileNnz - 1) / kTileNnz);
-            lr.pad = 0;
-            for (int32_t c = 0; c < lr.nchunks; ++c) {
-                const int64_t b = rowptr[r] + (int64_t)c * kTileNnz;
-                L.tiles.push_back(Tile{(int32_t)b, (int32_t)std::min<int64_t>(kTileNnz, rowptr[r + 1] - b),
-                                       (int32_t)j, (int32_t)L.longrows.size()});
-            }
-            L.longrows.push_back(lr);
-            ++j;
-            continue;
-        }
-        const int64_t j0 = j, zb = rowptr[r];
-        while (j < nz_rows) {
-            const int32_t q = L.nzrow[(size_t)j];
-            if (rowptr[q + 1] - rowptr[q] > kTileNnz) break;
-            if (rowptr[q + 1] - zb > kTileNnz) break;
-            ++j;
-        }
-        const int32_t last = L.nzrow[(size_t)j - 1];
-        L.tiles.push_back(Tile{(int32_t)zb, (int32_t)(rowptr[last + 1] - zb), (int32_t)j0, -1});
-    }
-}
 
-std::vector<uint8_t> hot_columns(const Csr &m, int64_t H) {
-    const int64_t n = m.n;
-    std::vector<uint8_t> hot((size_t)n, 0);
-    if (H <= 0) return hot;
-    auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
-    std::vector<int64_t> idx;  // non-empty rows only: an empty row is never hot
-    idx.reserve((size_t)n);
-    for (int64_t r = 0; r < n; ++r)
-        if (deg(r) > 0) idx.push_back(r);
-    H = std::min<int64_t>(H, (int64_t)idx.size());
-    if (H <= 0) return hot;
-    std::nth_element(idx.begin(), idx.begin() + (H - 1), idx.end(), [&](int64_t a, int64_t b) {
-        const int64_t da = deg(a), db = deg(b);
-        return da != db ? da > db : a < b;
-    });
-    for (int64_t i = 0; i < H; ++i) hot[(size_t)idx[(size_t)i]] = 1;
-    return hot;
-}
 
-int64_t hot_count(int64_t n, int storage_bytes) {
-    return std::min<int64_t>(n, kHotBytes / std::max(1, storage_bytes));
-}
-
-void hub_first_order(const Csr &m, const int64_t *b, int32_t G, const uint8_t *hot,
-                     std::vector<int32_t> &pos) {
+void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos) {
     pos.assign((size_t)m.n, 0);
     auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
-#pragma omp parallel for schedule(dynamic, 1)
     for (int32_t q = 0; q < G; ++q) {
-        std::vector<int64_t> hr;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (hot && hot[(size_t)r]) hr.push_back(r);
-        std::sort(hr.begin(), hr.end(), [&](int64_t x, int64_t y) {
-            const int64_t dx = deg(x), dy = deg(y);
-            return dx != dy ? dx > dy : x < y;
-        });
-        int32_t p = 0;
-        for (int64_t r : hr) pos[(size_t)r] = p++;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (!(hot && hot[(size_t)r]) && deg(r) > 0) pos[(size_t)r] = p++;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r)
-            if (deg(r) == 0) pos[(size_t)r] = p++;
+        std::vector<int64_t> rows((size_t)(b[q + 1] - b[q]));
+        std::iota(rows.begin(), rows.end(), b[q]);
+        std::stable_sort(rows.begin(), rows.end(), [&](int64_t x, int64_t y) { return deg(x) > deg(y); });
+        for (size_t p = 0; p < rows.size(); ++p) pos[(size_t)rows[p]] = (int32_t)p;
     }
 }
 
-std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const uint8_t *hot,
-                                const int32_t *pos) {
+
+std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos) {
     std::vector<int32_t> cm((size_t)n);
     for (int32_t q = 0; q < G; ++q) {
 #pragma omp parallel for schedule(static)
-        for (int64_t c = b[q]; c < b[q + 1]; ++c) {
-            uint32_t cc = (uint32_t)(q * npad + pos[(size_t)c]);
-            if (hot && hot[(size_t)c]) cc |= kHotBit;
-            cm[(size_t)c] = (int32_t)cc;
-        }
+        for (int64_t c = b[q]; c < b[q + 1]; ++c) cm[(size_t)c] = (int32_t)(q * npad + pos[(size_t)c]);
     }
     return cm;
 }
@@ -345,8 +265,9 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
     const int64_t r0 = b[g], r1 = b[g + 1];
     const int64_t z0 = m.rowptr[(size_t)r0], z1 = m.rowptr[(size_t)r1];
-    if (z1 - z0 >= (1ll << 31) - kTileNnz) { err = "per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
+    if (z1 - z0 >= (1ll << 31) - (1ll << 26)) { err = "per-part nnz must be < 2^31 - 2^26"; return TOPK_E_INVALID; }
     if ((int64_t)G * npad >= (1ll << 31)) { err = "G * n_pad must be < 2^31"; return TOPK_E_INVALID; }
+    (void)G;
     out.row0 = r0;
     out.nrows = r1 - r0;
     out.npad = npad;
@@ -355,14 +276,18 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     for (int64_t r = r0; r < r1; ++r) out.perm[(size_t)pos[(size_t)r]] = (int32_t)(r - r0);
     out.rowptr.resize((size_t)(ng + 1));
     out.rowptr[0] = 0;
+    int64_t nne = 0;
     for (int64_t p = 0; p < ng; ++p) {
         const int64_t r = r0 + out.perm[(size_t)p];
-        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + (int32_t)(m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]);
+        const int64_t len = m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r];
+        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + (int32_t)len;
+        if (len > 0) nne = p + 1;
     }
-    out.col.resize((size_t)(z1 - z0));
-    out.val.resize((size_t)(z1 - z0));
-    // rows in hub-first order; entries of a row keep their (column-sorted) input
-    // order; column c -> owner(c) * npad + pos[c] (+ bit 31 if hot)
+    out.nnonempty = nne;
+    const int64_t z = z1 - z0;
+    out.col.resize((size_t)z);
+    out.val.resize((size_t)z);
+    // logical CSR: rows in degree order; entries of a row keep their (column-sorted) input order
 #pragma omp parallel for schedule(dynamic, 4096)
     for (int64_t p = 0; p < ng; ++p) {
         const int64_t r = r0 + out.perm[(size_t)p];
@@ -372,7 +297,61 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
             out.val[(size_t)o] = m.val[(size_t)k];
         }
     }
-    build_tiles(out.rowptr.data(), out.nrows, out);
+    // physical format: big rows (CSR prefix, chunked), then SELL-32 slices
+    int64_t nbig = 0;
+    while (nbig < nne && out.rowptr[(size_t)nbig + 1] - out.rowptr[(size_t)nbig] > kSellMaxLen) ++nbig;
+    out.nbig = (int32_t)nbig;
+    out.chunks.clear();
+    out.longrows.clear();
+    for (int64_t p = 0; p < nbig; ++p) {
+        const int32_t rb = out.rowptr[(size_t)p], len = out.rowptr[(size_t)p + 1] - rb;
+        const int32_t nch = (len + kChunkNnz - 1) / kChunkNnz;
+        const int32_t lid = nch > 1 ? (int32_t)out.longrows.size() : -1;
+        if (nch > 1) out.longrows.push_back(LongRow{(int32_t)p, (int32_t)out.chunks.size(), nch, 0});
+        for (int32_t c = 0; c < nch; ++c)
+            out.chunks.push_back(Chunk{(int32_t)p, rb + c * kChunkNnz, std::min(kChunkNnz, len - c * kChunkNnz), lid});
+    }
+    const int64_t zbig = out.rowptr[(size_t)nbig];
+    const int64_t nsl = (nne - nbig + 31) / 32;
+    out.sell.assign((size_t)(2 * nsl), 0);
+    int64_t phys = zbig;
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        const int64_t p0 = nbig + 32 * sl;
+        const int32_t w = out.rowptr[(size_t)p0 + 1] - out.rowptr[(size_t)p0];
+        out.sell[(size_t)(2 * sl)] = (int32_t)phys;
+        out.sell[(size_t)(2 * sl + 1)] = w;
+        phys += 32 * (int64_t)w;
+    }
+    if (phys >= (1ll << 31) - 256) { err = "padded per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
+    out.pcol.resize((size_t)phys);
+    out.pval.resize((size_t)phys);
+    std::copy(out.col.begin(), out.col.begin() + zbig, out.pcol.begin());
+    std::copy(out.val.begin(), out.val.begin() + zbig, out.pval.begin());
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        const int64_t base = out.sell[(size_t)(2 * sl)], w = out.sell[(size_t)(2 * sl + 1)];
+        for (int64_t i = 0; i < 32; ++i) {
+            const int64_t p = nbig + 32 * sl + i;
+            const int64_t rb = p < nne ? out.rowptr[(size_t)p] : 0;
+            const int64_t len = p < nne ? out.rowptr[(size_t)p + 1] - rb : 0;
+            for (int64_t e = 0; e < w; ++e) {
+                const size_t k = (size_t)(base + 32 * e + i);
+                out.pcol[k] = e < len ? out.col[(size_t)(rb + e)] : 0;
+                out.pval[k] = e < len ? out.val[(size_t)(rb + e)] : 0.0;
+            }
+        }
+    }
+    out.items.clear();
+    for (int64_t sl = 0; sl < nsl;) {
+        int64_t e = sl, width = 0;
+        while (e < nsl && (e == sl || width + out.sell[(size_t)(2 * e + 1)] <= kSellItemWidth)) {
+            width += out.sell[(size_t)(2 * e + 1)];
+            ++e;
+        }
+        out.items.push_back((int32_t)sl);
+        out.items.push_back((int32_t)e);
+        sl = e;
+    }
     return TOPK_OK;
 }
 

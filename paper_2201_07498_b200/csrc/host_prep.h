@@ -48,62 +48,68 @@ float round_f32(double x);
 uint16_t round_bf16_bits(double x);
 double bf16_bits_to_double(uint16_t b);
 
-// SpMV tile table (a4). A packed tile covers consecutive NON-EMPTY rows whose
-// nonzeros total <= kTileNnz (whole rows only); a row with more than kTileNnz
-// nonzeros is split into fixed kTileNnz chunks ("long row"). Empty rows belong
-// to no tile: their SpMV output is identically 0 (y is zeroed once at create).
-// Row ends are a bitmask over the part's nonzeros (bit k set iff k is the last
-// nonzero of its row). In the hub-first order the non-empty rows are positions
-// [0, n_nonempty), so the j-th row end of a tile is row end_begin + j and the
-// kernel never reads rowptr.
-constexpr int kTileNnz = 1024;
+// ---------------------------------------------------------------------------
+// Local row order of a part ("degree order"): the part's
+// rows sorted by (degree descending, original index ascending); empty rows
+// therefore come last and the non-empty rows are positions [0, n_nonempty).
+// Every part-local vector (Lanczos basis, y, w, the replica slot) is stored in
+// this order; perm[p] is the original part-local row at position p.
+//
+// Device column entry of column c (owner part q, position p): q * n_pad + p, an
+// index into the replica (= the V column at G = 1). In degree order the hub
+// columns are the dense prefix of every slot, so the SpMV's plain L1-cached x
+// gathers keep them resident.
+// pos[r] = position of global row r inside its part's degree order.
+void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos);
+// colmap[c] = device column entry of global column c (one lookup per nonzero).
+std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos);
 
-struct Tile {
-    int32_t nz_begin;   // first nonzero (part-local) of the tile / chunk
-    int32_t cnt;        // nonzeros in the tile / chunk (<= kTileNnz)
-    int32_t end_begin;  // position (= index among non-empty rows) of the tile's first row
-    int32_t long_id;    // -1 packed; else index into the long-row table
+// ---------------------------------------------------------------------------
+// SpMV physical format (a4), derived from the logical CSR in degree order:
+//  * "big" rows (positions [0, nbig), degree > kSellMaxLen) stay CSR; their
+//    nonzeros are the first rowptr[nbig] entries of the physical arrays (same
+//    as the logical CSR). Each big row is cut into chunks of <= kChunkNnz; a
+//    warp reduces one chunk; a row with several chunks ("long row") is finished
+//    by its last-arriving chunk in chunk order.
+//  * the other non-empty rows form SELL-32 slices (sliced ELLPACK, C = 32,
+//    sigma = the whole part): slice s = rows nbig + 32 s .. + 31, width
+//    w_s = degree of its first row (rows are degree-sorted), stored column-major
+//    (entry e of slice row i at base_s + 32 e + i), padded with (col = 0,
+//    value 0). One lane per row, coalesced 128-byte loads, no reductions.
+//  * work items: one per chunk, then groups of consecutive slices with
+//    sum(w_s) <= kSellItemWidth (about <= 2048 padded nonzeros per item).
+constexpr int kSellMaxLen = 128;
+constexpr int kChunkNnz = 2048;
+constexpr int kSellItemWidth = 64;
+
+struct Chunk {       // big-row chunk
+    int32_t row;     // position of the row
+    int32_t z0;      // first physical nonzero
+    int32_t cnt;     // nonzeros (<= kChunkNnz)
+    int32_t long_id; // -1: the chunk is the whole row; else index into longrows
 };
 struct LongRow {
     int32_t row;
-    int32_t first_tile;
+    int32_t first_chunk;
     int32_t nchunks;
     int32_t pad;
 };
 
 struct PartLayout {
-    int64_t row0 = 0, nrows = 0, npad = 0;
-    std::vector<int32_t> rowptr;    // nrows+1, rebased
-    hvec<int32_t> col;              // remapped into the padded replica index space
-    hvec<double> val;               // values (f64 source; rounded to the value dtype at upload)
-    std::vector<Tile> tiles;
-    std::vector<LongRow> longrows;
-    std::vector<uint32_t> endbits;  // ceil(nnz / 32) + 1 words
-    std::vector<int32_t> nzrow;     // positions of the non-empty rows, ascending
+    int64_t row0 = 0, nrows = 0, npad = 0, nnonempty = 0;
+    std::vector<int32_t> rowptr;    // nrows+1, logical CSR in degree order
+    hvec<int32_t> col;              // logical, device column entries
+    hvec<double> val;               // logical values (f64 source; rounded at upload)
     std::vector<int32_t> perm;      // nrows: part-local original row at each position
+    // physical SpMV format
+    int32_t nbig = 0;
+    hvec<int32_t> pcol;             // physical col (big-row CSR prefix, then SELL slices)
+    hvec<double> pval;              // physical values
+    std::vector<Chunk> chunks;
+    std::vector<LongRow> longrows;
+    std::vector<int32_t> sell;      // 2 per slice: base, width
+    std::vector<int32_t> items;     // 2 per SELL work item: first slice, end slice
 };
-
-// Hot rows/columns: the H non-empty rows of largest degree
-// (row nnz = column nnz, M symmetric), ties by lower index, H = kHotBytes /
-// (vector storage bytes) so their x values fill ~192 KB of L1. Their col entries
-// carry bit 31 so the SpMV gathers them evict-last into L1 while all other
-// gathers bypass L1 allocation. Local row order of a part ("hub-first"): hot rows
-// (degree descending, index ascending), then the other non-empty rows ascending,
-// then the empty rows ascending -- so the hot x values are packed densely in
-// 32-byte sectors and the non-empty rows are exactly positions [0, n_nonempty).
-constexpr int64_t kHotBytes = 192 * 1024;
-constexpr uint32_t kHotBit = 0x80000000u;
-int64_t hot_count(int64_t n, int storage_bytes);
-std::vector<uint8_t> hot_columns(const Csr &m, int64_t H);
-// pos[r] = position of global row r inside its part's hub-first order;
-// perm_g[p] = part-local original row at position p.
-void hub_first_order(const Csr &m, const int64_t *b, int32_t G, const uint8_t *hot,
-                     std::vector<int32_t> &pos);
-
-// colmap[c] = owner(c) * npad + pos[c], | kHotBit if c is hot: the device column
-// index of global column c (one lookup per nonzero in build_part).
-std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const uint8_t *hot,
-                                const int32_t *pos);
 
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err);

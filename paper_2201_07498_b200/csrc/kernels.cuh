@@ -25,8 +25,9 @@
 namespace topk {
 
 constexpr int kNT = 256;  // threads per block for the streaming kernels
+constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no shared memory)
 constexpr int kRitzKB = 8;  // Ritz outputs per thread
-constexpr int kStepJB = 8;  // basis columns per multi-dot pass of k_step
+constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step
 
 struct LzState {
     double *alpha;      // [m]     alpha_1..alpha_m
@@ -147,31 +148,31 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// a7: SpMV + alpha partial (Alg.1 l.9-10), warp-per-tile segmented reduction.
-// A warp owns a tile of whole non-empty rows (<= kTileNnz nonzeros) and walks
-// it in rounds of 256 nonzeros: lane l holds 8 consecutive nonzeros (two
-// 16-byte col loads, vector value loads, all L1::no_allocate streaming; the
-// next round's columns and row-end bits are prefetched while the current round
-// gathers). x is gathered through L1: hot columns (bit 31, the hub-first
-// prefix of every slot) evict-last, the rest no_allocate. Products in the
-// compute dtype; a lane-serial + warp-wide segmented scan over the row-end
-// bitmask gives the row sums. Non-empty rows occupy positions [0, n_nonempty)
-// in order, so the j-th row end of a tile is row end_begin + j. Rows longer
-// than kTileNnz are chunked; the last-arriving chunk warp sums the chunk
-// partials in chunk order. Epilogue: y_r = s_i * sum (deferred normalisation),
-// stored once rounded, and the alpha partial sum_r y_r * v_i[r].
-// Deterministic: fixed shuffle trees and fixed orders everywhere.
+// a7: SpMV + alpha partial (Alg.1 l.9-10) on the physical format of
+// host_prep.h (rows in degree order):
+//  * big rows (degree > kSellMaxLen): warp per chunk of <= kChunkNnz nonzeros,
+//    lanes stride the row with coalesced loads, warp shuffle reduction; a row
+//    of several chunks is finished by its last-arriving chunk in chunk order;
+//  * SELL-32 slices: lane per row, entry e of the slice's 32 rows is one
+//    coalesced 128-byte load of col and of val, no reduction at all.
+// x gathers are plain L1-cached loads: in degree order the hub columns are the
+// dense prefix of x, so they stay L1-resident while col/val are streamed with
+// L1::no_allocate (measured on B200 to beat a shared-memory hub cache 2x, see
+// DESIGN.md section 7); C3's 16.8 MB x is L2-resident. Products
+// and sums in the compute dtype (reading Q14). Epilogue per row: y_r = s_i *
+// sum (deferred normalisation), stored once rounded, alpha partial
+// y_r * s_i * u_i[r]. Deterministic: fixed orders and shuffle trees.
 struct SpmvArgs {
-    const int32_t *col;
-    const void *val;
-    const uint32_t *endbits;
-    const Tile *tiles;
-    int ntiles;
-    const LongRow *longrows;
-    double *long_parts;   // [ntiles]
+    const int32_t *col;   // physical
+    const void *val;      // physical
+    const int4 *chunks;   // [nchunks] Chunk
+    const int4 *longrows; // [nlong] LongRow
+    const int2 *sell;     // [nslices] (base, width)
+    const int2 *items;    // [nitems] (first slice, end slice)
+    int nchunks, nitems, nbig, nnonempty, nlong;
+    double *long_parts;   // [nchunks]
     unsigned *long_cnt;   // [nlong]
     double *alpha_long;   // [nlong]
-    int nlong;
     const void *x;        // gather source: V column it-1 (G = 1) or the replica
     const void *ui;       // local u_it (V column it-1)
     void *y;              // v_tmp (Q2), storage dtype
@@ -183,196 +184,154 @@ struct SpmvArgs {
     int G, g;
 };
 
-// 8 consecutive matrix values (32-byte aligned group) converted to CT
-template <typename VT, typename CT> struct Val8;
-template <typename CT> struct Val8<float, CT> {
-    static __device__ __forceinline__ void load(const float *p, CT (&o)[8]) {
-        const float4 a = ld_stream(reinterpret_cast<const float4 *>(p));
-        const float4 b = ld_stream(reinterpret_cast<const float4 *>(p) + 1);
-        o[0] = (CT)a.x; o[1] = (CT)a.y; o[2] = (CT)a.z; o[3] = (CT)a.w;
-        o[4] = (CT)b.x; o[5] = (CT)b.y; o[6] = (CT)b.z; o[7] = (CT)b.w;
-    }
-};
-template <typename CT> struct Val8<double, CT> {
-    static __device__ __forceinline__ void load(const double *p, CT (&o)[8]) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double2 a = ld_stream(reinterpret_cast<const double2 *>(p) + q);
-            o[2 * q] = (CT)a.x;
-            o[2 * q + 1] = (CT)a.y;
-        }
-    }
-};
-template <typename CT> struct Val8<bf16, CT> {
-    static __device__ __forceinline__ void load(const bf16 *p, CT (&o)[8]) {
-        const int4 v = ld_stream(reinterpret_cast<const int4 *>(p));
-        const bf16 *e = reinterpret_cast<const bf16 *>(&v);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) o[q] = cvt<CT>(e[q]);
-    }
-};
-
-// x[c] for a remapped column entry: bit 31 set = hot column (kept in L1).
-template <typename ST, typename CT>
-__device__ __forceinline__ CT gather_x(const ST *__restrict__ x, int c) {
-    if (c < 0) return cvt<CT>(ld_keep<ST>(x + (c & 0x7FFFFFFF)));
-    return cvt<CT>(ld_noalloc<ST>(x + c));
+template <typename VT> __device__ __forceinline__ VT ld_val_stream(const VT *p);
+template <> __device__ __forceinline__ float ld_val_stream<float>(const float *p) { return ld_noalloc<float>(p); }
+template <> __device__ __forceinline__ double ld_val_stream<double>(const double *p) { return ld_noalloc<double>(p); }
+template <> __device__ __forceinline__ bf16 ld_val_stream<bf16>(const bf16 *p) { return ld_noalloc<bf16>(p); }
+__device__ __forceinline__ int ld_col_stream(const int32_t *p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
 template <typename VT, typename ST, typename CT>
-__global__ void __launch_bounds__(kNT, 4) k_spmv(SpmvArgs a, int it) {
-    constexpr int EPL = 8, RND = 32 * EPL;  // nonzeros per lane / per warp round
-    __shared__ CT red[kNT / 32];
-    __shared__ double redd[kNT / 32];
+__global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
+    __shared__ CT red[kSpmvNT / 32];
+    __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
 
     double sd;
     if (!lz_prologue(it, a.st, a.ex, a.G, sd)) return;
     const CT s = (CT)sd;
     const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int gwarp = (int)((blockIdx.x * kNT + threadIdx.x) >> 5);
-    const int nwarps = (int)(gridDim.x * (kNT / 32));
+    const int gwarp = (int)((blockIdx.x * kSpmvNT + threadIdx.x) >> 5);
+    const int nwarps = (int)(gridDim.x * (kSpmvNT / 32));
     const VT *__restrict__ val = reinterpret_cast<const VT *>(a.val);
+    const int32_t *__restrict__ col = a.col;
     const ST *__restrict__ x = reinterpret_cast<const ST *>(a.x);
     const ST *__restrict__ ui = reinterpret_cast<const ST *>(a.ui);
     ST *__restrict__ y = reinterpret_cast<ST *>(a.y);
     CT alpha_acc = CT(0);
-
-    for (int t = gwarp; t < a.ntiles; t += nwarps) {
-        const int4 T = __ldg(reinterpret_cast<const int4 *>(a.tiles) + t);
-        const int zb = T.x, zend = T.x + T.y;
-        const int z8 = zb & ~7;
-        if (T.w < 0) {
-            CT carry = CT(0);
-            int jrow = T.z;
-            // prefetch of round 0: columns + row-end bits
-            int k0 = z8 + EPL * lane;
-            int4 ca = make_int4(0, 0, 0, 0), cb = ca;
-            unsigned wb = 0u;
-            if (k0 < zend) {
-                ca = ld_stream(reinterpret_cast<const int4 *>(a.col + k0));
-                cb = ld_stream(reinterpret_cast<const int4 *>(a.col + k0) + 1);
-                wb = __ldg(a.endbits + (k0 >> 5));
+    const int nwork = a.nchunks + a.nitems;
+    constexpr int GQ = 8;  // nonzeros per lane per group; the next group's col/val are in flight
+                           // while the current group's x gathers are
+    for (int wi = gwarp; wi < nwork; wi += nwarps) {
+        if (wi < a.nchunks) {
+            // ---- big-row chunk: lane stream k = zb + lane + 32 t, warp reduction
+            const int4 C = __ldg(a.chunks + wi);
+            const int zb = C.y, ze = C.y + C.z;
+            const int nt = (ze - zb - lane + 31) / 32;  // this lane's element count
+            CT acc0 = CT(0), acc1 = CT(0);
+            int cc[GQ];
+            VT vv[GQ];
+#pragma unroll
+            for (int q = 0; q < GQ; ++q) {
+                const int k = zb + lane + 32 * q;
+                cc[q] = q < nt ? ld_col_stream(col + k) : 0;
+                vv[q] = q < nt ? ld_val_stream<VT>(val + k) : VT(0);
             }
-            for (int base = z8; base < zend; base += RND) {
-                const int cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-                const int kc = k0;
-                const unsigned wcur = wb;
-                k0 += RND;
-                if (k0 < zend) {  // next round's columns in flight during this round's gathers
-                    ca = ld_stream(reinterpret_cast<const int4 *>(a.col + k0));
-                    cb = ld_stream(reinterpret_cast<const int4 *>(a.col + k0) + 1);
-                    wb = __ldg(a.endbits + (k0 >> 5));
+            for (int t0 = 0; t0 < nt; t0 += GQ) {
+                ST xg[GQ];  // raw storage values, converted at use
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) xg[q] = (t0 + q < nt) ? __ldg(x + cc[q]) : ST(0);
+                VT vc[GQ];
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) {
+                    vc[q] = vv[q];
+                    const int t = t0 + GQ + q;
+                    const int k = zb + lane + 32 * t;
+                    cc[q] = t < nt ? ld_col_stream(col + k) : 0;
+                    vv[q] = t < nt ? ld_val_stream<VT>(val + k) : VT(0);
                 }
-                // valid-element mask of this lane's 8 slots: [zb, zend) intersect [kc, kc + 8)
-                const int lo = max(zb - kc, 0), hi = min(zend - kc, EPL);
-                const unsigned valid = (hi > lo) ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
-                CT p[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) p[e] = CT(0);
-                if (valid) {
-                    CT v8[8];
-                    Val8<VT, CT>::load(val + kc, v8);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if ((valid >> e) & 1u) p[e] = v8[e] * gather_x<ST, CT>(x, cc[e]);
+                for (int q = 0; q < GQ; q += 2) {
+                    acc0 += cvt<CT>(vc[q]) * cvt<CT>(xg[q]);
+                    acc1 += cvt<CT>(vc[q + 1]) * cvt<CT>(xg[q + 1]);
                 }
-                const unsigned fb = (wcur >> (kc & 31)) & valid & 0xFFu;
-                // lane-serial segment sums
-                CT part[8], run = CT(0), head = CT(0);
-                bool seen = false;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    run += p[e];
-                    part[e] = run;
-                    if ((fb >> e) & 1u) {
-                        if (!seen) { head = run; seen = true; }
-                        run = CT(0);
-                    }
-                }
-                // inclusive segmented scan of the open tails across lanes
-                CT v = (lane == 0 && !seen) ? carry + run : run;
-                int f = seen;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const CT vu = __shfl_up_sync(0xffffffffu, v, o);
-                    const int fu = __shfl_up_sync(0xffffffffu, f, o);
-                    if (lane >= o) {
-                        if (!f) v = vu + v;
-                        f |= fu;
-                    }
-                }
-                CT cin = __shfl_up_sync(0xffffffffu, v, 1);
-                if (lane == 0) cin = carry;
-                carry = __shfl_sync(0xffffffffu, v, 31);
-                // rank of this lane's row ends within the tile (ne <= 8)
-                const unsigned ne = __popc(fb);
-                const unsigned b0 = __ballot_sync(0xffffffffu, ne & 1u);
-                const unsigned b1 = __ballot_sync(0xffffffffu, ne & 2u);
-                const unsigned b2 = __ballot_sync(0xffffffffu, ne & 4u);
-                const unsigned b3 = __ballot_sync(0xffffffffu, ne & 8u);
-                int row = jrow + __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask) +
-                          8 * __popc(b3 & lt_mask);
-                jrow += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
-                if (fb) {
-                    bool first = true;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        if ((fb >> e) & 1u) {
-                            const CT tot = first ? cin + head : part[e];
-                            first = false;
-                            const CT yv = s * tot;
-                            y[row] = rnd_ct<ST, CT>(yv);
-                            alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
-                            if (a.y_dbg) a.y_dbg[row] = (double)tot;
-                            ++row;
-                        }
+            }
+            CT part = warp_sum(acc0 + acc1);
+            if (lane == 0) {
+                if (C.w < 0) {
+                    const CT yv = s * part;
+                    y[C.x] = rnd_ct<ST, CT>(yv);
+                    alpha_acc += yv * (s * cvt<CT>(ui[C.x]));
+                    if (a.y_dbg) a.y_dbg[C.x] = (double)part;
+                } else {
+                    const int4 L = __ldg(a.longrows + C.w);
+                    a.long_parts[wi] = (double)part;
+                    __threadfence();
+                    const unsigned prev = atomicAdd(a.long_cnt + C.w, 1u);
+                    if (prev == (unsigned)L.z - 1) {
+                        __threadfence();
+                        CT sum = CT(0);
+                        for (int q = 0; q < L.z; ++q) sum += (CT)__ldcg(a.long_parts + L.y + q);
+                        const CT yv = s * sum;
+                        y[L.x] = rnd_ct<ST, CT>(yv);
+                        a.alpha_long[C.w] = (double)(yv * (s * cvt<CT>(ui[L.x])));
+                        if (a.y_dbg) a.y_dbg[L.x] = (double)sum;
+                        a.long_cnt[C.w] = 0u;
                     }
                 }
             }
         } else {
-            // chunk of a long row: warp partial, last-arriving chunk finishes the row
-            CT part = CT(0);
-            for (int base = z8; base < zend; base += RND) {
-                const int kc = base + EPL * lane;
-                const int lo = max(zb - kc, 0), hi = min(zend - kc, EPL);
-                if (hi > lo) {
-                    const unsigned valid = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-                    const int4 ca = ld_stream(reinterpret_cast<const int4 *>(a.col + kc));
-                    const int4 cb = ld_stream(reinterpret_cast<const int4 *>(a.col + kc) + 1);
-                    const int cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-                    CT v8[8];
-                    Val8<VT, CT>::load(val + kc, v8);
+            // ---- SELL-32 slices of this item: their storage is contiguous, so lane l
+            // streams base + 32 t + l for t = 0 .. sum(w) - 1; slice boundaries are
+            // warp-uniform (row result emitted, accumulator reset)
+            const int2 I = __ldg(a.items + (wi - a.nchunks));
+            const int base = __ldg(a.sell + I.x).x;
+            const int2 Sl = __ldg(a.sell + (I.y - 1));
+            const int ntot = (Sl.x - base) / 32 + Sl.y;  // total width of the item
+            int sl = I.x;
+            int bound = __ldg(a.sell + sl).y;  // t at which slice sl ends
+            CT acc = CT(0);
+            int cc[GQ];
+            VT vv[GQ];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if ((valid >> e) & 1u) part += v8[e] * gather_x<ST, CT>(x, cc[e]);
-                }
+            for (int q = 0; q < GQ; ++q) {
+                const int k = base + lane + 32 * q;
+                cc[q] = q < ntot ? ld_col_stream(col + k) : 0;
+                vv[q] = q < ntot ? ld_val_stream<VT>(val + k) : VT(0);
             }
-            part = warp_sum(part);
-            if (lane == 0) {
-                const LongRow L = a.longrows[T.w];
-                a.long_parts[t] = (double)part;
-                __threadfence();
-                const unsigned prev = atomicAdd(a.long_cnt + T.w, 1u);
-                if (prev == (unsigned)L.nchunks - 1) {
-                    __threadfence();
-                    CT sum = CT(0);
-                    for (int q = 0; q < L.nchunks; ++q) sum += (CT)__ldcg(a.long_parts + L.first_tile + q);
-                    const CT yv = s * sum;
-                    y[L.row] = rnd_ct<ST, CT>(yv);
-                    a.alpha_long[T.w] = (double)(yv * (s * cvt<CT>(ui[L.row])));
-                    if (a.y_dbg) a.y_dbg[L.row] = (double)sum;
-                    a.long_cnt[T.w] = 0u;
+            for (int t0 = 0; t0 < ntot; t0 += GQ) {
+                ST xg[GQ];  // raw storage values, converted at use
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) xg[q] = (t0 + q < ntot) ? __ldg(x + cc[q]) : ST(0);
+                VT vc[GQ];
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) {
+                    vc[q] = vv[q];
+                    const int t = t0 + GQ + q;
+                    const int k = base + lane + 32 * t;
+                    cc[q] = t < ntot ? ld_col_stream(col + k) : 0;
+                    vv[q] = t < ntot ? ld_val_stream<VT>(val + k) : VT(0);
+                }
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) {
+                    const int t = t0 + q;
+                    if (t < ntot) {
+                        acc += cvt<CT>(vc[q]) * cvt<CT>(xg[q]);
+                        if (t + 1 == bound) {  // warp-uniform: slice sl complete
+                            const int row = a.nbig + 32 * sl + lane;
+                            if (row < a.nnonempty) {
+                                const CT yv = s * acc;
+                                y[row] = rnd_ct<ST, CT>(yv);
+                                alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
+                                if (a.y_dbg) a.y_dbg[row] = (double)acc;
+                            }
+                            acc = CT(0);
+                            ++sl;
+                            if (sl < I.y) bound += __ldg(a.sell + sl).y;
+                        }
+                    }
                 }
             }
         }
     }
-    const CT tot = block_sum<CT, kNT>(alpha_acc, red);
+    const CT tot = block_sum<CT, kSpmvNT>(alpha_acc, red);
     if (threadIdx.x == 0) a.slots[blockIdx.x] = (double)tot;
     if (arrive_last(a.counter, &sflag)) {
-        const double s1 = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, redd);
-        const double s2 = block_sum_array<double, kNT>(a.alpha_long, a.nlong, 1, redd);
+        const double s1 = block_sum_array<double, kSpmvNT>(a.slots, gridDim.x, 1, redd);
+        const double s2 = block_sum_array<double, kSpmvNT>(a.alpha_long, a.nlong, 1, redd);
         if (threadIdx.x == 0) {
             a.ex.alpha_part[a.g] = s1 + s2;
             *a.counter = 0u;
@@ -401,7 +360,7 @@ struct StepArgs {
 };
 
 template <typename ST, typename CT, int JB>
-__global__ void __launch_bounds__(kNT, 4) k_step(StepArgs a, int it) {
+__global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
     constexpr int VW = Vw<ST>::N;
     __shared__ CT part[kNT / 32][JB];
     __shared__ CT red[kNT / 32];
@@ -455,45 +414,40 @@ __global__ void __launch_bounds__(kNT, 4) k_step(StepArgs a, int it) {
         return;
     }
 
-    // Multi-dot h_j = u_j . w: the block's threads form NG column groups of LPG
-    // lanes; group g takes columns j0 + g*JB .. +JB-1 for the SAME rows, so one
-    // pass over the rows streams every basis column from DRAM once (y, u_i,
-    // u_{i-1}, w are re-read by the other groups from L1/L2) while each thread
-    // keeps only JB accumulators. Passes over further column blocks (it > NG*JB)
-    // read the stored w.
-    constexpr int NG = 4, LPG = kNT / NG;
-    const int grp = tid / LPG, gl = tid - grp * LPG;
-    for (int jb0 = 0; jb0 < it; jb0 += NG * JB) {
-        const int j0 = jb0 + grp * JB;
+    // Multi-dot h_j = u_j . w in passes over blocks of JB basis columns: a thread
+    // issues the loads of all JB columns of its row-vector at once (memory-level
+    // parallelism; measured ~6.2 TB/s for a 16-column block on B200), the first
+    // pass also forms w (recurrence) and stores it, later passes re-read w (L2).
+    for (int j0 = 0; j0 < it; j0 += JB) {
         CT acc[JB];
 #pragma unroll
         for (int q = 0; q < JB; ++q) acc[q] = CT(0);
-        for (int64_t v = (int64_t)blockIdx.x * LPG + gl; v < nvec; v += (int64_t)gridDim.x * LPG) {
+        for (int64_t v = (int64_t)blockIdx.x * kNT + tid; v < nvec; v += (int64_t)gridDim.x * kNT) {
+            uint4 u[JB];  // raw 16-byte storage vectors, converted at use (register budget)
+#pragma unroll
+            for (int q = 0; q < JB; ++q)
+                if (j0 + q < it) u[q] = __ldg(reinterpret_cast<const uint4 *>(V + (size_t)(j0 + q) * a.npad + v * VW));
             CT w[VW];
             if (a.mode == 2) {
                 vload<ST, CT>(src2 + v * VW, w);
-            } else if (jb0 == 0) {
+            } else if (j0 == 0) {
                 CT yy[VW], u1[VW], u0[VW];
                 vload<ST, CT>(yv + v * VW, yy);
                 vload<ST, CT>(ucur + v * VW, u1);
                 if (it > 1) vload<ST, CT>(uprev + v * VW, u0);
 #pragma unroll
                 for (int q = 0; q < VW; ++q) w[q] = yy[q] - c1 * u1[q] - (it > 1 ? c2 * u0[q] : CT(0));
-                // w rounded once; every group dots with the rounded (stored) value
-                if (grp == 0) vstore_back<ST, CT>(wv + v * VW, w);
-                else round_back<ST, CT>(w);
+                vstore_back<ST, CT>(wv + v * VW, w);  // w rounded once; dots use what was stored
             } else {
                 vload<ST, CT>(wv + v * VW, w);
             }
 #pragma unroll
             for (int q = 0; q < JB; ++q) {
-                const int j = j0 + q;
-                if (j < it) {
-                    CT u[VW];
-                    vload<ST, CT>(V + (size_t)j * a.npad + v * VW, u);
+                if (j0 + q < it) {
+                    const ST *ue = reinterpret_cast<const ST *>(&u[q]);
                     CT d = CT(0);
 #pragma unroll
-                    for (int e = 0; e < VW; ++e) d += u[e] * w[e];
+                    for (int e = 0; e < VW; ++e) d += cvt<CT>(ue[e]) * w[e];
                     acc[q] += d;
                 }
             }
@@ -504,13 +458,11 @@ __global__ void __launch_bounds__(kNT, 4) k_step(StepArgs a, int it) {
             if (lane == 0) part[wid][q] = r;
         }
         __syncthreads();
-        if (tid < NG * JB && jb0 + tid < it) {  // column jb0 + tid = group tid / JB, slot tid % JB
-            constexpr int WPG = LPG / 32;
-            const int g2 = tid / JB, q = tid - g2 * JB;
+        if (tid < JB && j0 + tid < it) {
             CT r = CT(0);
 #pragma unroll
-            for (int w8 = 0; w8 < WPG; ++w8) r += part[g2 * WPG + w8][q];
-            a.slots[(size_t)blockIdx.x * a.ld + jb0 + tid] = (double)r;
+            for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][tid];
+            a.slots[(size_t)blockIdx.x * a.ld + j0 + tid] = (double)r;
         }
         __syncthreads();
     }
@@ -792,9 +744,9 @@ __global__ void k_jacobi(JacArgs a) {
 //   pass 0: recompute y_k row by row, per-block partials of ||y_k||^2 ->
 //           ex.ritz_part[g][k] (last-arriving block per output group, fixed order)
 //   pass 1: recompute y_k, scale by 1/||y_k|| (norms summed over parts in rank
-//           order) and store once, in the output dtype, to the caller's buffer
-//           in ORIGINAL row order (position p -> row perm[p]; hub-first order
-//           keeps all non-hot rows ascending, so the stores stay coalesced).
+//           order) and store once, in the output dtype, row-major in position
+//           order (yt[p][k]); k_unperm then writes the caller's buffer in
+//           original row order (one contiguous K-vector read per row).
 // Thread = VW consecutive rows (one 16-byte load per basis column) x KB outputs;
 // block b = (row range b / ngroups, output group b % ngroups). coefS holds the sign
 // fix and the deferred normalisation s_j.
@@ -806,9 +758,9 @@ struct RitzArgs {
     unsigned *counter;        // [ceil(K / KB)]
     LzState st;
     Exch ex;
-    void *const *out_ptr;     // device param: output base (K vectors of nrows)
+    void *const *out_ptr;     // device param: output base (pass 1 writes only if non-NULL)
     const int *out_dtype;     // device param: 0 f64, 1 f32
-    const int32_t *perm;      // position -> part-local original row (output order)
+    void *yt;                 // [npad][K] Ritz vectors in position order, output dtype
 };
 
 template <typename ST, typename CT, int KB>
@@ -873,25 +825,20 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
 #pragma unroll
                 for (int e = 0; e < VW; ++e) nrm[q] += acc[e][q] * acc[e][q];
         } else {
-            int32_t orow[VW];
+            // row-major [position][K]: this thread's KB outputs of a row are one
+            // contiguous, sector-aligned group (whole 32-byte sectors per row)
 #pragma unroll
             for (int e = 0; e < VW; ++e) {
                 const int64_t r = v * VW + e;
-                orow[e] = (r < a.nrows) ? __ldg(a.perm + r) : 0;
-            }
+                if (r < a.nrows) {
+                    const size_t o = (size_t)r * K + k0;
 #pragma unroll
-            for (int q = 0; q < KB; ++q) {
-                if (k0 + q >= kf) break;
-                const double iv = inv[q];
-                const size_t base = (size_t)(k0 + q) * a.nrows;
-#pragma unroll
-                for (int e = 0; e < VW; ++e) {
-                    const int64_t r = v * VW + e;
-                    if (r < a.nrows) {
-                        const size_t o = base + (size_t)orow[e];
-                        const double yv = (double)acc[e][q] * iv;
-                        if (dt == 0) __stcs(reinterpret_cast<double *>(out) + o, yv);
-                        else __stcs(reinterpret_cast<float *>(out) + o, (float)yv);
+                    for (int q = 0; q < KB; ++q) {
+                        const double yv = (k0 + q < kf) ? (double)acc[e][q] * inv[q] : 0.0;
+                        if (k0 + q < K) {
+                            if (dt == 0) reinterpret_cast<double *>(a.yt)[o + q] = yv;
+                            else reinterpret_cast<float *>(a.yt)[o + q] = (float)yv;
+                        }
                     }
                 }
             }
@@ -920,6 +867,37 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
         }
         __syncthreads();
         if (tid == 0) a.counter[grp] = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a15: eigenvectors back to the original row order: out[k][r] = yt[inv[r]][k]
+// (the caller's K x n_local buffer, vector k contiguous).
+struct UnpermArgs {
+    const void *yt;
+    const int32_t *inv;
+    int64_t nrows;
+    int K;
+    const int *k_found;
+    void *const *out_ptr;
+    const int *out_dtype;
+};
+
+__global__ void __launch_bounds__(kNT) k_unperm(UnpermArgs a) {
+    void *out = *a.out_ptr;
+    if (!out) return;
+    const int kf = *a.k_found, dt = *a.out_dtype, K = a.K;
+    for (int64_t r = (int64_t)blockIdx.x * kNT + threadIdx.x; r < a.nrows; r += (int64_t)gridDim.x * kNT) {
+        const size_t src = (size_t)__ldg(a.inv + r) * K;
+        if (dt == 0) {
+            const double *yt = reinterpret_cast<const double *>(a.yt) + src;
+            double *o = reinterpret_cast<double *>(out);
+            for (int k = 0; k < kf; ++k) __stcs(o + (size_t)k * a.nrows + r, __ldg(yt + k));
+        } else {
+            const float *yt = reinterpret_cast<const float *>(a.yt) + src;
+            float *o = reinterpret_cast<float *>(out);
+            for (int k = 0; k < kf; ++k) __stcs(o + (size_t)k * a.nrows + r, __ldg(yt + k));
+        }
     }
 }
 

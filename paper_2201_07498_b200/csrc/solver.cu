@@ -82,14 +82,18 @@ struct SolveParams {
 struct Part {
     int g = 0;
     int64_t row0 = 0, nrows = 0, npad = 0, nnz = 0;
-    int ntiles = 0, nlong = 0;
+    int nchunks = 0, nlong = 0, nitems = 0, nbig = 0;
+    int64_t nnonempty = 0, nphys = 0;
     int32_t *col = nullptr, *perm = nullptr;
     std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
-    uint32_t *endbits = nullptr;
+    int32_t *inv = nullptr;         // original part-local row -> position
+    std::vector<int32_t> h_sell;    // host copy of the SELL table (export_layout)
     std::vector<int32_t> h_rowptr;  // host copy (export_layout)
     void *val = nullptr;
-    Tile *tiles = nullptr;
+    Chunk *chunks = nullptr;
     LongRow *longrows = nullptr;
+    int32_t *sell = nullptr, *items = nullptr;
+    void *yt = nullptr;            // Ritz output in position order, K values per row
     double *long_parts = nullptr, *alpha_long = nullptr;
     unsigned *long_cnt = nullptr;
     void *V = nullptr, *y = nullptr, *w = nullptr;
@@ -124,6 +128,7 @@ struct topk_eig_s {
     double *jac_work = nullptr;
     size_t jac_smem = 0, jac_bytes = 0;
     int jac_ld_log2 = 0, jac_hl_log2 = 0;
+
     int jac_threads = 32;
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -211,9 +216,11 @@ static void *rep_slot(topk_eig_s *h, Part &p) {
 template <typename VT, typename ST, typename CT>
 static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     SpmvArgs a;
-    a.col = p.col; a.val = p.val; a.endbits = p.endbits;
-    a.tiles = p.tiles; a.ntiles = p.ntiles;
-    a.longrows = p.longrows; a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
+    a.col = p.col; a.val = p.val;
+    a.chunks = reinterpret_cast<const int4 *>(p.chunks); a.longrows = reinterpret_cast<const int4 *>(p.longrows);
+    a.sell = reinterpret_cast<const int2 *>(p.sell); a.items = reinterpret_cast<const int2 *>(p.items);
+    a.nchunks = p.nchunks; a.nitems = p.nitems; a.nbig = p.nbig; a.nnonempty = (int)p.nnonempty;
+    a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
     a.alpha_long = p.alpha_long; a.nlong = p.nlong;
     const void *ucol = (const char *)p.V + (size_t)(it - 1) * p.npad * sizeof(ST);
     a.x = (h->G == 1) ? ucol : h->replica;
@@ -222,7 +229,7 @@ static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     a.slots = p.slots; a.counter = p.counters + 1;
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g;
     prof_begin(h, p, 1);
-    k_spmv<VT, ST, CT><<<h->grid_spmv, kNT, 0, h->stream>>>(a, it);
+    k_spmv<VT, ST, CT><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -322,7 +329,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) +
                                         offsetof(SolveParams, out_ptr));
             a.out_dtype = &h->dparams->out_dtype;
-            a.perm = p.perm;
+            a.yt = p.yt;
             const size_t smem = (size_t)h->m * kRitzKB * sizeof(double);
             const unsigned ngroups = (unsigned)((h->K + kRitzKB - 1) / kRitzKB);
             const dim3 grid((unsigned)h->grid_ritz * ngroups);
@@ -333,6 +340,19 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             h->launches++;
         }
         if (pass == 0) exch_ritz(h);
+    }
+    // a15 prep: position order -> original row order into the caller's buffer
+    for (Part &p : h->parts) {
+        UnpermArgs a;
+        a.yt = p.yt; a.inv = p.inv; a.nrows = p.nrows; a.K = h->K; a.k_found = p.st.k_found;
+        a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) +
+                                    offsetof(SolveParams, out_ptr));
+        a.out_dtype = &h->dparams->out_dtype;
+        prof_begin(h, p, 7);
+        k_unperm<<<h->grid_stream, kNT, 0, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
     }
 }
 
@@ -346,9 +366,9 @@ static void set_kernels(topk_eig_s *h) {
     h->enqueue = &enqueue_solve<VT, ST, CT>;
     h->spmv_only = &spmv_only<VT, ST, CT>;
     int occ = 0;
-    // the SpMV uses (almost) no shared memory: give the whole unified L1 to the x gathers
+    // the SpMV uses no dynamic shared memory: the whole unified L1 caches x
     CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT>, kNT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT>, kSpmvNT, 0);
     h->grid_spmv = h->nsm * std::max(1, occ);
     int occ2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
@@ -413,18 +433,19 @@ static const double *hptr(const Part &p, const double *devptr) {
 }
 
 static void upload_values(topk_eig_s *h, Part &p, const PartLayout &L) {
-    const size_t z = L.val.size();
+    const size_t z = L.pval.size();
+    if (z == 0) return;
     if (h->ms == TOPK_F64) {
-        CUDA_TRY(cudaMemcpy(p.val, L.val.data(), z * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(p.val, L.pval.data(), z * 8, cudaMemcpyHostToDevice));
     } else if (h->ms == TOPK_F32) {
         hvec<float> t(z);
 #pragma omp parallel for schedule(static)
-        for (size_t k = 0; k < z; ++k) t[k] = round_f32(L.val[k]);
+        for (size_t k = 0; k < z; ++k) t[k] = round_f32(L.pval[k]);
         CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 4, cudaMemcpyHostToDevice));
     } else {
         hvec<uint16_t> t(z);
 #pragma omp parallel for schedule(static)
-        for (size_t k = 0; k < z; ++k) t[k] = round_bf16_bits(L.val[k]);
+        for (size_t k = 0; k < z; ++k) t[k] = round_bf16_bits(L.pval[k]);
         CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 2, cudaMemcpyHostToDevice));
     }
 }
@@ -488,11 +509,10 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     s = partition_rule_p(csr.rowptr.data(), n, G, h->bounds.data());
     if (s != TOPK_OK) return fail(s, "partition failed");
     const int64_t npad = padded_rows(h->bounds.data(), G);
-    const std::vector<uint8_t> hot = hot_columns(csr, hot_count(n, (int)dsize(storage)));
     std::vector<int32_t> pos;
-    hub_first_order(csr, h->bounds.data(), G, hot.data(), pos);
-    const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, hot.data(), pos.data());
-    clk.mark("partition + hot + order");
+    degree_order(csr, h->bounds.data(), G, pos);
+    const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
+    clk.mark("partition + order");
 
     // device
     int ndev = 0;
@@ -516,6 +536,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->ex.norm_part = h->alloc<double>((size_t)G);
         h->ex.hpart = h->alloc<double>((size_t)G * (m + 1));
         h->ex.ritz_part = h->alloc<double>((size_t)G * K);
+
         if (G > 1) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
         h->ex.replica = h->replica;
         const int nlocal = (world > 1) ? 1 : G;
@@ -550,25 +571,36 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             if (s != TOPK_OK) return fail(s, err);
             clk.mark("build_part");
             p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.col.size();
-            p.ntiles = (int)L.tiles.size(); p.nlong = (int)L.longrows.size();
-            // col/val padded by 128 entries: the SpMV issues aligned 4-wide loads
-            p.col = h->alloc<int32_t>(L.col.size() + 128);
-            p.val = h->alloc<char>((L.val.size() + 128) * dsize(ms));
-            p.endbits = h->alloc<uint32_t>(L.endbits.size());
+            p.nchunks = (int)L.chunks.size(); p.nlong = (int)L.longrows.size();
+            p.nitems = (int)L.items.size() / 2; p.nbig = L.nbig; p.nnonempty = L.nnonempty;
+            p.nphys = (int64_t)L.pcol.size();
+            // physical col/val padded by 128 entries
+            p.col = h->alloc<int32_t>(L.pcol.size() + 128);
+            p.val = h->alloc<char>((L.pval.size() + 128) * dsize(ms));
             p.h_rowptr = L.rowptr;
             p.h_perm = L.perm;
+            p.h_sell = L.sell;
             p.perm = h->alloc<int32_t>(L.perm.size());
-            p.tiles = h->alloc<Tile>(L.tiles.size());
+            p.inv = h->alloc<int32_t>(L.perm.size());
+            p.chunks = h->alloc<Chunk>(L.chunks.size());
             p.longrows = h->alloc<LongRow>(L.longrows.size());
-            p.long_parts = h->alloc<double>(L.tiles.size());
+            p.sell = h->alloc<int32_t>(L.sell.size());
+            p.items = h->alloc<int32_t>(L.items.size());
+            p.long_parts = h->alloc<double>(L.chunks.size());
             p.long_cnt = h->alloc<unsigned>(L.longrows.size());
             p.alpha_long = h->alloc<double>(L.longrows.size());
             CUDA_TRY(cudaStreamSynchronize(h->stream));
-            CUDA_TRY(cudaMemcpy(p.endbits, L.endbits.data(), L.endbits.size() * 4, cudaMemcpyHostToDevice));
-            if (!L.perm.empty()) CUDA_TRY(cudaMemcpy(p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(cudaMemcpy(p.col, L.col.data(), L.col.size() * 4, cudaMemcpyHostToDevice));
-            if (!L.tiles.empty()) CUDA_TRY(cudaMemcpy(p.tiles, L.tiles.data(), L.tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+            if (!L.perm.empty()) {
+                std::vector<int32_t> inv(L.perm.size());
+                for (size_t q = 0; q < L.perm.size(); ++q) inv[(size_t)L.perm[q]] = (int32_t)q;
+                CUDA_TRY(cudaMemcpy(p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(cudaMemcpy(p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+            }
+            if (!L.pcol.empty()) CUDA_TRY(cudaMemcpy(p.col, L.pcol.data(), L.pcol.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.chunks.empty()) CUDA_TRY(cudaMemcpy(p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
+            if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
             upload_values(h.get(), p, L);
             clk.mark("upload (H2D)");
             const size_t vsz = dsize(storage);
@@ -576,6 +608,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.y = h->alloc<char>((size_t)npad * vsz);
             p.w = h->alloc<char>((size_t)npad * vsz);
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
+            p.yt = h->alloc<double>((size_t)K * std::max<int64_t>(p.npad, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
             p.slots = h->alloc<double>((size_t)std::max(h->grid_spmv, std::max(h->grid_stream, h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
             p.counters = h->alloc<unsigned>(8 + 64);
@@ -799,9 +832,9 @@ topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t
 }
 
 topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g, topk_dtype_t storage,
-                                   topk_dtype_t values_storage, int64_t *n_pad, int64_t *n_rows, int64_t *nnz,
-                                   int64_t *ntiles, int64_t *rowptr, int32_t *col, double *val, int32_t *tiles,
-                                   int32_t *perm) {
+                                   topk_dtype_t values_storage, int64_t *sizes, int64_t *rowptr, int32_t *col,
+                                   double *val, int32_t *perm, int32_t *pcol, double *pval, int32_t *chunks,
+                                   int32_t *sell, int32_t *items) {
     if (!A) return fail(TOPK_E_INVALID, "A must be non-NULL");
     if (G < 1 || G > 64 || g < 0 || g >= G) return fail(TOPK_E_INVALID, "need 1 <= G <= 64 and 0 <= g < G");
     if (values_storage < TOPK_F64 || values_storage > TOPK_BF16 || storage < TOPK_F64 || storage > TOPK_BF16)
@@ -818,29 +851,35 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
         s = partition_rule_p(csr.rowptr.data(), csr.n, G, b.data());
         if (s != TOPK_OK) return fail(s, "partition failed");
         const int64_t npad = padded_rows(b.data(), G);
-        PartLayout L;
-        const std::vector<uint8_t> hot = hot_columns(csr, hot_count(csr.n, (int)dsize(storage)));
         std::vector<int32_t> pos;
-        hub_first_order(csr, b.data(), G, hot.data(), pos);
-        const std::vector<int32_t> colmap = column_map(csr.n, b.data(), G, npad, hot.data(), pos.data());
-        clk.mark("partition + hot + order");
+        degree_order(csr, b.data(), G, pos);
+        const std::vector<int32_t> colmap = column_map(csr.n, b.data(), G, npad, pos.data());
+        clk.mark("partition + order");
+        PartLayout L;
         s = build_part(csr, b.data(), G, g, npad, pos.data(), colmap.data(), L, err);
         if (s != TOPK_OK) return fail(s, err);
         clk.mark("build_part");
-        if (n_pad) *n_pad = npad;
-        if (n_rows) *n_rows = L.nrows;
-        if (nnz) *nnz = (int64_t)L.col.size();
-        if (ntiles) *ntiles = (int64_t)L.tiles.size();
+        auto rv = [&](double x) {
+            return values_storage == TOPK_F64 ? x
+                   : values_storage == TOPK_F32 ? (double)round_f32(x) : bf16_bits_to_double(round_bf16_bits(x));
+        };
+        if (sizes) {
+            sizes[0] = npad; sizes[1] = L.nrows; sizes[2] = (int64_t)L.col.size(); sizes[3] = L.nnonempty;
+            sizes[4] = L.nbig; sizes[5] = (int64_t)L.chunks.size(); sizes[6] = (int64_t)L.sell.size() / 2;
+            sizes[7] = (int64_t)L.items.size() / 2; sizes[8] = (int64_t)L.pcol.size();
+        }
         if (rowptr)
             for (size_t i = 0; i < L.rowptr.size(); ++i) rowptr[i] = L.rowptr[i];
         if (col) std::memcpy(col, L.col.data(), L.col.size() * 4);
         if (val)
-            for (size_t k = 0; k < L.val.size(); ++k)
-                val[k] = values_storage == TOPK_F64 ? L.val[k]
-                         : values_storage == TOPK_F32 ? (double)round_f32(L.val[k])
-                                                      : bf16_bits_to_double(round_bf16_bits(L.val[k]));
-        if (tiles) std::memcpy(tiles, L.tiles.data(), L.tiles.size() * sizeof(Tile));
+            for (size_t k = 0; k < L.val.size(); ++k) val[k] = rv(L.val[k]);
         if (perm) std::memcpy(perm, L.perm.data(), L.perm.size() * 4);
+        if (pcol) std::memcpy(pcol, L.pcol.data(), L.pcol.size() * 4);
+        if (pval)
+            for (size_t k = 0; k < L.pval.size(); ++k) pval[k] = rv(L.pval[k]);
+        if (chunks) std::memcpy(chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk));
+        if (sell) std::memcpy(sell, L.sell.data(), L.sell.size() * 4);
+        if (items) std::memcpy(items, L.items.data(), L.items.size() * 4);
     } catch (std::bad_alloc &) {
         return fail(TOPK_E_NOMEM, "host allocation failed");
     }
@@ -864,19 +903,37 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
     try {
         if (rowptr)
             for (size_t i = 0; i < p.h_rowptr.size(); ++i) rowptr[i] = p.h_rowptr[i];
-        if (col) CUDA_TRY(cudaMemcpy(col, p.col, (size_t)p.nnz * 4, cudaMemcpyDeviceToHost));
-        if (val) {
-            const size_t z = (size_t)p.nnz;
-            if (h->ms == TOPK_F64) {
-                CUDA_TRY(cudaMemcpy(val, p.val, z * 8, cudaMemcpyDeviceToHost));
-            } else if (h->ms == TOPK_F32) {
-                std::vector<float> t(z);
-                CUDA_TRY(cudaMemcpy(t.data(), p.val, z * 4, cudaMemcpyDeviceToHost));
-                for (size_t k = 0; k < z; ++k) val[k] = t[k];
-            } else {
-                std::vector<uint16_t> t(z);
-                CUDA_TRY(cudaMemcpy(t.data(), p.val, z * 2, cudaMemcpyDeviceToHost));
-                for (size_t k = 0; k < z; ++k) val[k] = bf16_bits_to_double(t[k]);
+        if (col || val) {
+            // logical entry k of position row q -> physical index (big-row CSR prefix or SELL slot)
+            std::vector<int64_t> phys((size_t)p.nnz);
+            for (int64_t q = 0; q < p.nrows; ++q) {
+                const int64_t rb = p.h_rowptr[(size_t)q], re = p.h_rowptr[(size_t)q + 1];
+                for (int64_t k = rb; k < re; ++k) {
+                    if (q < p.nbig) { phys[(size_t)k] = k; continue; }
+                    const int64_t sl = (q - p.nbig) / 32, i = (q - p.nbig) % 32;
+                    phys[(size_t)k] = p.h_sell[(size_t)(2 * sl)] + 32 * (k - rb) + i;
+                }
+            }
+            const size_t zp = (size_t)p.nphys;
+            if (col) {
+                std::vector<int32_t> t(zp);
+                if (zp) CUDA_TRY(cudaMemcpy(t.data(), p.col, zp * 4, cudaMemcpyDeviceToHost));
+                for (size_t k = 0; k < phys.size(); ++k) col[k] = t[(size_t)phys[k]];
+            }
+            if (val) {
+                std::vector<double> t(zp);
+                if (h->ms == TOPK_F64) {
+                    if (zp) CUDA_TRY(cudaMemcpy(t.data(), p.val, zp * 8, cudaMemcpyDeviceToHost));
+                } else if (h->ms == TOPK_F32) {
+                    std::vector<float> f(zp);
+                    if (zp) CUDA_TRY(cudaMemcpy(f.data(), p.val, zp * 4, cudaMemcpyDeviceToHost));
+                    for (size_t k = 0; k < zp; ++k) t[k] = f[k];
+                } else {
+                    std::vector<uint16_t> f(zp);
+                    if (zp) CUDA_TRY(cudaMemcpy(f.data(), p.val, zp * 2, cudaMemcpyDeviceToHost));
+                    for (size_t k = 0; k < zp; ++k) t[k] = bf16_bits_to_double(f[k]);
+                }
+                for (size_t k = 0; k < phys.size(); ++k) val[k] = t[(size_t)phys[k]];
             }
         }
     }

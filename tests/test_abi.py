@@ -101,38 +101,57 @@ def test_create_argument_errors_precede_device():
 @pytest.mark.parametrize("storage,dtype", [("f64", "f64"), ("f32", "f32"), ("f32", "bf16"), ("bf16", "bf16")])
 def test_plan_layout_bit_exact_vs_oracle(G, storage, dtype):
     """Rows a3-a4: the library's host layout (what create
-    uploads) equals the oracle's, bit for bit: hub-first row order, remapped
-    columns with the hot bit, stored values and the SpMV tile table."""
-    A = S.rmat(13, 120_000, 5)  # long rows (> 1024 nnz) present
+    uploads) equals the oracle's, bit for bit: degree row order, remapped
+    columns, stored values."""
+    A = S.rmat(13, 120_000, 5)  # long rows (> 2048 nnz) present
     b = O.partition(A.rowptr, G)
     for g in range(G):
-        rp, col, val, npad, tiles, perm = T.plan_layout(A, G, g, storage, dtype)
-        orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, b, g, dtype, storage=storage,
-                                                 with_perm=True)
-        assert npad == onpad
-        assert np.array_equal(perm, operm)
-        assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
-        assert np.array_equal(val.view(np.uint64), oval.view(np.uint64))
-        assert np.array_equal(tiles, O.tiles(orp, 1024))
+        L = T.plan_layout(A, G, g, storage, dtype)
+        orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, b, g, dtype, with_perm=True)
+        assert L["n_pad"] == onpad
+        assert np.array_equal(L["perm"], operm)
+        assert np.array_equal(L["rowptr"], orp) and np.array_equal(L["col"], ocol)
+        assert np.array_equal(L["val"].view(np.uint64), oval.view(np.uint64))
 
 
-def test_tile_table_properties():
-    """Every nonzero of every non-empty row is covered exactly once; packed
-    tiles hold whole rows and <= 1024 nonzeros; long rows are split in order."""
+@pytest.mark.parametrize("G", [1, 3])
+def test_physical_format_unpacks_to_logical(G):
+    """The SpMV physical format (big-row CSR chunks + SELL-32 slices, host_prep.h)
+    holds exactly the logical CSR: every logical entry at its physical slot,
+    padding = (column 0, 0.0), slices degree-sorted, items cover all slices."""
     A = S.rmat(13, 120_000, 5)
-    rp = A.rowptr
-    t = O.tiles(rp, 1024)
-    nz_rows = np.flatnonzero(np.diff(rp) > 0)
-    cover = np.zeros(rp[-1], np.int32)
-    assert (t[:, 3] >= 0).any(), "fixture should contain long rows"
-    for zb, cnt, jb, lid in t:
-        assert 1 <= cnt <= 1024
-        cover[zb:zb + cnt] += 1
-        r = nz_rows[jb]
-        if lid < 0:
-            assert rp[r] == zb
-            end = zb + cnt
-            assert end in rp  # whole rows only
-        else:
-            assert rp[r] <= zb < rp[r + 1] and zb + cnt <= rp[r + 1]
-    assert (cover == 1).all()
+    for g in range(G):
+        L = T.plan_layout(A, G, g, "f32")
+        rp, col, val, nbig, nne = L["rowptr"], L["col"], L["val"], L["nbig"], L["nnonempty"]
+        deg = np.diff(rp)
+        assert np.all(deg[:-1] >= deg[1:]), "rows must be in degree order"
+        assert nne == int((deg > 0).sum()) and np.all(deg[:nbig] > 128) and np.all(deg[nbig:] <= 128)
+        pcol, pval, ch, sl, it = L["pcol"], L["pval"], L["chunks"], L["sell"], L["items"]
+        # big rows: CSR prefix, cut into <= 2048-nnz chunks in order
+        assert np.array_equal(pcol[:rp[nbig]], col[:rp[nbig]]) and np.array_equal(pval[:rp[nbig]], val[:rp[nbig]])
+        cover = np.zeros(rp[nbig], np.int32)
+        for row, z0, cnt, lid in ch:
+            assert rp[row] <= z0 and z0 + cnt <= rp[row + 1] and 1 <= cnt <= 2048
+            assert (lid >= 0) == (deg[row] > 2048)
+            cover[z0:z0 + cnt] += 1
+        assert np.all(cover == 1)
+        # SELL-32: slice s rows nbig + 32 s + i, width = degree of its first row, column-major
+        nsl = (nne - nbig + 31) // 32
+        assert len(sl) == nsl
+        seen = np.zeros(len(pcol), bool)
+        seen[:rp[nbig]] = True
+        for s_, (base, w) in enumerate(sl):
+            p0 = nbig + 32 * s_
+            assert w == deg[p0]
+            for i in range(32):
+                p = p0 + i
+                d = deg[p] if p < nne else 0
+                idx = base + 32 * np.arange(w) + i
+                seen[idx] = True
+                assert np.array_equal(pcol[idx[:d]], col[rp[p]:rp[p] + d]) if d else True
+                assert np.array_equal(pval[idx[:d]], val[rp[p]:rp[p] + d]) if d else True
+                assert np.all(pval[idx[d:]] == 0.0) and np.all(pcol[idx[d:]] == 0)
+        assert seen.all()
+        covered = np.concatenate([np.arange(a, b_) for a, b_ in it]) if len(it) else np.zeros(0, int)
+        assert np.array_equal(covered, np.arange(nsl))
+

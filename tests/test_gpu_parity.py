@@ -32,6 +32,15 @@ def c3s():
     return S.config_matrix("C3S")
 
 
+def bf16_values(A):
+    """A's values rounded to bf16 by the oracle's layout (O2), back in CSR order."""
+    lrp, _, lv, _, perm = O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16", with_perm=True)
+    idx = np.concatenate([np.arange(A.rowptr[r], A.rowptr[r + 1]) for r in perm]).astype(np.int64)
+    out = np.empty_like(np.asarray(A.val, dtype=np.float64))
+    out[idx] = lv
+    return out
+
+
 def normwise(a, b):
     a, b = np.sort(a), np.sort(b)
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
@@ -72,8 +81,7 @@ def test_layout_bit_exact_c1(T, c1, G, dtype):
         assert np.array_equal(b, O.partition(csr.rowptr, G))
         for g in range(G):
             rp, col, val, npad = h.layout(g)
-            orp, ocol, oval, onpad = O.layout(csr.rowptr, csr.col, csr.val, G, b, g, dtype,
-                                              storage=dtype if dtype != "bf16" else "f32")
+            orp, ocol, oval, onpad = O.layout(csr.rowptr, csr.col, csr.val, G, b, g, dtype)
             assert npad == onpad
             assert np.array_equal(rp, orp)
             assert np.array_equal(col, ocol)
@@ -103,10 +111,7 @@ def test_spmv_parity(T, c1, c3s, name, storage, vals, G):
         y = h.debug_spmv(x)
     xr = x.astype(np.float32).astype(np.float64) if storage == "f32" else x
     if vals == "bf16":
-        # bf16-rounded values in the original order (no hot rows -> identity row order)
-        _, _, vb, _ = O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16",
-                               hot=np.zeros(A.n, np.uint8))
-        av = vb
+        av = bf16_values(A)
     else:
         av = A.val if vals == "f64" else A.val.astype(np.float32).astype(np.float64)
     yr = O.spmv(A.rowptr, A.col, av, xr)
@@ -179,8 +184,7 @@ def test_rmat_parity(T, c3s, K, m, storage, compute, vals):
     A = c3s
     av = A.val
     if vals == "bf16":  # generator weights are bf16-exact: the matrix is unchanged
-        assert np.array_equal(O.layout(A.rowptr, A.col, A.val, 1, np.array([0, A.n]), 0, "bf16",
-                                       hot=np.zeros(A.n, np.uint8))[2], A.val)
+        assert np.array_equal(bf16_values(A), A.val)
     ref = O.solve(A.rowptr, A.col, av, K=K, m=m, seed=7, tau=O.TAU["f64"])
     r = T.solve(A, K, storage=storage, compute=compute, m=m, seed=7, values_storage=vals)
     th = T_all(T, A, K, storage, compute, m, 7, values_storage=vals)

@@ -40,7 +40,8 @@ def _worker(rank, port, q):
         allb = [torch.zeros(G + 1, dtype=torch.int64) for _ in range(G)]
         dist.all_gather(allb, torch.from_numpy(b))
         same_b = all(np.array_equal(x.numpy(), b) for x in allb)
-        rp, col, val, npad, tiles, perm = T.plan_layout(A, G, rank, "f64")
+        L = T.plan_layout(A, G, rank, "f64")
+        rp, col, val, npad, perm = L["rowptr"], L["col"], L["val"], L["n_pad"], L["perm"]
         orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, O.partition(A.rowptr, G), rank,
                                                  "f64", with_perm=True)
         layout_ok = (np.array_equal(rp, orp) and np.array_equal(col, ocol) and np.array_equal(val, oval)
@@ -54,8 +55,8 @@ def _worker(rank, port, q):
         dist.all_gather(slots, torch.from_numpy(slot))
         replica = torch.cat(slots).numpy()
         # local SpMV on the remapped columns, then the alpha partial (Alg.1 l.9-10)
-        cidx = col & 0x7FFFFFFF  # strip the hot-column bit
-        y = np.array([np.dot(val[rp[r]:rp[r + 1]], replica[cidx[rp[r]:rp[r + 1]]]) for r in range(r1 - r0)])
+        xg = replica[col]
+        y = np.array([np.dot(val[rp[r]:rp[r + 1]], xg[rp[r]:rp[r + 1]]) for r in range(r1 - r0)])
         parts = [torch.zeros(1, dtype=torch.float64) for _ in range(G)]
         vloc = v[r0 + perm]
         dist.all_gather(parts, torch.tensor([np.dot(y, vloc)], dtype=torch.float64))

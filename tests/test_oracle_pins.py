@@ -134,8 +134,7 @@ def test_layout_reassembles_matrix(G, dtype):
     rp, c, v = er_csr(500, 3000, 11)
     b = O.partition(rp, G)
     npad_expect = int(math.ceil(max(np.diff(b)) / 64) * 64)
-    hot = O.hot_columns(rp, 37)
-    parts = [O.layout(rp, c, v, G, b, g, dtype, hot=hot, with_perm=True) for g in range(G)]
+    parts = [O.layout(rp, c, v, G, b, g, dtype, with_perm=True) for g in range(G)]
     perms = [pt[4] for pt in parts]
     dense = np.zeros((500, 500))
     np.add.at(dense, (np.repeat(np.arange(500), np.diff(rp)), c), v)
@@ -144,12 +143,9 @@ def test_layout_reassembles_matrix(G, dtype):
         assert npad == npad_expect
         assert lrp[0] == 0 and len(lrp) == b[g + 1] - b[g] + 1
         assert sorted(perm) == list(range(b[g + 1] - b[g]))
-        flag = lc < 0  # hot-column bit 31
-        lc = lc & 0x7FFFFFFF
         owner, local = lc // npad, lc % npad
         assert np.all(local < np.diff(b)[owner])
         gcol = np.array([b[o] + perms[o][q] for o, q in zip(owner, local)], np.int64)
-        assert np.array_equal(flag, hot[gcol].astype(bool))
         grow = b[g] + np.repeat(perm, np.diff(lrp))
         np.add.at(got, (grow, gcol), lv)
     if dtype == "f64":
@@ -161,34 +157,19 @@ def test_layout_reassembles_matrix(G, dtype):
         check_bf16_rounding(dense[nz], got[nz])
 
 
-def test_hub_first_positions_brute_force():
-    """Inside each part: hot rows first by (degree desc, index asc), then the
-    other rows ascending."""
+def test_degree_order_positions_brute_force():
+    """Inside each part: rows by (degree desc, index asc), so empty rows last
+    (DESIGN.md 2)."""
     rp, c, v = er_csr(300, 200, 3)
     deg = np.diff(rp)
     assert (deg == 0).any()
-    hot = O.hot_columns(rp, 23)
     for G in (1, 2, 3):
         b = O.partition(rp, G)
-        pos = O.positions(rp, G, b, hot)
+        pos = O.positions(rp, G, b)
         for g in range(G):
             rows = list(range(b[g], b[g + 1]))
-            order = sorted([r for r in rows if hot[r]], key=lambda r: (-deg[r], r)) + \
-                [r for r in rows if not hot[r] and deg[r] > 0] + [r for r in rows if deg[r] == 0]
+            order = sorted(rows, key=lambda r: (-deg[r], r))
             assert [pos[r] for r in order] == list(range(len(rows)))
-
-
-def test_hot_columns_are_the_largest_degrees():
-    """Hot set = top-H non-empty columns by (degree desc, index asc), by brute force."""
-    rp, c, v = er_csr(500, 300, 11)
-    deg = np.diff(rp)
-    assert (deg == 0).any(), "fixture should contain empty rows"
-    for H in (0, 1, 17, 500):
-        hot = O.hot_columns(rp, H)
-        order = sorted([r for r in range(500) if deg[r] > 0], key=lambda r: (-deg[r], r))
-        expect = np.zeros(500, np.uint8)
-        expect[order[:H]] = 1
-        assert np.array_equal(hot, expect)
 
 
 def check_bf16_rounding(x, r):
