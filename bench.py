@@ -208,7 +208,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="C5 precision sweep on the C3 matrix (report lines, not the bench line)")
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     wl = dict(WORKLOADS[args.workload], name=args.workload)
     if args.warmup < 3:
         args.warmup = 3
@@ -369,6 +373,58 @@ def run_e2e(T, A, wl, kw, args, N, rank, dist):
             "s_per_step": float(np.mean(times)),
             "note": "create (host canonicalise + partition + layout + H2D, symmetry check skipped) "
                     "+ solve + eigenvalues/eigenvectors (f32) D2H, wall clock"}
+
+
+SWEEP_ARMS = [  # (name, vector storage, compute, value storage)
+    ("DDD", "f64", "f64", "f64"),
+    ("FDF", "f32", "f64", "f32"),
+    ("FFF", "f32", "f32", "f32"),
+    ("bf16val-f32vec-f64", "f32", "f64", "bf16"),
+    ("bf16val-bf16vec-f64", "bf16", "f64", "bf16"),
+]
+
+
+def run_sweep(args):
+    """C5 (BASELINE.json configs[4]; the paper's Fig. 4 analogue):
+    accuracy vs time of every (storage, compute) arm on the C3 matrix, K = 24,
+    m in {24, 192}. Accuracy is normwise against the DDD arm (itself checked
+    against the fp64 oracle by the parity tests); bf16 vectors are report-only
+    (reading Q21). One JSON line per (arm, m)."""
+    import torch
+    import paper_2201_07498_b200 as T
+    torch.cuda.set_device(0)
+    A = make_matrix("C3")
+    K = 24
+    for m in (24, 192):
+        ref = None
+        for name, st, ct, vs in SWEEP_ARMS:
+            with T.TopkEig(A, K, storage=st, compute=ct, values_storage=vs, m=m, check_symmetry=False) as h:
+                ev = torch.zeros(K, dtype=torch.float64, device="cuda")
+                for i in range(args.warmup):
+                    h.solve_async(1, ev.data_ptr(), None)
+                    h.sync()
+                stream = torch.cuda.ExternalStream(h.stream)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = max(3, min(args.steps, 20))
+                e0.record(stream)
+                for i in range(reps):
+                    h.solve_async(1, ev.data_ptr(), None)
+                e1.record(stream)
+                h.sync()
+                ms = e0.elapsed_time(e1) / reps
+                r = h.solve(seed=1, vectors=False)
+                _, _, theta = h.tridiag()
+            theta = np.sort(theta)
+            if ref is None:
+                ref = (theta, r.eigenvalues)
+            errn = float(np.abs(theta - ref[0]).max() / np.abs(ref[0]).max()) if len(theta) == len(ref[0]) else None
+            top = float(np.nanmax(np.abs(r.eigenvalues - ref[1])) / abs(ref[1][0]))
+            print(json.dumps({"kind": "precision_sweep", "workload": "C5 (C3 matrix)", "arm": name, "K": K, "m": m,
+                              "ms_per_solve": ms, "iter_per_s": m / (ms / 1e3),
+                              "ritz_normwise_err_vs_DDD": errn, "topK_err_vs_DDD": top,
+                              "residual_est_max_rel": float(np.nanmax(r.residual_est) / abs(r.eigenvalues[0])),
+                              "report_only": vs == "bf16" and st == "bf16"}), flush=True)
+    return 0
 
 
 if __name__ == "__main__":

@@ -241,13 +241,17 @@ double bf16_bits_to_double(uint16_t b) {
 
 
 void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos) {
+    // stable counting sort by degree, descending (ties keep ascending row index)
     pos.assign((size_t)m.n, 0);
     auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
+#pragma omp parallel for schedule(dynamic, 1)
     for (int32_t q = 0; q < G; ++q) {
-        std::vector<int64_t> rows((size_t)(b[q + 1] - b[q]));
-        std::iota(rows.begin(), rows.end(), b[q]);
-        std::stable_sort(rows.begin(), rows.end(), [&](int64_t x, int64_t y) { return deg(x) > deg(y); });
-        for (size_t p = 0; p < rows.size(); ++p) pos[(size_t)rows[p]] = (int32_t)p;
+        int64_t dmax = 0;
+        for (int64_t r = b[q]; r < b[q + 1]; ++r) dmax = std::max(dmax, deg(r));
+        std::vector<int64_t> start((size_t)dmax + 2, 0);  // start[d] = first position of degree d
+        for (int64_t r = b[q]; r < b[q + 1]; ++r) start[(size_t)(dmax - deg(r)) + 1]++;
+        for (size_t d = 1; d < start.size(); ++d) start[d] += start[d - 1];
+        for (int64_t r = b[q]; r < b[q + 1]; ++r) pos[(size_t)r] = (int32_t)start[(size_t)(dmax - deg(r))]++;
     }
 }
 
@@ -284,19 +288,6 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
         if (len > 0) nne = p + 1;
     }
     out.nnonempty = nne;
-    const int64_t z = z1 - z0;
-    out.col.resize((size_t)z);
-    out.val.resize((size_t)z);
-    // logical CSR: rows in degree order; entries of a row keep their (column-sorted) input order
-#pragma omp parallel for schedule(dynamic, 4096)
-    for (int64_t p = 0; p < ng; ++p) {
-        const int64_t r = r0 + out.perm[(size_t)p];
-        int64_t o = out.rowptr[(size_t)p];
-        for (int64_t k = m.rowptr[(size_t)r]; k < m.rowptr[(size_t)r + 1]; ++k, ++o) {
-            out.col[(size_t)o] = colmap[(size_t)m.col[(size_t)k]];
-            out.val[(size_t)o] = m.val[(size_t)k];
-        }
-    }
     // physical format: big rows (CSR prefix, chunked), then SELL-32 slices
     int64_t nbig = 0;
     while (nbig < nne && out.rowptr[(size_t)nbig + 1] - out.rowptr[(size_t)nbig] > kSellMaxLen) ++nbig;
@@ -325,19 +316,36 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     if (phys >= (1ll << 31) - 256) { err = "padded per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
     out.pcol.resize((size_t)phys);
     out.pval.resize((size_t)phys);
-    std::copy(out.col.begin(), out.col.begin() + zbig, out.pcol.begin());
-    std::copy(out.val.begin(), out.val.begin() + zbig, out.pval.begin());
+    // every entry straight from the canonical CSR to its physical slot (rows in
+    // degree order, entries of a row in their column-sorted input order)
+#pragma omp parallel for schedule(dynamic, 2048)
+    for (int64_t p = 0; p < nne; ++p) {
+        const int64_t r = r0 + out.perm[(size_t)p];
+        const int64_t kb = m.rowptr[(size_t)r], len = m.rowptr[(size_t)r + 1] - kb;
+        size_t dst, stride;
+        if (p < nbig) {
+            dst = (size_t)out.rowptr[(size_t)p];
+            stride = 1;
+        } else {
+            const int64_t sl = (p - nbig) / 32, i = (p - nbig) % 32;
+            dst = (size_t)(out.sell[(size_t)(2 * sl)] + i);
+            stride = 32;
+        }
+        for (int64_t e = 0; e < len; ++e, dst += stride) {
+            out.pcol[dst] = colmap[(size_t)m.col[(size_t)(kb + e)]];
+            out.pval[dst] = m.val[(size_t)(kb + e)];
+        }
+    }
+    // SELL padding: (column 0, value 0) past each row's length
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t sl = 0; sl < nsl; ++sl) {
         const int64_t base = out.sell[(size_t)(2 * sl)], w = out.sell[(size_t)(2 * sl + 1)];
         for (int64_t i = 0; i < 32; ++i) {
             const int64_t p = nbig + 32 * sl + i;
-            const int64_t rb = p < nne ? out.rowptr[(size_t)p] : 0;
-            const int64_t len = p < nne ? out.rowptr[(size_t)p + 1] - rb : 0;
-            for (int64_t e = 0; e < w; ++e) {
-                const size_t k = (size_t)(base + 32 * e + i);
-                out.pcol[k] = e < len ? out.col[(size_t)(rb + e)] : 0;
-                out.pval[k] = e < len ? out.val[(size_t)(rb + e)] : 0.0;
+            const int64_t len = p < nne ? out.rowptr[(size_t)p + 1] - out.rowptr[(size_t)p] : 0;
+            for (int64_t e = len; e < w; ++e) {
+                out.pcol[(size_t)(base + 32 * e + i)] = 0;
+                out.pval[(size_t)(base + 32 * e + i)] = 0.0;
             }
         }
     }
@@ -353,6 +361,25 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
         sl = e;
     }
     return TOPK_OK;
+}
+
+void logical_from_physical(const PartLayout &L, hvec<int32_t> &col, hvec<double> &val) {
+    const int64_t z = L.rowptr.empty() ? 0 : L.rowptr.back();
+    col.resize((size_t)z);
+    val.resize((size_t)z);
+    for (int64_t p = 0; p < L.nnonempty; ++p) {
+        const int64_t rb = L.rowptr[(size_t)p], len = L.rowptr[(size_t)p + 1] - rb;
+        for (int64_t e = 0; e < len; ++e) {
+            size_t src;
+            if (p < L.nbig) src = (size_t)(rb + e);
+            else {
+                const int64_t sl = (p - L.nbig) / 32, i = (p - L.nbig) % 32;
+                src = (size_t)(L.sell[(size_t)(2 * sl)] + 32 * e + i);
+            }
+            col[(size_t)(rb + e)] = L.pcol[src];
+            val[(size_t)(rb + e)] = L.pval[src];
+        }
+    }
 }
 
 }  // namespace topk

@@ -98,8 +98,6 @@ struct LongRow {
 struct PartLayout {
     int64_t row0 = 0, nrows = 0, npad = 0, nnonempty = 0;
     std::vector<int32_t> rowptr;    // nrows+1, logical CSR in degree order
-    hvec<int32_t> col;              // logical, device column entries
-    hvec<double> val;               // logical values (f64 source; rounded at upload)
     std::vector<int32_t> perm;      // nrows: part-local original row at each position
     // physical SpMV format
     int32_t nbig = 0;
@@ -113,5 +111,9 @@ struct PartLayout {
 
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err);
+
+// The logical CSR (degree order; device column entries, values) read back out of
+// the physical arrays (exports and tests).
+void logical_from_physical(const PartLayout &L, hvec<int32_t> &col, hvec<double> &val);
 
 }  // namespace topk

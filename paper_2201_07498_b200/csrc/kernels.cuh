@@ -418,7 +418,10 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
     // issues the loads of all JB columns of its row-vector at once (memory-level
     // parallelism; measured ~6.2 TB/s for a 16-column block on B200), the first
     // pass also forms w (recurrence) and stores it, later passes re-read w (L2).
-    for (int j0 = 0; j0 < it; j0 += JB) {
+    // balanced passes: it columns in ceil(it / JB) passes of equal width
+    const int npass = (it + JB - 1) / JB, width = (it + npass - 1) / npass;
+    for (int j0 = 0; j0 < it; j0 += width) {
+        const int jend = min(it, j0 + width);
         CT acc[JB];
 #pragma unroll
         for (int q = 0; q < JB; ++q) acc[q] = CT(0);
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
             uint4 u[JB];  // raw 16-byte storage vectors, converted at use (register budget)
 #pragma unroll
             for (int q = 0; q < JB; ++q)
-                if (j0 + q < it) u[q] = __ldg(reinterpret_cast<const uint4 *>(V + (size_t)(j0 + q) * a.npad + v * VW));
+                if (j0 + q < jend) u[q] = __ldg(reinterpret_cast<const uint4 *>(V + (size_t)(j0 + q) * a.npad + v * VW));
             CT w[VW];
             if (a.mode == 2) {
                 vload<ST, CT>(src2 + v * VW, w);
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
             }
 #pragma unroll
             for (int q = 0; q < JB; ++q) {
-                if (j0 + q < it) {
+                if (j0 + q < jend) {
                     const ST *ue = reinterpret_cast<const ST *>(&u[q]);
                     CT d = CT(0);
 #pragma unroll
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
             if (lane == 0) part[wid][q] = r;
         }
         __syncthreads();
-        if (tid < JB && j0 + tid < it) {
+        if (tid < JB && j0 + tid < jend) {
             CT r = CT(0);
 #pragma unroll
             for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][tid];
@@ -744,9 +747,10 @@ __global__ void k_jacobi(JacArgs a) {
 //   pass 0: recompute y_k row by row, per-block partials of ||y_k||^2 ->
 //           ex.ritz_part[g][k] (last-arriving block per output group, fixed order)
 //   pass 1: recompute y_k, scale by 1/||y_k|| (norms summed over parts in rank
-//           order) and store once, in the output dtype, row-major in position
-//           order (yt[p][k]); k_unperm then writes the caller's buffer in
-//           original row order (one contiguous K-vector read per row).
+//           order) and store once, in the output dtype, in position order
+//           blocked by output group (yt[g][p][q], k = g KB + q; coalesced
+//           stores); k_unperm then writes the caller's buffer in original row
+//           order (one 32/64-byte sector per group per row).
 // Thread = VW consecutive rows (one 16-byte load per basis column) x KB outputs;
 // block b = (row range b / ngroups, output group b % ngroups). coefS holds the sign
 // fix and the deferred normalisation s_j.
@@ -760,11 +764,11 @@ struct RitzArgs {
     Exch ex;
     void *const *out_ptr;     // device param: output base (pass 1 writes only if non-NULL)
     const int *out_dtype;     // device param: 0 f64, 1 f32
-    void *yt;                 // [npad][K] Ritz vectors in position order, output dtype
+    void *yt;                 // [ceil(K/KB)][npad][KB] Ritz vectors in position order, output dtype
 };
 
-template <typename ST, typename CT, int KB>
-__global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
+template <typename ST, typename CT, int KB, int pass>
+__global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
     constexpr int VW = Vw<ST>::N;
     extern __shared__ double rsm[];  // coef[m'][KB]
     __shared__ CT part[kNT / 32][KB];
@@ -808,15 +812,30 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
         for (int e = 0; e < VW; ++e)
 #pragma unroll
             for (int q = 0; q < KB; ++q) acc[e][q] = CT(0);
-        for (int j = 0; j < mm; ++j) {
-            CT u[VW];
-            vload_cs<ST, CT>(V + (size_t)j * a.npad + v * VW, u);
-            const CT *cj = coef + j * KB;
+        // basis columns 4 at a time: the 4 loads are in flight together (raw
+        // registers), then 4 x VW x KB fp64 FMAs; coefficient pairs via 16-byte
+        // shared-memory broadcasts
+        constexpr int JU = 4;
+        for (int j0 = 0; j0 < mm; j0 += JU) {
+            int4 raw[JU];
 #pragma unroll
-            for (int q = 0; q < KB; ++q) {
-                const CT c = cj[q];
+            for (int t = 0; t < JU; ++t)
+                raw[t] = (j0 + t < mm) ? ld_stream(reinterpret_cast<const int4 *>(V + (size_t)(j0 + t) * a.npad + v * VW))
+                                       : make_int4(0, 0, 0, 0);
 #pragma unroll
-                for (int e = 0; e < VW; ++e) acc[e][q] += c * u[e];
+            for (int t = 0; t < JU; ++t) {
+                if (j0 + t >= mm) break;
+                const ST *ue = reinterpret_cast<const ST *>(&raw[t]);
+                CT u[VW];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) u[e] = cvt<CT>(ue[e]);
+                const CT *cj = coef + (j0 + t) * KB;
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    const CT c = cj[q];
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) acc[e][q] += c * u[e];
+                }
             }
         }
         if (pass == 0) {
@@ -825,22 +844,27 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
 #pragma unroll
                 for (int e = 0; e < VW; ++e) nrm[q] += acc[e][q] * acc[e][q];
         } else {
-            // row-major [position][K]: this thread's KB outputs of a row are one
-            // contiguous, sector-aligned group (whole 32-byte sectors per row)
+            // yt layout [group][position][KB]: this thread's VW rows x KB outputs are
+            // one contiguous block and consecutive lanes own consecutive blocks, so
+            // the stores are fully coalesced 16-byte vectors
+            const size_t o = ((size_t)grp * a.npad + (size_t)v * VW) * KB;
+            if (dt == 0) {
+                double *dst = reinterpret_cast<double *>(a.yt) + o;
 #pragma unroll
-            for (int e = 0; e < VW; ++e) {
-                const int64_t r = v * VW + e;
-                if (r < a.nrows) {
-                    const size_t o = (size_t)r * K + k0;
+                for (int e = 0; e < VW; ++e)
 #pragma unroll
-                    for (int q = 0; q < KB; ++q) {
-                        const double yv = (k0 + q < kf) ? (double)acc[e][q] * inv[q] : 0.0;
-                        if (k0 + q < K) {
-                            if (dt == 0) reinterpret_cast<double *>(a.yt)[o + q] = yv;
-                            else reinterpret_cast<float *>(a.yt)[o + q] = (float)yv;
-                        }
-                    }
-                }
+                    for (int q = 0; q < KB; q += 2)
+                        __stcs(reinterpret_cast<double2 *>(dst + e * KB + q),
+                               make_double2((double)acc[e][q] * inv[q], (double)acc[e][q + 1] * inv[q + 1]));
+            } else {
+                float *dst = reinterpret_cast<float *>(a.yt) + o;
+#pragma unroll
+                for (int e = 0; e < VW; ++e)
+#pragma unroll
+                    for (int q = 0; q < KB; q += 4)
+                        __stcs(reinterpret_cast<float4 *>(dst + e * KB + q),
+                               make_float4((float)(acc[e][q] * inv[q]), (float)(acc[e][q + 1] * inv[q + 1]),
+                                           (float)(acc[e][q + 2] * inv[q + 2]), (float)(acc[e][q + 3] * inv[q + 3])));
             }
         }
     }
@@ -874,9 +898,9 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a, int pass) {
 // a15: eigenvectors back to the original row order: out[k][r] = yt[inv[r]][k]
 // (the caller's K x n_local buffer, vector k contiguous).
 struct UnpermArgs {
-    const void *yt;
+    const void *yt;            // [ceil(K/KB)][npad][KB]
     const int32_t *inv;
-    int64_t nrows;
+    int64_t nrows, npad;
     int K;
     const int *k_found;
     void *const *out_ptr;
@@ -886,17 +910,33 @@ struct UnpermArgs {
 __global__ void __launch_bounds__(kNT) k_unperm(UnpermArgs a) {
     void *out = *a.out_ptr;
     if (!out) return;
-    const int kf = *a.k_found, dt = *a.out_dtype, K = a.K;
+    const int kf = *a.k_found, dt = *a.out_dtype;
     for (int64_t r = (int64_t)blockIdx.x * kNT + threadIdx.x; r < a.nrows; r += (int64_t)gridDim.x * kNT) {
-        const size_t src = (size_t)__ldg(a.inv + r) * K;
-        if (dt == 0) {
-            const double *yt = reinterpret_cast<const double *>(a.yt) + src;
-            double *o = reinterpret_cast<double *>(out);
-            for (int k = 0; k < kf; ++k) __stcs(o + (size_t)k * a.nrows + r, __ldg(yt + k));
-        } else {
-            const float *yt = reinterpret_cast<const float *>(a.yt) + src;
-            float *o = reinterpret_cast<float *>(out);
-            for (int k = 0; k < kf; ++k) __stcs(o + (size_t)k * a.nrows + r, __ldg(yt + k));
+        const size_t p = (size_t)__ldg(a.inv + r);
+        for (int k0 = 0; k0 < kf; k0 += kRitzKB) {
+            const size_t src = ((size_t)(k0 / kRitzKB) * a.npad + p) * kRitzKB;
+            if (dt == 0) {
+                double g[kRitzKB];
+#pragma unroll
+                for (int q = 0; q < kRitzKB; q += 2) {
+                    const double2 t = ld_stream(reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(a.yt) + src + q));
+                    g[q] = t.x;
+                    g[q + 1] = t.y;
+                }
+#pragma unroll
+                for (int q = 0; q < kRitzKB; ++q)
+                    if (k0 + q < kf) __stcs(reinterpret_cast<double *>(out) + (size_t)(k0 + q) * a.nrows + r, g[q]);
+            } else {
+                float g[kRitzKB];
+#pragma unroll
+                for (int q = 0; q < kRitzKB; q += 4) {
+                    const float4 t = ld_stream(reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(a.yt) + src + q));
+                    g[q] = t.x; g[q + 1] = t.y; g[q + 2] = t.z; g[q + 3] = t.w;
+                }
+#pragma unroll
+                for (int q = 0; q < kRitzKB; ++q)
+                    if (k0 + q < kf) __stcs(reinterpret_cast<float *>(out) + (size_t)(k0 + q) * a.nrows + r, g[q]);
+            }
         }
     }
 }

@@ -118,7 +118,7 @@ struct topk_eig_s {
     double tau = 1e-12;
     int use_graph = 1;
     int nsm = 148;
-    int grid_spmv = 0, grid_stream = 0, grid_ritz = 0;
+    int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -247,7 +247,7 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     const int cols = it;
     prof_begin(h, p, 2);
     (void)cols;
-    k_step<ST, CT, kStepJB><<<h->grid_stream, kNT, 0, h->stream>>>(a, it);
+    k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -262,7 +262,7 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
     size_t smem = (size_t)(h->m + 1) * sizeof(double);
     prof_begin(h, p, 3);
-    k_correct<ST, CT><<<h->grid_stream, kNT, smem, h->stream>>>(a, it);
+    k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -334,7 +334,8 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             const unsigned ngroups = (unsigned)((h->K + kRitzKB - 1) / kRitzKB);
             const dim3 grid((unsigned)h->grid_ritz * ngroups);
             prof_begin(h, p, 5 + pass);
-            k_ritz<ST, CT, kRitzKB><<<grid, kNT, smem, h->stream>>>(a, pass);
+            if (pass == 0) k_ritz<ST, CT, kRitzKB, 0><<<grid, kNT, smem, h->stream>>>(a);
+            else k_ritz<ST, CT, kRitzKB, 1><<<grid, kNT, smem, h->stream>>>(a);
             CUDA_TRY(cudaGetLastError());
             prof_end(h, p);
             h->launches++;
@@ -344,7 +345,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // a15 prep: position order -> original row order into the caller's buffer
     for (Part &p : h->parts) {
         UnpermArgs a;
-        a.yt = p.yt; a.inv = p.inv; a.nrows = p.nrows; a.K = h->K; a.k_found = p.st.k_found;
+        a.yt = p.yt; a.inv = p.inv; a.nrows = p.nrows; a.npad = p.npad; a.K = h->K; a.k_found = p.st.k_found;
         a.out_ptr = (void *const *)((char *)h->dparams + sizeof(SolveParams) * (1 + (&p - &h->parts[0])) +
                                     offsetof(SolveParams, out_ptr));
         a.out_dtype = &h->dparams->out_dtype;
@@ -372,12 +373,18 @@ static void set_kernels(topk_eig_s *h) {
     h->grid_spmv = h->nsm * std::max(1, occ);
     int occ2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
-    h->grid_stream = h->nsm * std::max(1, std::min(occ2, 4));
+    h->grid_step = h->nsm * std::max(1, std::min(occ2, 8));
+    int occ4 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_correct<ST, CT>, kNT, (size_t)(h->m + 1) * sizeof(double));
+    h->grid_corr = h->nsm * std::max(1, std::min(occ4, 8));
+    h->grid_stream = h->nsm * 4;
     int occ3 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB>, kNT, (size_t)h->m * kRitzKB * 8);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);
     h->grid_ritz = h->nsm * std::max(1, std::min(occ3, 2));
     CUDA_TRY(cudaFuncSetAttribute(k_correct<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 * kRitzKB * sizeof(double))));
+    CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(1024 * kRitzKB * sizeof(double))));
 }
 
@@ -552,6 +559,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->jac_hl_log2 = hs;
         const size_t jbytes = (size_t)2 * M * ((size_t)1 << ls) * 8 + (size_t)M * 8 + (size_t)M * 4 + (size_t)M * 2 + 64;
         const int items = std::max((M / 2) << hs, (M / 2) << ls);
+        // one thread per 2x2 block update / S column pair of a round (measured: a
+        // single warp serialising them is 3x slower at m = 24)
         h->jac_threads = std::max(32, std::min(1024, (items + 31) / 32 * 32));
         if (jbytes <= 200 * 1024) {
             h->jac_smem = jbytes;
@@ -570,7 +579,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             s = build_part(csr, h->bounds.data(), G, p.g, npad, pos.data(), colmap.data(), L, err);
             if (s != TOPK_OK) return fail(s, err);
             clk.mark("build_part");
-            p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.col.size();
+            p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.rowptr.back();
             p.nchunks = (int)L.chunks.size(); p.nlong = (int)L.longrows.size();
             p.nitems = (int)L.items.size() / 2; p.nbig = L.nbig; p.nnonempty = L.nnonempty;
             p.nphys = (int64_t)L.pcol.size();
@@ -608,9 +617,9 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.y = h->alloc<char>((size_t)npad * vsz);
             p.w = h->alloc<char>((size_t)npad * vsz);
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
-            p.yt = h->alloc<double>((size_t)K * std::max<int64_t>(p.npad, 1));
+            p.yt = h->alloc<double>((size_t)((K + kRitzKB - 1) / kRitzKB) * kRitzKB * std::max<int64_t>(p.npad, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
-            p.slots = h->alloc<double>((size_t)std::max(h->grid_spmv, std::max(h->grid_stream, h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
+            p.slots = h->alloc<double>((size_t)std::max(std::max(h->grid_spmv, h->grid_corr), std::max(std::max(h->grid_stream, h->grid_step), h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
             p.counters = h->alloc<unsigned>(8 + 64);
             carve_state(h.get(), p);
             h->bytes_model += model_bytes(h.get(), p);
@@ -863,16 +872,19 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
             return values_storage == TOPK_F64 ? x
                    : values_storage == TOPK_F32 ? (double)round_f32(x) : bf16_bits_to_double(round_bf16_bits(x));
         };
+        hvec<int32_t> lcol;
+        hvec<double> lval;
+        logical_from_physical(L, lcol, lval);
         if (sizes) {
-            sizes[0] = npad; sizes[1] = L.nrows; sizes[2] = (int64_t)L.col.size(); sizes[3] = L.nnonempty;
+            sizes[0] = npad; sizes[1] = L.nrows; sizes[2] = (int64_t)lcol.size(); sizes[3] = L.nnonempty;
             sizes[4] = L.nbig; sizes[5] = (int64_t)L.chunks.size(); sizes[6] = (int64_t)L.sell.size() / 2;
             sizes[7] = (int64_t)L.items.size() / 2; sizes[8] = (int64_t)L.pcol.size();
         }
         if (rowptr)
             for (size_t i = 0; i < L.rowptr.size(); ++i) rowptr[i] = L.rowptr[i];
-        if (col) std::memcpy(col, L.col.data(), L.col.size() * 4);
+        if (col) std::memcpy(col, lcol.data(), lcol.size() * 4);
         if (val)
-            for (size_t k = 0; k < L.val.size(); ++k) val[k] = rv(L.val[k]);
+            for (size_t k = 0; k < lval.size(); ++k) val[k] = rv(lval[k]);
         if (perm) std::memcpy(perm, L.perm.data(), L.perm.size() * 4);
         if (pcol) std::memcpy(pcol, L.pcol.data(), L.pcol.size() * 4);
         if (pval)

@@ -18,8 +18,15 @@ sell.astype(np.int32).tofile(f"{out}/sell.bin")
 L["items"].astype(np.int32).tofile(f"{out}/items.bin")
 H = int(min(A.n, 200 * 1024 // 4))
 np.array([nb, L["nnonempty"], A.n, H], np.int64).tofile(f"{out}/meta.bin")
-L["pcol"][:z0].astype(np.int32).tofile(f"{out}/bcol.bin")
-L["pval"][:z0].astype(np.float32).tofile(f"{out}/bval.bin")
+bc, bv = L["pcol"][:z0].copy(), L["pval"][:z0].copy()
+if os.environ.get("SORT_ROWS") == "1":  # entries of each big row sorted by device column (position)
+    rp = L["rowptr"]
+    for p in range(nb):
+        a, b = rp[p], rp[p + 1]
+        o = np.argsort(bc[a:b], kind="stable")
+        bc[a:b], bv[a:b] = bc[a:b][o], bv[a:b][o]
+bc.astype(np.int32).tofile(f"{out}/bcol.bin")
+bv.astype(np.float32).tofile(f"{out}/bval.bin")
 L["chunks"].astype(np.int32).tofile(f"{out}/chunks.bin")
 print("sell nnz slots", len(L["pcol"]) - z0, "big nnz", z0, "nbig", nb, "pad frac",
       (len(L["pcol"]) - z0) / max(1, (L["rowptr"][L["nnonempty"]] - z0)) - 1)

@@ -21,6 +21,20 @@ __device__ __forceinline__ float gat(const float *x, const float *hot, int c) {
     float v;
     const unsigned idx = (unsigned)c & 0x7fffffffu;
     if (P == 0) return __ldg(x + idx);
+    if (P == 4) {  // position-based: hub prefix [0, 65536) evict_last, the rest evict_first
+        asm volatile("{.reg .pred p; setp.lt.u32 p, %1, 65536;\n\t"
+                     "@p ld.global.nc.L1::evict_last.f32 %0, [%2];\n\t"
+                     "@!p ld.global.nc.L1::evict_first.f32 %0, [%2];}"
+                     : "=f"(v) : "r"(idx), "l"(x + idx));
+        return v;
+    }
+    if (P == 5) {  // position-based: hub prefix normal, the rest evict_first
+        asm volatile("{.reg .pred p; setp.lt.u32 p, %1, 65536;\n\t"
+                     "@p ld.global.nc.f32 %0, [%2];\n\t"
+                     "@!p ld.global.nc.L1::evict_first.f32 %0, [%2];}"
+                     : "=f"(v) : "r"(idx), "l"(x + idx));
+        return v;
+    }
     if (P == 1) {
         asm volatile("{.reg .pred p; setp.lt.s32 p, %1, 0;\n\t"
                      "@p ld.global.nc.L1::evict_last.f32 %0, [%2];\n\t"
@@ -49,7 +63,7 @@ template <int P, int NT, int STREAM = 0>
 __global__ void __launch_bounds__(NT) k(const int *col, const float *val, const int2 *sell, const int2 *items, int nitems,
                                         int nbig, int nne, const float *x, int H, double *y) {
     extern __shared__ float hot[];
-    if (P >= 2) {
+    if (P == 2 || P == 3) {
         for (int i = threadIdx.x; i < H; i += NT) hot[i] = x[i];
         __syncthreads();
     }
@@ -97,7 +111,7 @@ template <int V, int NT, int P = 0>
 __global__ void __launch_bounds__(NT) kc(const int *col, const float *val, const int4 *chunks, int nch,
                                          const float *x, double *y, int H) {
     extern __shared__ float hot[];
-    if (P >= 2) {
+    if (P == 2 || P == 3) {
         for (int i = threadIdx.x; i < H; i += NT) hot[i] = x[i];
         __syncthreads();
     }
@@ -175,10 +189,8 @@ int main(int argc, char **argv) {
         printf("%-40s %8.3f us   (%s)\n", name, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
     };
     run("SELL P0 ldg 256x8", k<0, 256>, 256, 8, 0);
-    run("SELL P1 evict_last/no_alloc 256x8", k<1, 256>, 256, 8, 0);
-    run("SELL P2 smem/no_alloc 1024x1", k<2, 1024>, 1024, 1, (size_t)H * 4);
-    run("SELL P3 smem/ldg 1024x1", k<3, 1024>, 1024, 1, (size_t)H * 4);
-    run("SELL stream only 256x8", k<0, 256, 1>, 256, 8, 0);
+    run("SELL P4 pos<64k evict_last / evict_first 256x8", k<4, 256>, 256, 8, 0);
+    run("SELL P5 pos<64k normal / evict_first 256x8", k<5, 256>, 256, 8, 0);
     auto bcol = rd<int>(d + "/bcol.bin"); auto bval = rd<float>(d + "/bval.bin"); auto ch = rd<int>(d + "/chunks.bin");
     int *dbc; float *dbv; int4 *dch;
     CK(cudaMalloc(&dbc, bcol.size() * 4 + 4096)); CK(cudaMalloc(&dbv, bval.size() * 4 + 4096)); CK(cudaMalloc(&dch, ch.size() * 4));
@@ -198,11 +210,9 @@ int main(int argc, char **argv) {
         printf("%-40s %8.3f us  %.0f GB/s algorithmic (%s)\n", name, ms * 1e3, bcol.size() * 8.0 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
     runc("chunks scalar P0 256x8", kc<0, 256, 0>, 256, 8);
-    runc("chunks scalar P1 256x8", kc<0, 256, 1>, 256, 8);
-    runc("chunks scalar P2 1024x1", kc<0, 1024, 2>, 1024, 1, (size_t)H * 4);
-    runc("chunks scalar P3 1024x1", kc<0, 1024, 3>, 1024, 1, (size_t)H * 4);
+    runc("chunks scalar P4 256x8", kc<0, 256, 4>, 256, 8);
+    runc("chunks scalar P5 256x8", kc<0, 256, 5>, 256, 8);
     runc("chunks vec4 P0 256x8", kc<1, 256, 0>, 256, 8);
-    runc("chunks vec4 P1 256x8", kc<1, 256, 1>, 256, 8);
-    runc("chunks vec4 P2 1024x1", kc<1, 1024, 2>, 1024, 1, (size_t)H * 4);
+    runc("chunks vec4 P5 256x8", kc<1, 256, 5>, 256, 8);
     return 0;
 }
