@@ -43,12 +43,16 @@ struct LzState {
     double *evals;      // [K]
     double *coefS;      // [m*K]   sign-fixed S[j, sel_k] * s_j (Ritz coefficients)
     double *resid;      // [K]
+    double *gram;       // [m*m] G_jl = u_j . u_l of the stored (unnormalised) basis, summed over parts
+    double *rnrm2;      // [K] ||y_k||^2 of the selected Ritz vectors from the Gram matrix
+    int use_gram;       // 1: Ritz norms from the Gram matrix (k_step_tma path), 0: Ritz pass 0
+    int m;
     double tau;
 };
 
 struct Exch {            // cross-part exchange buffers, slot g written by part g
     double *alpha_part;  // [G]
-    double *hpart;       // [G][m+1]
+    double *hpart;       // [G][2 (m+1)]: reorth dots h_j at [0, m+1), Gram u_j . u_i at [m+1, 2 (m+1))
     double *norm_part;   // [G]
     double *ritz_part;   // [G][K]
     void *replica;       // [G * npad] storage dtype (G > 1)
@@ -78,6 +82,7 @@ __device__ __forceinline__ bool lz_prologue(int it, const LzState &st, const Exc
     if (lead) {
         st.beta[it - 1] = (it == 1) ? 0.0 : b;
         st.scale[it - 1] = s;
+        st.gram[(size_t)(it - 1) * st.m + (it - 1)] = sq;  // ||u_it||^2 (Gram diagonal)
         *st.m_found = it;
     }
     return true;
@@ -102,7 +107,8 @@ struct V1Args {
 
 template <typename ST, typename CT>
 __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
-    __shared__ CT red[kNT / 32];
+    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
+    CT *red = reinterpret_cast<CT *>(red_storage);
     __shared__ int sflag;
     constexpr int VW = Vw<ST>::N;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
     CT t = block_sum<CT, kNT>(nrm, red);
     if (threadIdx.x == 0) a.slots[blockIdx.x] = (double)t;
     if (arrive_last(a.counter, &sflag)) {
-        double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, reinterpret_cast<double *>(red));
+        double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
         if (threadIdx.x == 0) {
             a.ex.norm_part[a.g] = tot;
             *a.counter = 0;
@@ -363,7 +369,8 @@ template <typename ST, typename CT, int JB>
 __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
     constexpr int VW = Vw<ST>::N;
     __shared__ CT part[kNT / 32][JB];
-    __shared__ CT red[kNT / 32];
+    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
+    CT *red = reinterpret_cast<CT *>(red_storage);
     __shared__ int sflag;
     if (*(volatile int *)a.st.done) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
         const CT tb = block_sum<CT, kNT>(nrm, red);
         if (tid == 0) a.slots[blockIdx.x] = (double)tb;
         if (arrive_last(a.counter, &sflag)) {
-            const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, reinterpret_cast<double *>(red));
+            const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
             if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
         }
         return;
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
             double r = 0.0;
             for (int b = lane; b < (int)gridDim.x; b += 32) r += __ldcg(a.slots + (size_t)b * a.ld + j);
             r = warp_sum(r);
-            if (lane == 0) a.ex.hpart[(size_t)a.g * a.ld + j] = r;
+            if (lane == 0) a.ex.hpart[(size_t)a.g * 2 * a.ld + j] = r;
         }
         __syncthreads();
         if (tid == 0) *a.counter = 0u;
@@ -504,14 +511,15 @@ template <typename ST, typename CT>
 __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     constexpr int VW = Vw<ST>::N;
     extern __shared__ double dsm[];  // coef[it]
-    __shared__ CT red[kNT / 32];
+    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
+    CT *red = reinterpret_cast<CT *>(red_storage);
     __shared__ int sflag;
     if (*(volatile int *)a.st.done) return;
     const int tid = threadIdx.x;
     CT *coef = reinterpret_cast<CT *>(dsm);
     for (int j = tid; j < it; j += kNT) {
         double h = 0.0;
-        for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * a.ld + j);
+        for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + j);
         const double sj = a.st.scale[j];
         coef[j] = (CT)(h * sj * sj);
     }
@@ -557,7 +565,262 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     const CT tb = block_sum<CT, kNT>(nrm, red);
     if (tid == 0) a.slots[blockIdx.x] = (double)tb;
     if (arrive_last(a.counter, &sflag)) {
-        const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, reinterpret_cast<double *>(red));
+        const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
+        if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined a9 / a11 for it <= kTmaCols basis columns (the whole paper mode
+// at K <= 24). A persistent CTA per SM walks tiles of R = 4096 B / s rows; for
+// each tile one elected thread issues cp.async.bulk copies of the tile's slice
+// of every needed column (y or w, and V[0..it-1]) into a 2-stage shared-memory
+// ring completed by an mbarrier (tx bytes), so up to ~200 KB per SM are in
+// flight without register cost; the 256 threads then read one 16-byte vector
+// per column per tile from shared memory. Same arithmetic, rounding points and
+// reduction order as k_step / k_correct (deterministic).
+constexpr int kTmaCols = 24;
+constexpr int kTmaColBytes = 4096;
+constexpr size_t kTmaSmem = (size_t)2 * (kTmaCols + 1) * kTmaColBytes;
+
+template <typename ST, typename CT>
+__device__ __forceinline__ void sload(const unsigned char *p, CT (&o)[Vw<ST>::N]) {
+    const uint4 raw = *reinterpret_cast<const uint4 *>(p);
+    const ST *e = reinterpret_cast<const ST *>(&raw);
+#pragma unroll
+    for (int q = 0; q < Vw<ST>::N; ++q) o[q] = cvt<CT>(e[q]);
+}
+
+// Issue one tile's column slices: column c of the stage <- src[c] + r0 (bytes each).
+__device__ __forceinline__ void tma_issue(unsigned char *stage, uint64_t *bar, const unsigned char *const *src,
+                                          int ncol, size_t off, unsigned bytes) {
+    mbar_expect_tx(bar, bytes * (unsigned)ncol);
+    for (int c = 0; c < ncol; ++c) bulk_g2s(stage + (size_t)c * kTmaColBytes, src[c] + off, bytes, bar);
+}
+
+template <typename ST, typename CT>
+__global__ void __launch_bounds__(kNT, 1) k_step_tma(StepArgs a, int it) {
+    constexpr int VW = Vw<ST>::N;
+    constexpr int R = kTmaColBytes / (int)sizeof(ST);  // rows per tile = kNT * VW
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ const unsigned char *srcp[kTmaCols + 1];
+    __shared__ CT part[kNT / 32][kTmaCols];
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    CT c1 = CT(0), c2 = CT(0);
+    if (a.mode != 2) {
+        double al = 0.0;
+        for (int q = 0; q < a.G; ++q) al += __ldcg(a.ex.alpha_part + q);  // l.10, rank order
+        const double bi = a.st.beta[it - 1];
+        if (blockIdx.x == 0 && tid == 0) {
+            a.st.alpha[it - 1] = al;
+            double ts = *a.st.tscale;
+            ts = fmax(ts, fabs(al));
+            ts = fmax(ts, bi);
+            *a.st.tscale = ts;
+        }
+        c1 = (CT)(al * a.st.scale[it - 1]);
+        c2 = (it > 1) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);
+    }
+    const ST *V = reinterpret_cast<const ST *>(a.V);
+    ST *wv = reinterpret_cast<ST *>(a.w);
+    const int ncol = it + 1;  // [base][V0 .. V(it-1)], base = y (mode 0) or V[:, it] (mode 2)
+    if (tid == 0) {
+        srcp[0] = reinterpret_cast<const unsigned char *>(a.mode == 2 ? V + (size_t)it * a.npad
+                                                                      : reinterpret_cast<const ST *>(a.y));
+        for (int j = 0; j < it; ++j) srcp[j + 1] = reinterpret_cast<const unsigned char *>(V + (size_t)j * a.npad);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (a.npad + R - 1) / R;
+    auto issue = [&](int64_t t, int stg) {
+        const int64_t r0 = t * R;
+        const int64_t rows = (a.npad - r0 < (int64_t)R) ? a.npad - r0 : (int64_t)R;
+        const unsigned bytes = (unsigned)(rows * (int64_t)sizeof(ST));
+        tma_issue(tsm + (size_t)stg * (kTmaCols + 1) * kTmaColBytes, &bar[stg], srcp, ncol,
+                  (size_t)r0 * sizeof(ST), bytes);
+    };
+    if (tid == 0) {
+        if ((int64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+        if ((int64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+    }
+    CT acc[kTmaCols], gacc[kTmaCols];  // reorth dots u_j . w; Gram u_j . u_it (j < it - 1)
+#pragma unroll
+    for (int q = 0; q < kTmaCols; ++q) acc[q] = gacc[q] = CT(0);
+    const bool gram = (a.mode == 0);
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int stg = k & 1;
+        mbar_wait(&bar[stg], (unsigned)((k >> 1) & 1));
+        const unsigned char *stage = tsm + (size_t)stg * (kTmaCols + 1) * kTmaColBytes + (size_t)tid * 16;
+        const int64_t row = t * R + (int64_t)tid * VW;
+        if (row < a.npad) {
+            CT w[VW], u1[VW];
+            sload<ST, CT>(stage, w);
+            if (a.mode != 2) {
+                CT u0[VW];
+                sload<ST, CT>(stage + (size_t)it * kTmaColBytes, u1);  // V[it-1] = u_i
+                if (it > 1) sload<ST, CT>(stage + (size_t)(it - 1) * kTmaColBytes, u0);
+#pragma unroll
+                for (int q = 0; q < VW; ++q) w[q] = w[q] - c1 * u1[q] - (it > 1 ? c2 * u0[q] : CT(0));
+                vstore_back<ST, CT>(wv + row, w);  // w rounded once; dots use what was stored
+            }
+#pragma unroll
+            for (int j = 0; j < kTmaCols; ++j) {
+                if (j < it) {
+                    CT u[VW];
+                    sload<ST, CT>(stage + (size_t)(j + 1) * kTmaColBytes, u);
+                    CT d = CT(0), gd = CT(0);
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) d += u[e] * w[e];
+                    acc[j] += d;
+                    if (gram && j < it - 1) {
+#pragma unroll
+                        for (int e = 0; e < VW; ++e) gd += u[e] * u1[e];
+                        gacc[j] += gd;
+                    }
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with this stage
+        if (tid == 0 && t + 2 * (int64_t)gridDim.x < ntiles) issue(t + 2 * (int64_t)gridDim.x, stg);
+    }
+    // block partials: reorth dots at slots [0, it), Gram dots at [ld, ld + it - 1)
+    const int ng = gram ? it - 1 : 0;
+#pragma unroll
+    for (int j = 0; j < kTmaCols; ++j) {
+        if (j < it) {
+            const CT r = warp_sum(acc[j]);
+            if (lane == 0) part[wid][j] = r;
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < it; j += kNT) {
+        CT r = CT(0);
+#pragma unroll
+        for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][j];
+        a.slots[(size_t)blockIdx.x * 2 * a.ld + j] = (double)r;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTmaCols; ++j) {
+        if (j < ng) {
+            const CT r = warp_sum(gacc[j]);
+            if (lane == 0) part[wid][j] = r;
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < ng; j += kNT) {
+        CT r = CT(0);
+#pragma unroll
+        for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][j];
+        a.slots[(size_t)blockIdx.x * 2 * a.ld + a.ld + j] = (double)r;
+    }
+    if (arrive_last(a.counter, &sflag)) {
+        for (int j = wid; j < it + ng; j += kNT / 32) {
+            const int col = j < it ? j : a.ld + (j - it);
+            double r = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) r += __ldcg(a.slots + (size_t)b * 2 * a.ld + col);
+            r = warp_sum(r);
+            if (lane == 0) a.ex.hpart[(size_t)a.g * 2 * a.ld + col] = r;
+        }
+        __syncthreads();
+        if (tid == 0) *a.counter = 0u;
+    }
+}
+
+template <typename ST, typename CT>
+__global__ void __launch_bounds__(kNT, 1) k_correct_tma(CorrArgs a, int it) {
+    constexpr int VW = Vw<ST>::N;
+    constexpr int R = kTmaColBytes / (int)sizeof(ST);
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ const unsigned char *srcp[kTmaCols + 1];
+    __shared__ CT coef[kTmaCols];
+    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
+    CT *red = reinterpret_cast<CT *>(red_storage);
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < it; j += kNT) {
+        double h = 0.0;
+        for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + j);
+        const double sj = a.st.scale[j];
+        coef[j] = (CT)(h * sj * sj);
+    }
+    if (blockIdx.x == 0 && a.in_col < 0 && a.st.use_gram) {
+        // Gram column of u_it (dots computed by k_step_tma), summed over parts in rank order
+        for (int j = tid; j < it - 1; j += kNT) {
+            double gsum = 0.0;
+            for (int q = 0; q < a.G; ++q) gsum += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + a.ld + j);
+            a.st.gram[(size_t)j * a.st.m + (it - 1)] = gsum;
+            a.st.gram[(size_t)(it - 1) * a.st.m + j] = gsum;
+        }
+    }
+    ST *V = reinterpret_cast<ST *>(a.V);
+    ST *dst = V + (size_t)it * a.npad;
+    const int ncol = it + 1;  // [w or V[:, in_col]][V0 .. V(it-1)]
+    if (tid == 0) {
+        srcp[0] = reinterpret_cast<const unsigned char *>(a.in_col < 0 ? reinterpret_cast<const ST *>(a.w)
+                                                                       : V + (size_t)a.in_col * a.npad);
+        for (int j = 0; j < it; ++j) srcp[j + 1] = reinterpret_cast<const unsigned char *>(V + (size_t)j * a.npad);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (a.npad + R - 1) / R;
+    // tiles in DESCENDING order: k_step just streamed the same columns ascending,
+    // so the most recently read ones are still L2-resident
+    auto tile_of = [&](int64_t kk) { return ntiles - 1 - ((int64_t)blockIdx.x + kk * gridDim.x); };
+    auto issue = [&](int64_t t, int stg) {
+        const int64_t r0 = t * R;
+        const int64_t rows = (a.npad - r0 < (int64_t)R) ? a.npad - r0 : (int64_t)R;
+        const unsigned bytes = (unsigned)(rows * (int64_t)sizeof(ST));
+        tma_issue(tsm + (size_t)stg * (kTmaCols + 1) * kTmaColBytes, &bar[stg], srcp, ncol,
+                  (size_t)r0 * sizeof(ST), bytes);
+    };
+    const int64_t nmine = ((int64_t)blockIdx.x < ntiles) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (tid == 0) {
+        if (nmine > 0) issue(tile_of(0), 0);
+        if (nmine > 1) issue(tile_of(1), 1);
+    }
+    CT nrm = CT(0);
+    for (int64_t k = 0; k < nmine; ++k) {
+        const int stg = (int)(k & 1);
+        const int64_t t = tile_of(k);
+        mbar_wait(&bar[stg], (unsigned)((k >> 1) & 1));
+        const unsigned char *stage = tsm + (size_t)stg * (kTmaCols + 1) * kTmaColBytes + (size_t)tid * 16;
+        const int64_t row = t * R + (int64_t)tid * VW;
+        if (row < a.npad) {
+            CT acc[VW];
+            sload<ST, CT>(stage, acc);
+#pragma unroll
+            for (int j = 0; j < kTmaCols; ++j) {
+                if (j < it) {
+                    CT u[VW];
+                    sload<ST, CT>(stage + (size_t)(j + 1) * kTmaColBytes, u);
+                    const CT cj = coef[j];
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) acc[e] -= cj * u[e];
+                }
+            }
+            vstore_back<ST, CT>(dst + row, acc);
+            if (a.rep_slot) vstore<ST, CT>(reinterpret_cast<ST *>(a.rep_slot) + row, acc);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) nrm += acc[e] * acc[e];
+        }
+        __syncthreads();
+        if (tid == 0 && k + 2 < nmine) issue(tile_of(k + 2), stg);
+    }
+    const CT tb = block_sum<CT, kNT>(nrm, red);
+    if (tid == 0) a.slots[blockIdx.x] = (double)tb;
+    if (arrive_last(a.counter, &sflag)) {
+        const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
         if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
     }
 }
@@ -727,6 +990,16 @@ __global__ void k_jacobi(JacArgs a) {
             st.evals[rank] = tc;
             for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[(j << LS) + c] * st.scale[j];
             st.resid[rank] = fabs(st.beta[mm] * S[((mm - 1) << LS) + c]);
+            if (st.use_gram) {  // ||y_k||^2 = c^T G c with c_j = S[j,c] s_j (the sign cancels)
+                double nrm = 0.0;
+                for (int j = 0; j < mm; ++j) {
+                    const double cj = S[(j << LS) + c] * st.scale[j];
+                    double rowsum = 0.0;
+                    for (int l = 0; l < mm; ++l) rowsum += st.gram[(size_t)j * st.m + l] * (S[(l << LS) + c] * st.scale[l]);
+                    nrm += cj * rowsum;
+                }
+                st.rnrm2[rank] = nrm;
+            }
         }
     }
     for (int k = kf + tid; k < K; k += nt) {
@@ -797,7 +1070,9 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
     }
     if (pass == 1 && tid < KB) {
         double s = 0.0;
-        for (int q = 0; q < a.G; ++q) s += __ldcg(a.ex.ritz_part + (size_t)q * K + k0 + tid);
+        if (a.st.use_gram) s = (k0 + tid < kf) ? a.st.rnrm2[k0 + tid] : 1.0;
+        else
+            for (int q = 0; q < a.G; ++q) s += __ldcg(a.ex.ritz_part + (size_t)q * K + k0 + tid);
         inv[tid] = (k0 + tid < kf) ? 1.0 / sqrt(s) : 0.0;
     }
     __syncthreads();

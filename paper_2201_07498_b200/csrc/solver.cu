@@ -119,6 +119,8 @@ struct topk_eig_s {
     int use_graph = 1;
     int nsm = 148;
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
+    bool use_tma = true;  // TMA-pipelined k_step / k_correct for it <= kTmaCols (TOPK_NO_TMA=1: off)
+    bool use_gram = false;  // Ritz norms from the Gram matrix the TMA multi-dot computes (no Ritz pass 0)
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -200,7 +202,7 @@ static void exch_alpha(topk_eig_s *h) {
 static void exch_h(topk_eig_s *h) {
     if (!h->comm) return;
     size_t ld = (size_t)h->m + 1;
-    NCCL_TRY(ncclAllGather(h->ex.hpart + h->rank * ld, h->ex.hpart, ld, ncclFloat64, h->comm, h->stream));
+    NCCL_TRY(ncclAllGather(h->ex.hpart + h->rank * 2 * ld, h->ex.hpart, 2 * ld, ncclFloat64, h->comm, h->stream));
 }
 static void exch_ritz(topk_eig_s *h) {
     if (!h->comm) return;
@@ -247,7 +249,10 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     const int cols = it;
     prof_begin(h, p, 2);
     (void)cols;
-    k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
+    if (mode != 1 && it <= kTmaCols && h->use_tma)
+        k_step_tma<ST, CT><<<h->nsm, kNT, kTmaSmem, h->stream>>>(a, it);
+    else
+        k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -262,7 +267,10 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
     size_t smem = (size_t)(h->m + 1) * sizeof(double);
     prof_begin(h, p, 3);
-    k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
+    if (it <= kTmaCols && h->use_tma)
+        k_correct_tma<ST, CT><<<h->nsm, kNT, kTmaSmem, h->stream>>>(a, it);
+    else
+        k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -320,7 +328,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     }
     if (!want_vectors) return;
     // a14: Ritz projection + normalisation, two streaming passes (norms, output)
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = h->use_gram ? 1 : 0; pass < 2; ++pass) {
         for (Part &p : h->parts) {
             RitzArgs a;
             a.V = p.V; a.npad = p.npad; a.nrows = p.nrows; a.K = h->K; a.G = h->G; a.g = p.g;
@@ -378,6 +386,13 @@ static void set_kernels(topk_eig_s *h) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_correct<ST, CT>, kNT, (size_t)(h->m + 1) * sizeof(double));
     h->grid_corr = h->nsm * std::max(1, std::min(occ4, 8));
     h->grid_stream = h->nsm * 4;
+    CUDA_TRY(cudaFuncSetAttribute(k_step_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_correct_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    {
+        const char *e = std::getenv("TOPK_NO_TMA");
+        h->use_tma = !(e && e[0] == '1');
+        h->use_gram = h->use_tma && h->reorth != -1 && h->m <= kTmaCols;
+    }
     int occ3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);
     h->grid_ritz = h->nsm * std::max(1, std::min(occ3, 2));
@@ -428,6 +443,11 @@ static void carve_state(topk_eig_s *h, Part &p) {
     p.st.resid = reinterpret_cast<double *>(b + o_resid);
     p.st.coefS = reinterpret_cast<double *>(b + o_coef);
     p.st.tau = h->tau;
+    // Gram matrix of the basis and the Ritz norms: device-only (not copied back per solve)
+    p.st.gram = h->alloc<double>((size_t)m * m);
+    p.st.rnrm2 = h->alloc<double>((size_t)K);
+    p.st.m = m;
+    p.st.use_gram = h->use_gram ? 1 : 0;
 }
 
 template <typename T> static T hget(const Part &p, const void *devptr) {
@@ -541,7 +561,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         // exchange buffers (shared by the local parts)
         h->ex.alpha_part = h->alloc<double>((size_t)G);
         h->ex.norm_part = h->alloc<double>((size_t)G);
-        h->ex.hpart = h->alloc<double>((size_t)G * (m + 1));
+        h->ex.hpart = h->alloc<double>((size_t)G * 2 * (m + 1));
         h->ex.ritz_part = h->alloc<double>((size_t)G * K);
 
         if (G > 1) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
@@ -619,7 +639,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
             p.yt = h->alloc<double>((size_t)((K + kRitzKB - 1) / kRitzKB) * kRitzKB * std::max<int64_t>(p.npad, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
-            p.slots = h->alloc<double>((size_t)std::max(std::max(h->grid_spmv, h->grid_corr), std::max(std::max(h->grid_stream, h->grid_step), h->grid_ritz)) * (size_t)std::max(m + 1, K) + 64);
+            p.slots = h->alloc<double>((size_t)std::max(std::max(h->grid_spmv, h->grid_corr), std::max(std::max(h->grid_stream, h->grid_step), h->grid_ritz)) * (size_t)std::max(2 * (m + 2), K) + 64);
             p.counters = h->alloc<unsigned>(8 + 64);
             carve_state(h.get(), p);
             h->bytes_model += model_bytes(h.get(), p);

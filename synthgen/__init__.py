@@ -159,6 +159,8 @@ def config_matrix(name: str):
     C2D: Dirichlet tridiag n=1,000,000.   C2C: cycle Laplacian n=1,000,000.
     C3: R-MAT S=22 (n=4,194,304), 31,457,280 samples, seed 22 -> nnz ~ 60M.
     C3S: R-MAT S=16 (n=65,536), 491,520 samples, seed 16 (C3 shape, oracle-fast).
+    C4: R-MAT ids over 2^27 rejected if >= n = 100,000,000, 1,410,000,000 samples,
+        seed 27 -> nnz ~ 1.5e9 (host RAM ~45 GB while generating).
     """
     if name == "C1":
         return er_coo(10_000, 50_000, 1)
@@ -170,4 +172,6 @@ def config_matrix(name: str):
         return rmat(22, 31_457_280, 22)
     if name == "C3S":
         return rmat(16, 491_520, 16)
+    if name == "C4":
+        return rmat(27, 1_410_000_000, 27, n=100_000_000)
     raise KeyError(name)

@@ -1,0 +1,82 @@
+"""C4 at full size on one B200 (BASELINE.json configs[3]: R-MAT n = 1e8,
+nnz ~ 1.5e9, FDF, K = m = 16), G = 1 and G = 8 loopback parts on one device.
+Opt-in (TOPK_C4=1: ~3 min of generation, ~90 GB host RAM, ~50 GB HBM). Sampled
+parity against the CPU oracle where it can afford n = 1e8:
+  * the SpMV kernel (Alg.1 l.9) on a seeded x, every row, against the oracle's
+    fp64 SpMV with the rigorous per-row bound (len + 2) u sum |a x|;
+  * alpha_1 = v1^T M v1 (Alg.1 l.10) against the oracle (same v1, reading Q8);
+  * the top Ritz pair: true residual ||M y - theta y|| / |theta| (oracle SpMV
+    on the GPU eigenvector) against the residual estimate |beta s_mk|.
+Prints one "C4CHECK {json}" line per run (summarised under profiles/)."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synthgen as S
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("TOPK_C4") != "1", reason="opt-in: TOPK_C4=1")]
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_2201_07498_b200 as T
+    return T
+
+
+def run_c4(T, parts):
+    out = {"config": "C4", "parts": parts}
+    t0 = time.time()
+    A = S.config_matrix("C4")
+    out.update(n=int(A.n), nnz=int(A.nnz), gen_s=round(time.time() - t0, 1))
+    t0 = time.time()
+    K, m = 16, 16
+    with T.TopkEig(A, K, storage="f32", compute="f64", m=m, parts=parts, check_symmetry=False) as h:
+        out["create_s"] = round(time.time() - t0, 1)
+        # SpMV parity, every row
+        x = np.random.default_rng(4).standard_normal(A.n)
+        y = h.debug_spmv(x)
+        xr = x.astype(np.float32).astype(np.float64)
+        av = A.val.astype(np.float32).astype(np.float64)
+        yr = O.spmv(A.rowptr, A.col, av, xr)
+        absprod = O.spmv(A.rowptr, A.col, np.abs(av), np.abs(xr))
+        bound = (np.diff(A.rowptr) + 2) * 2.0 ** -53 * absprod
+        viol = int(np.sum(np.abs(y - yr) > bound))
+        out["spmv_rows_checked"] = int(A.n)
+        out["spmv_bound_violations"] = viol
+        out["spmv_max_err_over_bound"] = float(np.max(np.abs(y - yr) / (bound + 1e-300)))
+        del y, yr, absprod, bound
+        # one solve, alpha_1 and the top Ritz pair
+        t0 = time.time()
+        r = h.solve(seed=1, vectors=True, vec_dtype="f32")
+        out["solve_wall_s"] = round(time.time() - t0, 2)
+        out["ms_solve_device"] = r.info["ms_solve"]
+        alpha, beta, theta = h.tridiag()
+    v1 = O.v1(1, A.n)
+    v1 = v1 / np.linalg.norm(v1)
+    a1 = float(np.dot(v1, O.spmv(A.rowptr, A.col, av, v1)))
+    out["alpha1_gpu"] = float(alpha[0])
+    out["alpha1_oracle"] = a1
+    out["alpha1_rel_err"] = abs(alpha[0] - a1) / abs(a1)
+    y0 = r.eigenvectors[0].astype(np.float64)
+    th = float(r.eigenvalues[0])
+    res = float(np.linalg.norm(O.spmv(A.rowptr, A.col, av, y0) - th * y0) / abs(th))
+    out.update(theta1=th, residual_true_rel=res, residual_est_rel=float(r.residual_est[0] / abs(th)),
+               k_found=int(r.info["k_found"]), iterations=int(r.info["iterations"]))
+    print("C4CHECK " + json.dumps(out), flush=True)
+    return out
+
+
+
+
+@pytest.mark.parametrize("parts", [1, 8])
+def test_c4_full_size(T, parts):
+    out = run_c4(T, parts)
+    assert out["spmv_bound_violations"] == 0
+    assert out["alpha1_rel_err"] <= 1e-6
+    assert out["k_found"] == 16
+    assert abs(out["residual_true_rel"] - out["residual_est_rel"]) <= 1e-4 + 1e-2 * out["residual_est_rel"]
