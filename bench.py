@@ -388,10 +388,15 @@ def run_e2e(T, A, wl, kw, args, N, rank, dist):
     times = []
     h2d = d2h = 0
     for i in range(steps + 1):
+        kwi = dict(kw)
         if dist:
+            # a fresh NCCL unique id per communicator (ids are not reusable)
+            obj = [T.nccl_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            kwi["nccl_id"] = obj[0]
             dist.barrier()
         t0 = time.perf_counter()
-        with T.TopkEig(A, wl["K"], check_symmetry=False, **kw) as h2:
+        with T.TopkEig(A, wl["K"], check_symmetry=False, **kwi) as h2:
             r = h2.solve(seed=500 + i, vectors=True, vec_dtype="f32")
             rp, _, _, _ = h2.layout(0) if i == 0 else (None, None, None, None)
             if i == 0:

@@ -121,6 +121,7 @@ struct topk_eig_s {
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
     bool use_tma = true;  // TMA-pipelined k_step / k_correct for it <= kTmaCols (TOPK_NO_TMA=1: off)
     bool use_gram = false;  // Ritz norms from the Gram matrix the TMA multi-dot computes (no Ritz pass 0)
+    bool tma_correct = false;  // TOPK_TMA_CORRECT=1: TMA-ring k_correct_tma instead of k_correct
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -250,7 +251,7 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     prof_begin(h, p, 2);
     (void)cols;
     if (mode != 1 && it <= kTmaCols && h->use_tma)
-        k_step_tma<ST, CT><<<h->nsm, kNT, kTmaSmem, h->stream>>>(a, it);
+        k_step_tma<ST, CT><<<h->nsm, 256 * kStepNG, kTmaSmem, h->stream>>>(a, it);
     else
         k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
@@ -267,8 +268,10 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
     size_t smem = (size_t)(h->m + 1) * sizeof(double);
     prof_begin(h, p, 3);
-    if (it <= kTmaCols && h->use_tma)
-        k_correct_tma<ST, CT><<<h->nsm, kNT, kTmaSmem, h->stream>>>(a, it);
+    // the register-pipelined correction measured faster than the TMA ring here (57 vs 75 us
+    // at it = 17, gpurun_out/r01n); k_correct_tma stays selectable for experiments
+    if (it <= kTmaCols && h->use_tma && h->tma_correct)
+        k_correct_tma<ST, CT><<<h->nsm, 256 * kCorrNG, kTmaSmem, h->stream>>>(a, it);
     else
         k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
@@ -392,6 +395,8 @@ static void set_kernels(topk_eig_s *h) {
         const char *e = std::getenv("TOPK_NO_TMA");
         h->use_tma = !(e && e[0] == '1');
         h->use_gram = h->use_tma && h->reorth != -1 && h->m <= kTmaCols;
+        const char *e2 = std::getenv("TOPK_TMA_CORRECT");
+        h->tma_correct = e2 && e2[0] == '1';
     }
     int occ3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);

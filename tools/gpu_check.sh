@@ -12,7 +12,7 @@ has() { [[ ",$WHAT," == *",$1,"* ]]; }
 if has smoke; then timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.log; fi
 if has tests; then timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "tests rc=$?"; tail -3 $OUT/pytest_gpu.log; fi
 if has bench; then timeout 900 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?"; tail -c 3000 $OUT/bench.log; fi
-SMALL="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e"
+SMALL="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-ttk"
 if has launches || has full; then
   timeout 600 $SMALL > $OUT/plain.log 2>&1; rc=$?; echo "plain rc=$rc"
   if [ $rc -eq 0 ]; then

@@ -21,6 +21,9 @@ __device__ __forceinline__ float gat(const float *x, const float *hot, int c) {
     float v;
     const unsigned idx = (unsigned)c & 0x7fffffffu;
     if (P == 0) return __ldg(x + idx);
+    if (P == 8) return (float)(idx & 7);   // no gather at all (stream-only bound)
+    if (P == 6) return hot[idx % 51200u];  // all gathers from shared memory (throughput probe)
+    if (P == 7) return hot[idx & 16383u];  // all gathers from a 64 KB smem window
     if (P == 4) {  // position-based: hub prefix [0, 65536) evict_last, the rest evict_first
         asm volatile("{.reg .pred p; setp.lt.u32 p, %1, 65536;\n\t"
                      "@p ld.global.nc.L1::evict_last.f32 %0, [%2];\n\t"
@@ -63,8 +66,9 @@ template <int P, int NT, int STREAM = 0>
 __global__ void __launch_bounds__(NT) k(const int *col, const float *val, const int2 *sell, const int2 *items, int nitems,
                                         int nbig, int nne, const float *x, int H, double *y) {
     extern __shared__ float hot[];
-    if (P == 2 || P == 3) {
-        for (int i = threadIdx.x; i < H; i += NT) hot[i] = x[i];
+    if (P == 2 || P == 3 || P == 6 || P == 7) {
+        const int HH = (P == 7) ? 16384 : H;
+        for (int i = threadIdx.x; i < HH; i += NT) hot[i] = x[i];
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -107,12 +111,13 @@ __global__ void __launch_bounds__(NT) k(const int *col, const float *val, const 
 // big-row chunks (rows of degree > 128, 72% of C3's nnz): warp per chunk
 // V 0: scalar lanes k = zb + lane + 32t (product structure), 8 in flight
 // V 1: 16-byte vectors: lane covers 4 consecutive nnz, aligned groups, masked ends
-template <int V, int NT, int P = 0>
+template <int V, int NT, int P = 0, int GQ = 8>
 __global__ void __launch_bounds__(NT) kc(const int *col, const float *val, const int4 *chunks, int nch,
                                          const float *x, double *y, int H) {
     extern __shared__ float hot[];
-    if (P == 2 || P == 3) {
-        for (int i = threadIdx.x; i < H; i += NT) hot[i] = x[i];
+    if (P == 2 || P == 3 || P == 6 || P == 7) {
+        const int HH = (P == 7) ? 16384 : H;
+        for (int i = threadIdx.x; i < HH; i += NT) hot[i] = x[i];
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -122,7 +127,6 @@ __global__ void __launch_bounds__(NT) kc(const int *col, const float *val, const
         const int zb = C.y, ze = C.y + C.z;
         double acc = 0;
         if (V == 0) {
-            constexpr int GQ = 8;
             for (int k0 = zb + lane; k0 < ze; k0 += 32 * GQ) {
                 int cc[GQ]; float vv[GQ];
 #pragma unroll
@@ -189,8 +193,9 @@ int main(int argc, char **argv) {
         printf("%-40s %8.3f us   (%s)\n", name, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
     };
     run("SELL P0 ldg 256x8", k<0, 256>, 256, 8, 0);
-    run("SELL P4 pos<64k evict_last / evict_first 256x8", k<4, 256>, 256, 8, 0);
-    run("SELL P5 pos<64k normal / evict_first 256x8", k<5, 256>, 256, 8, 0);
+    run("SELL P6 all-smem 1024x1", k<6, 1024>, 1024, 1, (size_t)H * 4);
+    run("SELL P2 smem/no_alloc 1024x1", k<2, 1024>, 1024, 1, (size_t)H * 4);
+    run("SELL P0 ldg 1024x1", k<0, 1024>, 1024, 1, 0);
     auto bcol = rd<int>(d + "/bcol.bin"); auto bval = rd<float>(d + "/bval.bin"); auto ch = rd<int>(d + "/chunks.bin");
     int *dbc; float *dbv; int4 *dch;
     CK(cudaMalloc(&dbc, bcol.size() * 4 + 4096)); CK(cudaMalloc(&dbv, bval.size() * 4 + 4096)); CK(cudaMalloc(&dch, ch.size() * 4));
@@ -210,9 +215,11 @@ int main(int argc, char **argv) {
         printf("%-40s %8.3f us  %.0f GB/s algorithmic (%s)\n", name, ms * 1e3, bcol.size() * 8.0 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
     runc("chunks scalar P0 256x8", kc<0, 256, 0>, 256, 8);
-    runc("chunks scalar P4 256x8", kc<0, 256, 4>, 256, 8);
-    runc("chunks scalar P5 256x8", kc<0, 256, 5>, 256, 8);
-    runc("chunks vec4 P0 256x8", kc<1, 256, 0>, 256, 8);
-    runc("chunks vec4 P5 256x8", kc<1, 256, 5>, 256, 8);
+    runc("chunks scalar P8 stream-only 256x8", kc<0, 256, 8>, 256, 8);
+    runc("chunks scalar P8 stream-only GQ16 256x8", kc<0, 256, 8, 16>, 256, 8);
+    runc("chunks scalar P0 GQ16 256x8", kc<0, 256, 0, 16>, 256, 8);
+    runc("chunks scalar P0 GQ4 256x8", kc<0, 256, 0, 4>, 256, 8);
+    runc("chunks vec4 P8 stream-only 256x8", kc<1, 256, 8>, 256, 8);
+    runc("chunks vec4 P6 all-smem 1024x1", kc<1, 1024, 6>, 1024, 1, (size_t)H * 4);
     return 0;
 }
