@@ -121,6 +121,20 @@ def make_matrix(name: str):
     return S.config_matrix(name)
 
 
+def gather_bound(nnz_g, t_ms):
+    """The SpMV's other ceiling: one random 4/8-byte x gather
+    per nonzero. profiles/gather_ceiling.json holds the measured B200 rate of
+    uniform random gathers from an L2-resident vector (tools/lab/bwlab.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_ceiling.json")) as f:
+            g = json.load(f)
+        ach = nnz_g / (t_ms * 1e-3)
+        return {"gathers_per_launch": int(nnz_g), "achieved_per_s": ach,
+                "ceiling_per_s": g["gathers_per_s"], "frac": ach / g["gathers_per_s"], "source": g["source"]}
+    except Exception:
+        return None
+
+
 def spmv_bytes(nnz_g, n_g, n_x, s, sv):
     """B_spmv = z_g (4 + s_v) + 4 (n_g + 1) + s n_x + s n_g."""
     return nnz_g * (4 + sv) + 4 * (n_g + 1) + s * n_x + s * n_g
@@ -331,7 +345,8 @@ def main():
                              "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
                              "peak_source": peak_src, "traffic": traffic,
                              "algorithmic_bytes_per_launch": b_spmv, "avg_launch_ms": t_spmv,
-                             "launches_timed": spmv_n},
+                             "launches_timed": spmv_n,
+                             "gather_bound": gather_bound(nnz_g, t_spmv)},
                 "kernels": kernels,
                 "cpu_baseline": cpu,
                 "e2e": e2e,

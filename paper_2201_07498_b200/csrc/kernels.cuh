@@ -967,36 +967,70 @@ __global__ void k_jacobi(JacArgs a) {
                 rot[k] = doit;
             }
             __syncthreads();
-            // phase B1: T <- J^T T J as 2x2 blocks (rows of pair k, columns of pair l)
-            for (int i = tid; i < (half << HS); i += nt) {
-                const int k = i >> HS, l = i & (HD - 1);
-                if (l >= half || !(rot[k] | rot[l])) continue;
-                const int pk = pq[2 * k], qk = pq[2 * k + 1], pl = pq[2 * l], ql = pq[2 * l + 1];
-                const double ck = cs[2 * k], sk = cs[2 * k + 1], cl = cs[2 * l], sl = cs[2 * l + 1];
-                double *r0 = T + (pk << LS), *r1 = T + (qk << LS);
-                const double b00 = r0[pl], b01 = r0[ql], b10 = r1[pl], b11 = r1[ql];
-                const double e00 = cl * b00 - sl * b01, e01 = sl * b00 + cl * b01;  // columns (T J)
-                const double e10 = cl * b10 - sl * b11, e11 = sl * b10 + cl * b11;
-                r0[pl] = ck * e00 - sk * e10;                                      // rows (J^T .)
-                r1[pl] = sk * e00 + ck * e10;
-                if (k == l && rot[k]) {
-                    r0[ql] = 0.0;
-                    r1[pl] = 0.0;
-                } else {
-                    r0[ql] = ck * e01 - sk * e11;
+            // phase B1: T <- J^T T J as 2x2 blocks (rows of pair k, columns of pair l).
+            // Items are processed in batches of JB_: all loads of a batch first,
+            // then the math, then the stores (items are disjoint within a round),
+            // so a thread with many items pays one memory latency per batch
+            // (matters when T, S live in global memory, m > 96)
+            constexpr int JB_ = 4;
+            const int nB1 = half << HS;
+            for (int i0 = tid; i0 < nB1; i0 += nt * JB_) {
+                double b[JB_][4];
+                int ok[JB_];
+#pragma unroll
+                for (int u = 0; u < JB_; ++u) {
+                    const int i = i0 + u * nt;
+                    const int k = i >> HS, l = i & (HD - 1);
+                    ok[u] = (i < nB1) && l < half && (rot[k] | rot[l]);
+                    if (ok[u]) {
+                        const int pk = pq[2 * k], qk = pq[2 * k + 1], pl = pq[2 * l], ql = pq[2 * l + 1];
+                        const double *r0 = T + (pk << LS), *r1 = T + (qk << LS);
+                        b[u][0] = r0[pl]; b[u][1] = r0[ql]; b[u][2] = r1[pl]; b[u][3] = r1[ql];
+                    }
                 }
-                r1[ql] = sk * e01 + ck * e11;
+#pragma unroll
+                for (int u = 0; u < JB_; ++u) {
+                    if (!ok[u]) continue;
+                    const int i = i0 + u * nt;
+                    const int k = i >> HS, l = i & (HD - 1);
+                    const int pk = pq[2 * k], qk = pq[2 * k + 1], pl = pq[2 * l], ql = pq[2 * l + 1];
+                    const double ck = cs[2 * k], sk = cs[2 * k + 1], cl = cs[2 * l], sl = cs[2 * l + 1];
+                    double *r0 = T + (pk << LS), *r1 = T + (qk << LS);
+                    const double e00 = cl * b[u][0] - sl * b[u][1], e01 = sl * b[u][0] + cl * b[u][1];  // T J
+                    const double e10 = cl * b[u][2] - sl * b[u][3], e11 = sl * b[u][2] + cl * b[u][3];
+                    const bool diag = (k == l) && rot[k];
+                    r0[pl] = ck * e00 - sk * e10;                                                  // J^T .
+                    r1[pl] = diag ? 0.0 : sk * e00 + ck * e10;
+                    r0[ql] = diag ? 0.0 : ck * e01 - sk * e11;
+                    r1[ql] = sk * e01 + ck * e11;
+                }
             }
-            // phase B2: S <- S J (columns p, q), row r
-            for (int i = tid; i < (half << LS); i += nt) {
-                const int k = i >> LS, r = i & (LD - 1);
-                if (r >= mm || !rot[k]) continue;
-                const int p = pq[2 * k], q = pq[2 * k + 1];
-                const double c = cs[2 * k], sn = cs[2 * k + 1];
-                double *Sr = S + (r << LS);
-                const double sp = Sr[p], sq = Sr[q];
-                Sr[p] = c * sp - sn * sq;
-                Sr[q] = sn * sp + c * sq;
+            // phase B2: S <- S J (columns p, q), row r, same batching
+            const int nB2 = half << LS;
+            for (int i0 = tid; i0 < nB2; i0 += nt * JB_) {
+                double sv[JB_][2];
+                int ok[JB_];
+#pragma unroll
+                for (int u = 0; u < JB_; ++u) {
+                    const int i = i0 + u * nt;
+                    const int k = i >> LS, r = i & (LD - 1);
+                    ok[u] = (i < nB2) && r < mm && rot[k];
+                    if (ok[u]) {
+                        const double *Sr = S + (r << LS);
+                        sv[u][0] = Sr[pq[2 * k]];
+                        sv[u][1] = Sr[pq[2 * k + 1]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < JB_; ++u) {
+                    if (!ok[u]) continue;
+                    const int i = i0 + u * nt;
+                    const int k = i >> LS, r = i & (LD - 1);
+                    const double c = cs[2 * k], sn = cs[2 * k + 1];
+                    double *Sr = S + (r << LS);
+                    Sr[pq[2 * k]] = c * sv[u][0] - sn * sv[u][1];
+                    Sr[pq[2 * k + 1]] = sn * sv[u][0] + c * sv[u][1];
+                }
             }
             __syncthreads();
         }

@@ -292,3 +292,54 @@ def test_c3_full_size_parity(T):
     ref = O.solve(A.rowptr, A.col, A.val, K=24, m=24, seed=1)
     r = T.solve(A, 24, storage="f32", compute="f64", m=24, seed=1, vec_dtype="f32", check_symmetry=False)
     check_solve(r, ref, 1e-4)
+
+
+# ------------------------------------------------------------------ kernel-path equivalence
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_tma_path_matches_register_path(T, c3s, storage, monkeypatch):
+    """The TMA multi-dot (k_step_tma, Gram-based Ritz norms) and the register
+    multi-dot + Ritz norm pass compute the same iteration: Ritz values agree to
+    rounding, eigenvectors to the vector tolerance."""
+    K, m = 16, 24
+    monkeypatch.setenv("TOPK_NO_TMA", "0")
+    with T.TopkEig(c3s, K, storage, "f64", m=m) as h:
+        r1 = h.solve(seed=9)
+        _, _, t1 = h.tridiag()
+    monkeypatch.setenv("TOPK_NO_TMA", "1")
+    with T.TopkEig(c3s, K, storage, "f64", m=m) as h:
+        r2 = h.solve(seed=9)
+        _, _, t2 = h.tridiag()
+    tol = 1e-12 if storage == "f64" else 1e-6
+    assert normwise(t1, t2) <= tol
+    for k in range(K):
+        y1, y2 = r1.eigenvectors[k], r2.eigenvectors[k]
+        assert abs(np.linalg.norm(y1) - 1) < 1e-6 and abs(np.linalg.norm(y2) - 1) < 1e-6
+        assert min(np.linalg.norm(y1 - y2), np.linalg.norm(y1 + y2)) <= (1e-10 if storage == "f64" else 1e-4)
+
+
+# ------------------------------------------------------------------ closed form, random start (P5 via the ABI)
+@pytest.mark.parametrize("kind", ["dirichlet", "cycle"])
+def test_kahan_bound_1M_random_start(T, kind):
+    """C2 (n = 1e6), random v1, K = m = 16: every Ritz value lies within its true
+    residual ||A y - theta y|| of a closed-form eigenvalue (Kahan/Parlett bound;
+    SURVEY P5), residual computed by the oracle's SpMV on the GPU eigenvector."""
+    n = 1_000_000
+    A = S.dirichlet(n) if kind == "dirichlet" else S.cycle_laplacian(n)
+    r = T.solve(A, 16, storage="f64", compute="f64", m=16, seed=3)
+    k = np.arange(1, n + 1) if kind == "dirichlet" else np.arange(n)
+    lam = np.sort(2 - 2 * np.cos((np.pi if kind == "dirichlet" else 2 * np.pi) * k / ((n + 1) if kind == "dirichlet" else n)))
+    for th, y in zip(r.eigenvalues, r.eigenvectors):
+        res = np.linalg.norm(O.spmv(A.rowptr, A.col, A.val, y) - th * y)
+        i = np.searchsorted(lam, th)
+        gap = min(abs(lam[min(i, n - 1)] - th), abs(lam[max(i - 1, 0)] - th))
+        assert gap <= res * (1 + 1e-6) + 1e-12
+
+
+# ------------------------------------------------------------------ full C3 size, fp64
+def test_c3_full_size_parity_ddd(T):
+    """C3 at full size in DDD (f64 storage and compute): Ritz values within
+    1e-8 normwise of the oracle, vectors within 1e-5 (north-star gates)."""
+    A = S.config_matrix("C3")
+    ref = O.solve(A.rowptr, A.col, A.val, K=24, m=24, seed=2)
+    r = T.solve(A, 24, storage="f64", compute="f64", m=24, seed=2, check_symmetry=False)
+    check_solve(r, ref, 1e-8)
