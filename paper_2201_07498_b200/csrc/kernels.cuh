@@ -893,7 +893,7 @@ __device__ __forceinline__ int rr_player(int pos, int round, int M) {
 }
 
 template <bool kSmem>
-__global__ void k_jacobi(JacArgs a) {
+__global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
     extern __shared__ double jsm[];
     __shared__ int s_rot;
     __shared__ double s_fro;
@@ -972,7 +972,7 @@ __global__ void k_jacobi(JacArgs a) {
             // then the math, then the stores (items are disjoint within a round),
             // so a thread with many items pays one memory latency per batch
             // (matters when T, S live in global memory, m > 96)
-            constexpr int JB_ = 4;
+            constexpr int JB_ = kSmem ? 1 : 4;
             const int nB1 = half << HS;
             for (int i0 = tid; i0 < nB1; i0 += nt * JB_) {
                 double b[JB_][4];

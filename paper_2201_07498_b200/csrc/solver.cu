@@ -587,6 +587,13 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         // one thread per 2x2 block update / S column pair of a round (measured: a
         // single warp serialising them is 3x slower at m = 24)
         h->jac_threads = std::max(32, std::min(1024, (items + 31) / 32 * 32));
+        {
+            cudaFuncAttributes fa{};
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_jacobi<false>));
+            h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
+            CUDA_TRY(cudaFuncGetAttributes(&fa, k_jacobi<true>));
+            h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
+        }
         if (jbytes <= 200 * 1024) {
             h->jac_smem = jbytes;
             CUDA_TRY(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
