@@ -27,7 +27,8 @@ namespace topk {
 constexpr int kNT = 256;  // threads per block for the streaming kernels
 constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no shared memory)
 constexpr int kRitzKB = 8;  // Ritz outputs per thread
-constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step
+constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
+constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
 
 struct LzState {
     double *alpha;      // [m]     alpha_1..alpha_m
@@ -490,6 +491,97 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
 }
 
 // ---------------------------------------------------------------------------
+// a9 (reorth on), exact-width passes: one launch covers basis columns
+// [j0, j0 + NC) with NC a compile-time constant, so every row-vector issues
+// all NC 16-byte loads at once into raw registers without predication
+// (measured: 17 columns + y, u_i, u_{i-1} and the w store in ONE pass run at
+// ~6.2 TB/s on B200, tools/lab/step_lab.cu). The host splits `it` columns into
+// balanced passes of <= 16..17 columns; the first pass (j0 = 0) also forms the
+// recurrence w = y - alpha_i v_i - beta_i v_{i-1} (mode 0) and stores it rounded.
+// Same arithmetic, rounding points and reduction order as k_step.
+template <typename ST, typename CT, int NC>
+__global__ void __launch_bounds__(kNT, 2) k_stepw(StepArgs a, int it, int j0) {
+    constexpr int VW = Vw<ST>::N;
+    __shared__ CT part[kNT / 32][NC];
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const ST *__restrict__ V = reinterpret_cast<const ST *>(a.V);
+    const int64_t nvec = a.npad / VW;
+    CT c1 = CT(0), c2 = CT(0);
+    const bool form_w = (a.mode == 0 && j0 == 0);
+    if (form_w) {
+        double al = 0.0;
+        for (int q = 0; q < a.G; ++q) al += __ldcg(a.ex.alpha_part + q);  // l.10, rank order
+        const double bi = a.st.beta[it - 1];
+        if (blockIdx.x == 0 && tid == 0) {
+            a.st.alpha[it - 1] = al;
+            double ts = *a.st.tscale;
+            ts = fmax(ts, fabs(al));
+            ts = fmax(ts, bi);
+            *a.st.tscale = ts;
+        }
+        c1 = (CT)(al * a.st.scale[it - 1]);                       // alpha_i * s_i
+        c2 = (it > 1) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);    // beta_i * s_{i-1}
+    }
+    const ST *ucur = V + (size_t)(it - 1) * a.npad;
+    const ST *uprev = V + (size_t)(it > 1 ? it - 2 : 0) * a.npad;
+    const ST *yv = reinterpret_cast<const ST *>(a.y);
+    ST *wv = reinterpret_cast<ST *>(a.w);
+    const ST *base = (a.mode == 2) ? V + (size_t)it * a.npad : wv;
+    CT acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = CT(0);
+    for (int64_t v = (int64_t)blockIdx.x * kNT + tid; v < nvec; v += (int64_t)gridDim.x * kNT) {
+        uint4 u[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) u[q] = __ldg(reinterpret_cast<const uint4 *>(V + (size_t)(j0 + q) * a.npad + v * VW));
+        CT w[VW];
+        if (form_w) {
+            CT yy[VW], u1[VW], u0[VW];
+            vload<ST, CT>(yv + v * VW, yy);
+            vload<ST, CT>(ucur + v * VW, u1);
+            if (it > 1) vload<ST, CT>(uprev + v * VW, u0);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) w[e] = yy[e] - c1 * u1[e] - (it > 1 ? c2 * u0[e] : CT(0));
+            vstore_back<ST, CT>(wv + v * VW, w);  // w rounded once; dots use what was stored
+        } else {
+            vload<ST, CT>(base + v * VW, w);
+        }
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const ST *ue = reinterpret_cast<const ST *>(&u[q]);
+            CT d = CT(0);
+#pragma unroll
+            for (int e = 0; e < VW; ++e) d += cvt<CT>(ue[e]) * w[e];
+            acc[q] += d;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+        const CT r = warp_sum(acc[q]);
+        if (lane == 0) part[wid][q] = r;
+    }
+    __syncthreads();
+    for (int q = tid; q < NC; q += kNT) {
+        CT r = CT(0);
+#pragma unroll
+        for (int w8 = 0; w8 < kNT / 32; ++w8) r += part[w8][q];
+        a.slots[(size_t)blockIdx.x * a.ld + j0 + q] = (double)r;
+    }
+    if (arrive_last(a.counter, &sflag)) {
+        for (int q = wid; q < NC; q += kNT / 32) {
+            double r = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) r += __ldcg(a.slots + (size_t)b * a.ld + j0 + q);
+            r = warp_sum(r);
+            if (lane == 0) a.ex.hpart[(size_t)a.g * 2 * a.ld + j0 + q] = r;
+        }
+        __syncthreads();
+        if (tid == 0) *a.counter = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // a11: correction + publish: u_{i+1} = w - sum_j h_j v_j (h_j = s_j * dot_j),
 // rounded once; written to V column `it` (+ the replica slot when G > 1); norm
 // partial for beta_{i+1}. in_col: -1 reads w, else reads V column in_col
@@ -517,19 +609,29 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     if (*(volatile int *)a.st.done) return;
     const int tid = threadIdx.x;
     CT *coef = reinterpret_cast<CT *>(dsm);
+    double *hd = dsm + a.ld;   // [it] raw dots H_j (fp64)
+    double *cd = hd + a.ld;    // [it] fp64 coefficients
     for (int j = tid; j < it; j += kNT) {
         double h = 0.0;
         for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + j);
         const double sj = a.st.scale[j];
         coef[j] = (CT)(h * sj * sj);
+        hd[j] = h;
+        cd[j] = h * sj * sj;
     }
-    if (blockIdx.x == 0 && a.in_col < 0 && a.st.use_gram) {
-        // Gram column of u_it (dots computed by k_step_tma), summed over parts in rank order
-        for (int j = tid; j < it - 1; j += kNT) {
-            double gsum = 0.0;
-            for (int q = 0; q < a.G; ++q) gsum += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + a.ld + j);
-            a.st.gram[(size_t)j * a.st.m + (it - 1)] = gsum;
-            a.st.gram[(size_t)(it - 1) * a.st.m + j] = gsum;
+    __syncthreads();
+    if (blockIdx.x == 0 && a.st.use_gram && it < a.st.m) {
+        // Gram column of the new basis vector u_{it+1} = b - sum_l coef_l u_l (b = w, or
+        // the first-pass vector for CGS2) from the dots H_j = u_j . b this iteration
+        // measured and the Gram of the older columns: G_{j,it} = H_j - sum_l coef_l G_{j,l}
+        // (fp64; exact up to the storage rounding of u_{it+1}, reading Q24).
+        // Its diagonal ||u_{it+1}||^2 is stored exactly by the next SpMV prologue.
+        const int m = a.st.m;
+        for (int j = tid; j < it; j += kNT) {
+            double g = hd[j];
+            for (int l = 0; l < it; ++l) g -= cd[l] * a.st.gram[(size_t)j * m + l];
+            a.st.gram[(size_t)j * m + it] = g;
+            a.st.gram[(size_t)it * m + j] = g;
         }
     }
     __syncthreads();
@@ -677,7 +779,7 @@ __global__ void __launch_bounds__(256 * kStepNG, 1) k_step_tma(StepArgs a, int i
     CT acc[JPG], gacc[JPG];
 #pragma unroll
     for (int q = 0; q < JPG; ++q) acc[q] = gacc[q] = CT(0);
-    const bool gram = (a.mode == 0);
+    const bool gram = false;  // Gram entries come from the k_correct recursion (Q24)
     int k = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
         const int stg = k & 1;
@@ -769,19 +871,23 @@ __global__ void __launch_bounds__(256 * kCorrNG, 1) k_correct_tma(CorrArgs a, in
     if (*(volatile int *)a.st.done) return;
     const int tid = threadIdx.x;
     const int grp = tid % NG, vt = tid / NG;
+    __shared__ double hd[kTmaCols], cd[kTmaCols];
     for (int j = tid; j < it; j += NT) {
         double h = 0.0;
         for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + j);
         const double sj = a.st.scale[j];
         coef[j] = (CT)(h * sj * sj);
+        hd[j] = h;
+        cd[j] = h * sj * sj;
     }
-    if (blockIdx.x == 0 && a.in_col < 0 && a.st.use_gram) {
-        // Gram column of u_it (dots computed by k_step_tma), summed over parts in rank order
-        for (int j = tid; j < it - 1; j += NT) {
-            double gsum = 0.0;
-            for (int q = 0; q < a.G; ++q) gsum += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + a.ld + j);
-            a.st.gram[(size_t)j * a.st.m + (it - 1)] = gsum;
-            a.st.gram[(size_t)(it - 1) * a.st.m + j] = gsum;
+    __syncthreads();
+    if (blockIdx.x == 0 && a.st.use_gram && it < a.st.m) {  // Gram recursion, as in k_correct
+        const int m = a.st.m;
+        for (int j = tid; j < it; j += NT) {
+            double g = hd[j];
+            for (int l = 0; l < it; ++l) g -= cd[l] * a.st.gram[(size_t)j * m + l];
+            a.st.gram[(size_t)j * m + it] = g;
+            a.st.gram[(size_t)it * m + j] = g;
         }
     }
     ST *V = reinterpret_cast<ST *>(a.V);

@@ -122,6 +122,8 @@ struct topk_eig_s {
     bool use_tma = true;  // TMA-pipelined k_step / k_correct for it <= kTmaCols (TOPK_NO_TMA=1: off)
     bool use_gram = false;  // Ritz norms from the Gram matrix the TMA multi-dot computes (no Ritz pass 0)
     bool tma_correct = false;  // TOPK_TMA_CORRECT=1: TMA-ring k_correct_tma instead of k_correct
+    bool tma_step = false;     // TOPK_TMA_STEP=1: TMA-ring k_step_tma instead of k_stepw
+    int grid_stepw[kStepMaxNC + 1] = {0};
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -238,6 +240,34 @@ static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     h->launches++;
 }
 
+template <typename ST, typename CT, int NC>
+static void stepw_one(topk_eig_s *h, const StepArgs &a, int it, int j0) {
+    k_stepw<ST, CT, NC><<<h->grid_stepw[NC], kNT, 0, h->stream>>>(a, it, j0);
+    CUDA_TRY(cudaGetLastError());
+}
+template <typename ST, typename CT, int NC>
+static void stepw_dispatch(topk_eig_s *h, const StepArgs &a, int it, int j0, int width) {
+    if constexpr (NC > kStepMaxNC) {
+        throw CudaFail("multi-dot pass wider than kStepMaxNC");
+    } else {
+        if (width == NC) stepw_one<ST, CT, NC>(h, a, it, j0);
+        else stepw_dispatch<ST, CT, NC + 1>(h, a, it, j0, width);
+    }
+}
+template <typename ST, typename CT>
+static void launch_stepw(topk_eig_s *h, const StepArgs &a, int it, int j0, int width) {
+    stepw_dispatch<ST, CT, 1>(h, a, it, j0, width);
+}
+template <typename ST, typename CT, int NC>
+static void stepw_grids(topk_eig_s *h) {
+    if constexpr (NC <= kStepMaxNC) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stepw<ST, CT, NC>, kNT, 0);
+        h->grid_stepw[NC] = h->nsm * std::max(1, std::min(occ, 8));
+        stepw_grids<ST, CT, NC + 1>(h);
+    }
+}
+
 template <typename ST, typename CT>
 static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     StepArgs a;
@@ -247,16 +277,27 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
     a.npad = p.npad; a.ld = h->m + 1;
     a.slots = p.slots; a.counter = p.counters + 2;
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.mode = mode;
-    const int cols = it;
     prof_begin(h, p, 2);
-    (void)cols;
-    if (mode != 1 && it <= kTmaCols && h->use_tma)
-        k_step_tma<ST, CT><<<h->nsm, 256 * kStepNG, kTmaSmem, h->stream>>>(a, it);
-    else
+    if (mode == 1) {  // reorth off: recurrence + publish only
         k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
-    CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+    } else if (h->use_tma && h->tma_step && it <= kTmaCols) {
+        k_step_tma<ST, CT><<<h->nsm, 256 * kStepNG, kTmaSmem, h->stream>>>(a, it);
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+    } else {
+        // exact-width passes: one pass up to 17 columns, else balanced passes of <= 16
+        const int npass = (it <= kStepMaxNC) ? 1 : (it + 15) / 16;
+        int j0 = 0;
+        for (int ps = 0; ps < npass; ++ps) {
+            const int width = (it - j0 + (npass - ps) - 1) / (npass - ps);
+            launch_stepw<ST, CT>(h, a, it, j0, width);
+            j0 += width;
+            h->launches++;
+        }
+    }
     prof_end(h, p);
-    h->launches++;
 }
 
 template <typename ST, typename CT>
@@ -266,7 +307,7 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
     a.npad = p.npad; a.ld = h->m + 1;
     a.slots = p.slots; a.counter = p.counters + 3;
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
-    size_t smem = (size_t)(h->m + 1) * sizeof(double);
+    size_t smem = (size_t)3 * (h->m + 1) * sizeof(double);
     prof_begin(h, p, 3);
     // the register-pipelined correction measured faster than the TMA ring here (57 vs 75 us
     // at it = 17, gpurun_out/r01n); k_correct_tma stays selectable for experiments
@@ -386,17 +427,21 @@ static void set_kernels(topk_eig_s *h) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
     h->grid_step = h->nsm * std::max(1, std::min(occ2, 8));
     int occ4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_correct<ST, CT>, kNT, (size_t)(h->m + 1) * sizeof(double));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, k_correct<ST, CT>, kNT, (size_t)3 * (h->m + 1) * sizeof(double));
     h->grid_corr = h->nsm * std::max(1, std::min(occ4, 8));
     h->grid_stream = h->nsm * 4;
+    stepw_grids<ST, CT, 1>(h);
     CUDA_TRY(cudaFuncSetAttribute(k_step_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_correct_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     {
         const char *e = std::getenv("TOPK_NO_TMA");
         h->use_tma = !(e && e[0] == '1');
-        h->use_gram = h->use_tma && h->reorth != -1 && h->m <= kTmaCols;
+        // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed
+        h->use_gram = h->reorth != -1;
         const char *e2 = std::getenv("TOPK_TMA_CORRECT");
         h->tma_correct = e2 && e2[0] == '1';
+        const char *e3 = std::getenv("TOPK_TMA_STEP");
+        h->tma_step = e3 && e3[0] == '1';
     }
     int occ3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);
