@@ -229,9 +229,13 @@ def main():
     ap.add_argument("--no-ttk", action="store_true", help="skip the time-to-Top-K m sweep")
     ap.add_argument("--sweep", action="store_true",
                     help="C5 precision sweep on the C3 matrix (report lines, not the bench line)")
+    ap.add_argument("--quality", action="store_true",
+                    help="Fig. 3b analogue: eigenvector orthogonality and L2 error vs K, reorth on/off")
     args = ap.parse_args()
     if args.sweep:
         return run_sweep(args)
+    if args.quality:
+        return run_quality(args)
     wl = dict(WORKLOADS[args.workload], name=args.workload)
     if args.warmup < 3:
         args.warmup = 3
@@ -483,6 +487,55 @@ def run_sweep(args):
                               "ritz_normwise_err_vs_DDD": errn, "topK_err_vs_DDD": top,
                               "residual_est_max_rel": float(np.nanmax(r.residual_est) / abs(r.eigenvalues[0])),
                               "report_only": vs == "bf16" and st == "bf16"}), flush=True)
+    return 0
+
+
+def eigen_quality(A, Y, theta):
+    """Fig. 3b metrics of K returned eigenpairs against the fp64
+    matrix: the mean angle between every pair of eigenvectors (arccos |y_j . y_k|,
+    90 degrees for exact ones) and the mean L2 reconstruction error ||M y - lambda y||
+    (y unit norm, unnormalised by ||M||, as the paper plots it)."""
+    import scipy.sparse as sp
+    M = sp.csr_matrix((A.val, A.col, A.rowptr), shape=(A.n, A.n))
+    Y = np.asarray(Y, np.float64)
+    Y = Y / np.linalg.norm(Y, axis=1, keepdims=True)
+    G = np.abs(Y @ Y.T)
+    iu = np.triu_indices(len(Y), 1)
+    ang = np.degrees(np.arccos(np.clip(G[iu], 0.0, 1.0)))
+    R = (M @ Y.T).T - theta[:, None] * Y
+    res = np.linalg.norm(R, axis=1)
+    return {"mean_angle_deg": float(ang.mean()) if len(ang) else None,
+            "min_angle_deg": float(ang.min()) if len(ang) else None,
+            "max_abs_dot": float(G[iu].max()) if len(ang) else None,
+            "mean_l2_err": float(res.mean()), "max_l2_err": float(res.max()),
+            "residuals": res}
+
+
+def run_quality(args):
+    """NEXT-3: the paper's Fig. 3b on the C3 matrix -- for K = 8, 16, 24
+    at m = K, reorthogonalisation on (CGS) and off, in DDD, FDF and
+    FFF: mean pairwise eigenvector angle and mean ||M y - lambda y||; plus how well the
+    device residual estimate |beta_{m+1} s_{m,k}| tracks the measured residual. One JSON
+    line per (arm, reorth, K); report lines, not the bench line."""
+    import torch
+    import paper_2201_07498_b200 as T
+    torch.cuda.set_device(0)
+    A = make_matrix("C3")
+    arms = [a for a in SWEEP_ARMS if a[0] in ("DDD", "FDF", "FFF")]
+    for name, st, ct, vs in arms:
+        for reorth in (1, -1):
+            for K in (8, 16, 24):
+                with T.TopkEig(A, K, storage=st, compute=ct, values_storage=vs, m=K, reorth=reorth,
+                               check_symmetry=False) as h:
+                    r = h.solve(seed=1, vectors=True, vec_dtype="f64")
+                kf = len(r.eigenvectors)
+                q = eigen_quality(A, r.eigenvectors, r.eigenvalues[:kf])
+                est = np.asarray(r.residual_est[:kf])
+                res = q.pop("residuals")
+                gap = float(np.max(np.abs(est - res)) / abs(r.eigenvalues[0]))
+                print(json.dumps({"kind": "quality", "workload": "C3", "arm": name,
+                                  "reorth": "cgs" if reorth == 1 else "off", "K": K, "m": K, "k_found": kf,
+                                  **q, "residual_est_vs_measured_max_rel": gap}), flush=True)
     return 0
 
 

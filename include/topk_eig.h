@@ -91,6 +91,14 @@ typedef struct {
     const void *nccl_id;     /* host, 128-byte ncclUniqueId from topk_eig_nccl_id() on rank 0     */
     int32_t profile;         /* 1 -> bracket every kernel of part 0 with CUDA events (recorded inside
                                 the graph) so topk_eig_kernel_times() can report per-class device time */
+    /* convergence-driven Krylov dimension (reading Q25; not in the
+     * paper, which runs a fixed count, Alg.1 l.3): with conv_tol > 0, after iterations
+     * i = c, 2c, ... (K <= i < krylov_dim) a Jacobi solve of T_i runs on the device and the
+     * iteration stops at the first i where all K selected Ritz pairs have residual estimate
+     * |beta_{i+1} s_{i,k}| <= conv_tol |theta_1|; krylov_dim becomes the cap. No host round trip:
+     * the remaining launches of the graph see the stop flag and return at once. */
+    double conv_tol;         /* 0 -> off (fixed krylov_dim iterations)                             */
+    int32_t conv_check;      /* check period c; 0 -> K                                             */
 } topk_eig_opts_t;
 
 typedef struct {
@@ -104,6 +112,8 @@ typedef struct {
     double ms_solve;          /* device time of the whole solve (CUDA events)                       */
     int64_t bytes_model;      /* algorithmic HBM bytes of the solve on this part        */
     int64_t gpu_launches;     /* kernels launched by the solve (this part)                          */
+    int32_t converged_stop;   /* 1 if conv_tol stopped the iteration at m' < krylov_dim             */
+    int32_t conv_checks;      /* convergence checks enqueued per solve                             */
 } topk_eig_info_t;
 
 /* Create a solver for M, K eigenpairs, storage/compute precision pair.

@@ -285,3 +285,42 @@ def solve(rowptr, col, val, K: int, m: int | None = None, seed: int = 1, v1vec=N
     mm = lz.m_found
     rest = np.abs(lz.beta[mm] * S[mm - 1, idx]) if mm > 0 else np.zeros(0)
     return SolveOut(evals, Y, theta, S, idx, lz, sw, conv, rest)
+
+
+def solve_adaptive(rowptr, col, val, K: int, m_max: int, tol: float, check: int | None = None,
+                   seed: int = 1, v1vec=None, reorth: int = 1, tau: float = 1e-12,
+                   want_vectors: bool = True) -> SolveOut:
+    """Convergence-driven Krylov dimension (reading Q25).
+    The paper runs a fixed number of iterations (Alg.1 l.3); this mode stops at the
+    first check point i = c, 2c, ... (c = check or K) with K <= i < m_max and
+    i <= m' (the iterations completed) where the K selected Ritz pairs of T_i all
+    have residual estimate |beta_{i+1} s_{i,k}| <= tol |theta_1| (O10, reading Q6),
+    and returns the solve at m = i. The first i Lanczos steps do not depend on how
+    many follow, so the run to m_max is truncated at i (plain definition)."""
+    n = len(rowptr) - 1
+    if v1vec is None:
+        v1vec = v1(seed, n)
+    lz = lanczos(rowptr, col, val, v1vec, m_max, reorth, tau, keep_V=want_vectors)
+    c = check or K
+    stop = None
+    i = c
+    while i < m_max and i <= lz.m_found:
+        if i >= K:
+            theta, S, _, _ = jacobi(tridiag_dense(lz.alpha[:i], lz.beta[:i + 1]))
+            idx = select(theta, K)
+            res = np.abs(lz.beta[i] * S[i - 1, idx])
+            if len(idx) == K and bool(np.all(res <= tol * abs(theta[idx[0]]))):
+                stop = i
+                break
+        i += c
+    if stop is not None:
+        lz = LanczosOut(lz.alpha[:stop].copy(), lz.beta[:stop + 1].copy(),
+                        None if lz.V is None else lz.V[:stop].copy(), stop, False)
+    T = tridiag_dense(lz.alpha, lz.beta)
+    theta, S, sw, conv = jacobi(T)
+    idx = select(theta, K)
+    Y = ritz(lz.V, S, idx) if want_vectors else None
+    mm = lz.m_found
+    rest = np.abs(lz.beta[mm] * S[mm - 1, idx]) if mm > 0 else np.zeros(0)
+    return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, rest,
+                    extra={"converged_stop": stop is not None})

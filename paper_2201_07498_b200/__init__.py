@@ -48,7 +48,8 @@ class _Opts(ctypes.Structure):
                 ("values_storage", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("breakdown_tol", ctypes.c_double), ("rank", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("profile", ctypes.c_int32)]
+                ("profile", ctypes.c_int32), ("conv_tol", ctypes.c_double),
+                ("conv_check", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -56,7 +57,8 @@ class Info(ctypes.Structure):
                 ("breakdown", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
                 ("jacobi_converged", ctypes.c_int32), ("num_parts", ctypes.c_int32),
                 ("beta_next", ctypes.c_double), ("ms_solve", ctypes.c_double),
-                ("bytes_model", ctypes.c_int64), ("gpu_launches", ctypes.c_int64)]
+                ("bytes_model", ctypes.c_int64), ("gpu_launches", ctypes.c_int64),
+                ("converged_stop", ctypes.c_int32), ("conv_checks", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -181,7 +183,8 @@ class TopkEig:
                  reorth: int = 1, parts: int = 1, device: int = 0, check_symmetry: bool = True,
                  values_storage: str | None = None, use_graph: bool = True,
                  breakdown_tol: float = 0.0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, profile: bool = False):
+                 nccl_id: bytes | None = None, profile: bool = False,
+                 conv_tol: float = 0.0, conv_check: int = 0):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -199,6 +202,8 @@ class TopkEig:
         o.breakdown_tol = float(breakdown_tol)
         o.rank, o.world = int(rank), int(world)
         o.profile = 1 if profile else 0
+        o.conv_tol = float(conv_tol)
+        o.conv_check = int(conv_check)
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -26,6 +26,7 @@ namespace topk {
 
 constexpr int kNT = 256;  // threads per block for the streaming kernels
 constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no shared memory)
+constexpr int kSpmvMinBlocks = 1;  // (256, 4) forces <= 64 registers: spills, measured 12% slower (r01s)
 constexpr int kRitzKB = 8;  // Ritz outputs per thread
 constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
 constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
@@ -202,7 +203,7 @@ __device__ __forceinline__ int ld_col_stream(const int32_t *p) {
 }
 
 template <typename VT, typename ST, typename CT>
-__global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
+__global__ void __launch_bounds__(kSpmvNT, kSpmvMinBlocks) k_spmv(SpmvArgs a, int it) {
     __shared__ CT red[kSpmvNT / 32];
     __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
@@ -989,6 +990,11 @@ struct JacArgs {
     double *work;  // global workspace when T, S do not fit in shared memory
     int ld_log2;   // LD = 1 << ld_log2 >= m + (m & 1)
     int hl_log2;   // 1 << hl_log2 >= (m + (m & 1)) / 2
+    // convergence check (reading Q25): 0 -> the final solve of T_m'; > 0 -> a check
+    // on T_i (i = m_found): if the K selected pairs all have residual estimate
+    // <= conv_tol |theta_1|, set *done = 2 (every later kernel returns at once)
+    int check;
+    double conv_tol;
 };
 
 __device__ __forceinline__ int rr_player(int pos, int round, int M) {
@@ -1005,6 +1011,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
     __shared__ double s_fro;
     const int tid = threadIdx.x, nt = blockDim.x;
     const LzState &st = a.st;
+    if (a.check && *(volatile int *)st.done) return;  // stopped or broke down already
     const int mm = *st.m_found;
     if (tid == 0 && !*st.done) {
         double sq = 0.0;
@@ -1166,6 +1173,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
             st.evals[rank] = tc;
             for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[(j << LS) + c] * st.scale[j];
             st.resid[rank] = fabs(st.beta[mm] * S[((mm - 1) << LS) + c]);
+            if (a.check) continue;  // norms are the final solve's business
             if (st.use_gram) {  // ||y_k||^2 = c^T G c with c_j = S[j,c] s_j (the sign cancels)
                 double nrm = 0.0;
                 for (int j = 0; j < mm; ++j) {
@@ -1177,6 +1185,16 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
                 st.rnrm2[rank] = nrm;
             }
         }
+    }
+    if (a.check) {
+        __syncthreads();
+        if (tid == 0 && kf == K) {
+            const double lim = a.conv_tol * fabs(st.evals[0]);
+            int ok = 1;
+            for (int k = 0; k < K; ++k) ok &= (st.resid[k] <= lim);
+            if (ok) *st.done = 2;
+        }
+        return;
     }
     for (int k = kf + tid; k < K; k += nt) {
         st.evals[k] = __longlong_as_double(0x7ff8000000000000ll);
@@ -1319,7 +1337,9 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
             }
         }
     }
-    if (pass == 1) return;
+    if constexpr (pass == 1) {
+        return;
+    } else {
 #pragma unroll
     for (int q = 0; q < KB; ++q) {
         const CT rr = warp_sum(nrm[q]);
@@ -1342,6 +1362,7 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
         }
         __syncthreads();
         if (tid == 0) a.counter[grp] = 0u;
+    }
     }
 }
 

@@ -116,6 +116,9 @@ struct topk_eig_s {
     topk_dtype_t vs = TOPK_F64, ms = TOPK_F64, cs = TOPK_F64;
     int reorth = 1;
     double tau = 1e-12;
+    double conv_tol = 0.0;   // reading Q25 (0: fixed m)
+    int conv_check = 0;      // check period c
+    int conv_checks = 0;     // checks enqueued per solve
     int use_graph = 1;
     int nsm = 148;
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
@@ -185,6 +188,24 @@ static void prof_end(topk_eig_s *h, const Part &p) {
 
 // ---------------------------------------------------------------------------
 // exchanges (no-ops in loopback: shared buffers on one stream)
+static void launch_jacobi(topk_eig_s *h, int check) {
+    for (Part &p : h->parts) {
+        JacArgs a;
+        a.st = p.st; a.ex = h->ex; a.G = h->G; a.m = h->m; a.K = h->K; a.max_sweeps = 50;
+        a.work = h->jac_work ? h->jac_work + (size_t)(&p - &h->parts[0]) * (h->jac_bytes / 8) : nullptr;
+        a.ld_log2 = h->jac_ld_log2;
+        a.hl_log2 = h->jac_hl_log2;
+        a.check = check;
+        a.conv_tol = h->conv_tol;
+        prof_begin(h, p, 4);
+        if (h->jac_work) k_jacobi<false><<<1, h->jac_threads, 0, h->stream>>>(a);
+        else k_jacobi<true><<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+}
+
 static void exch_vec_norm(topk_eig_s *h) {
     if (!h->comm) return;
     Part &p = h->parts[0];
@@ -355,21 +376,12 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it);
         }
         exch_vec_norm(h);
+        if (h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0) {
+            launch_jacobi(h, 1);  // reading Q25: may set done = 2 (later launches return at once)
+        }
     }
     // a12-a13: Jacobi (redundant on every part, identical inputs)
-    for (Part &p : h->parts) {
-        JacArgs a;
-        a.st = p.st; a.ex = h->ex; a.G = h->G; a.m = h->m; a.K = h->K; a.max_sweeps = 50;
-        a.work = h->jac_work ? h->jac_work + (size_t)(&p - &h->parts[0]) * (h->jac_bytes / 8) : nullptr;
-        a.ld_log2 = h->jac_ld_log2;
-        a.hl_log2 = h->jac_hl_log2;
-        prof_begin(h, p, 4);
-        if (h->jac_work) k_jacobi<false><<<1, h->jac_threads, 0, h->stream>>>(a);
-        else k_jacobi<true><<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
-        CUDA_TRY(cudaGetLastError());
-        prof_end(h, p);
-        h->launches++;
-    }
+    launch_jacobi(h, 0);
     if (!want_vectors) return;
     // a14: Ritz projection + normalisation, two streaming passes (norms, output)
     for (int pass = h->use_gram ? 1 : 0; pass < 2; ++pass) {
@@ -569,6 +581,11 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (h->reorth != 1 && h->reorth != 2 && h->reorth != -1) return fail(TOPK_E_INVALID, "reorth must be 1, 2 or -1");
     h->tau = o.breakdown_tol > 0 ? o.breakdown_tol : (storage == TOPK_F64 ? 1e-12 : storage == TOPK_F32 ? 1e-6 : 1e-3);
     if (compute == TOPK_F32 && storage == TOPK_F64) return fail(TOPK_E_INVALID, "compute must be at least as precise as storage");
+    if (!(o.conv_tol >= 0.0) || o.conv_check < 0) return fail(TOPK_E_INVALID, "conv_tol must be >= 0 and conv_check >= 0");
+    h->conv_tol = o.conv_tol;
+    h->conv_check = o.conv_check > 0 ? o.conv_check : K;
+    if (h->conv_tol > 0.0)
+        for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
     h->use_graph = o.use_graph >= 0;
     h->profile = o.profile > 0;
     h->device = o.device;
@@ -783,7 +800,10 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     std::memset(info, 0, sizeof(*info));
     info->iterations = hget<int>(p, p.st.m_found);
     info->k_found = hget<int>(p, p.st.k_found);
-    info->breakdown = hget<int>(p, p.st.done);
+    const int done = hget<int>(p, p.st.done);
+    info->breakdown = done == 1;
+    info->converged_stop = done == 2;
+    info->conv_checks = h->conv_checks;
     info->jacobi_sweeps = hget<int>(p, p.st.jac_sweeps);
     info->jacobi_converged = hget<int>(p, p.st.jac_conv);
     info->num_parts = h->G;

@@ -1,0 +1,78 @@
+"""Convergence-driven Krylov dimension (reading Q25)
+through the C ABI against oracle.solve_adaptive: the device Jacobi check every c
+iterations must stop at the same iteration as the oracle (DDD; FDF may differ only
+at a check point whose residual ratio is within rounding of conv_tol), and the
+result equals the fixed-m solve at that m."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synthgen as S
+from test_gpu_parity import TOL, check_solve
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_2201_07498_b200 as T
+    return T
+
+
+@pytest.fixture(scope="module")
+def c3s():
+    return S.config_matrix("C3S")
+
+
+def _ratio(A, K, i, seed, tau):
+    r = O.solve(A.rowptr, A.col, A.val, K, m=i, seed=seed, tau=tau, want_vectors=False)
+    return float(np.max(r.residual_est) / abs(r.eigenvalues[0]))
+
+
+@pytest.mark.parametrize("storage,tol", [("f64", 1e-4), ("f64", 1e-7), ("f32", 1e-4)])
+def test_adaptive_stop_matches_oracle(T, c3s, storage, tol):
+    K, c, mmax, seed = 8, 8, 240, 2
+    tau = O.TAU[storage]
+    ref = O.solve_adaptive(c3s.rowptr, c3s.col, c3s.val, K, mmax, tol, check=c, seed=seed, tau=tau)
+    assert ref.extra["converged_stop"]
+    with T.TopkEig(c3s, K, storage=storage, compute="f64", m=mmax, conv_tol=tol, conv_check=c) as h:
+        res = h.solve(seed=seed, vectors=True)
+    it = res.info["iterations"]
+    assert res.info["conv_checks"] == sum(1 for i in range(K, mmax) if i % c == 0)
+    assert res.info["converged_stop"] == 1 and res.info["breakdown"] == 0
+    assert it % c == 0
+    if it != ref.lanczos.m_found:
+        # only a borderline decision may differ: the earlier of the two stop
+        # points has its residual ratio within rounding of tol
+        lo = min(it, ref.lanczos.m_found)
+        assert storage != "f64" and abs(_ratio(c3s, K, lo, seed, tau) / tol - 1) < 1e-3, (it, ref.lanczos.m_found)
+        ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K, m=it, seed=seed, tau=tau)
+    assert np.all(res.residual_est <= tol * abs(res.eigenvalues[0]) * (1 + 1e-12))
+    check_solve(res, ref, TOL[storage])
+
+
+def test_adaptive_unmet_tol_equals_fixed_m(T, c3s):
+    """A tolerance nothing meets runs all m iterations (checks included) and gives
+    bit-identical eigenvalues to the fixed-m solve (the checks only read state)."""
+    K, m = 8, 48
+    with T.TopkEig(c3s, K, "f32", "f64", m=m, conv_tol=1e-300, conv_check=8) as h:
+        a = h.solve(seed=4, vectors=False)
+    with T.TopkEig(c3s, K, "f32", "f64", m=m) as h:
+        b = h.solve(seed=4, vectors=False)
+    assert a.info["iterations"] == m and a.info["converged_stop"] == 0
+    assert a.info["conv_checks"] == 5  # i = 8, 16, 24, 32, 40
+    assert np.array_equal(a.eigenvalues, b.eigenvalues)
+    assert np.array_equal(a.residual_est, b.residual_est)
+
+
+def test_adaptive_loopback_parts_agree(T, c3s):
+    """G = 3 virtual ranks take the same stop decision as G = 1 (identical T on
+    every rank, reading Q25)."""
+    K, tol = 8, 1e-6
+    out = []
+    for G in (1, 3):
+        with T.TopkEig(c3s, K, "f64", "f64", m=200, parts=G, conv_tol=tol) as h:
+            out.append(h.solve(seed=6, vectors=False))
+    assert out[0].info["iterations"] == out[1].info["iterations"]
+    assert out[0].info["converged_stop"] == out[1].info["converged_stop"] == 1
+    assert np.max(np.abs(out[0].eigenvalues - out[1].eigenvalues)) <= 1e-10 * abs(out[0].eigenvalues[0])

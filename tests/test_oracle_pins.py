@@ -410,3 +410,33 @@ def test_p8_converged_pairs_match_arpack():
     conv = r.residual_est <= 1e-10 * nrm
     assert conv.sum() >= 4
     assert np.allclose(r.eigenvalues[conv], ref[conv], rtol=1e-10, atol=0)
+
+
+# ---------------------------------------------------------------- P11 (adaptive stop)
+def test_p11_adaptive_stop_kahan_and_minimal():
+    """solve_adaptive (reading Q25): every returned pair satisfies the Kahan bound
+    against dense eigenvalues (brute force), its explicit residual ||Ay - theta y||
+    is within tol |theta_1|, and the previous check point had not converged
+    (computed through plain solve at that m, not through the adaptive loop)."""
+    A = S.rmat(11, 12_000, 5)
+    n, K, tol, c = A.n, 6, 1e-7, 6
+    lam = np.linalg.eigvalsh(dense(n, A.rowptr, A.col, A.val))
+    r = O.solve_adaptive(A.rowptr, A.col, A.val, K, m_max=300, tol=tol, check=c, seed=2)
+    assert r.extra["converged_stop"]
+    i = r.lanczos.m_found
+    assert i % c == 0 and K <= i < 300
+    M = sp.csr_matrix((A.val, A.col, A.rowptr), shape=(n, n))
+    t1 = abs(r.eigenvalues[0])
+    for k in range(K):
+        y = r.eigenvectors[k]
+        true = np.linalg.norm(M @ y - r.eigenvalues[k] * y)
+        assert true <= tol * t1 * (1 + 1e-6) + 1e-12 * t1
+        assert np.min(np.abs(lam - r.eigenvalues[k])) <= true + 1e-12 * t1
+    assert abs(t1 - np.abs(lam).max()) <= 1e-10 * t1
+    if i - c >= K:
+        prev = O.solve(A.rowptr, A.col, A.val, K, m=i - c, seed=2, want_vectors=False)
+        assert np.any(prev.residual_est > tol * abs(prev.eigenvalues[0]))
+    # a tolerance nothing meets runs to m_max
+    r2 = O.solve_adaptive(A.rowptr, A.col, A.val, K, m_max=24, tol=1e-300, check=c, seed=2,
+                          want_vectors=False)
+    assert r2.lanczos.m_found == 24 and not r2.extra["converged_stop"]

@@ -32,3 +32,4 @@ if has launches || has full; then
     fi
   fi
 fi
+exit 0

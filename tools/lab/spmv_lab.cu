@@ -16,12 +16,24 @@ template <class T> std::vector<T> rd(const std::string &f) {
 // 2: predicated ld.shared (hot, smem index = c & mask) / ld.global no_allocate (cold);
 // 3: predicated ld.shared (hot) / plain ldg (cold). Hot flag = bit 31 of c. x index = c & mask
 // for P 0,1 (hot region = x prefix), smem index for P 2,3 (same value here: G = 1).
+__constant__ int c_H;
 template <int P>
 __device__ __forceinline__ float gat(const float *x, const float *hot, int c) {
     float v;
     const unsigned idx = (unsigned)c & 0x7fffffffu;
     if (P == 0) return __ldg(x + idx);
     if (P == 8) return (float)(idx & 7);   // no gather at all (stream-only bound)
+    if (P == 10) {  // position-based hybrid, predicated (no branch: both loads issue in the batch)
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(hot) + 4u * idx;
+        asm volatile("{.reg .pred p; setp.lt.u32 p, %1, %2;\n\t"
+                     "@p ld.shared.f32 %0, [%3];\n\t"
+                     "@!p ld.global.nc.f32 %0, [%4];}"
+                     : "=f"(v) : "r"(idx), "r"(c_H), "r"(sa), "l"(x + idx));
+        return v;
+    }
+    if (P == 9) {  // position-based hybrid: hub prefix [0, H) from shared memory, the rest plain ldg
+        return idx < (unsigned)c_H ? hot[idx] : __ldg(x + idx);
+    }
     if (P == 6) return hot[idx % 51200u];  // all gathers from shared memory (throughput probe)
     if (P == 7) return hot[idx & 16383u];  // all gathers from a 64 KB smem window
     if (P == 4) {  // position-based: hub prefix [0, 65536) evict_last, the rest evict_first
@@ -62,11 +74,11 @@ __device__ __forceinline__ int ldc(const int *p) { int v; asm volatile("ld.globa
 __device__ __forceinline__ float ldv(const float *p) { float v; asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v; }
 
 // SELL items. P = gather policy (see gat); STREAM: 1 = no gathers (stream-only bound)
-template <int P, int NT, int STREAM = 0>
-__global__ void __launch_bounds__(NT) k(const int *col, const float *val, const int2 *sell, const int2 *items, int nitems,
+template <int P, int NT, int STREAM = 0, int MB = 1>
+__global__ void __launch_bounds__(NT, MB) k(const int *col, const float *val, const int2 *sell, const int2 *items, int nitems,
                                         int nbig, int nne, const float *x, int H, double *y) {
     extern __shared__ float hot[];
-    if (P == 2 || P == 3 || P == 6 || P == 7) {
+    if (P == 2 || P == 3 || P == 6 || P == 7 || P == 9 || P == 10) {
         const int HH = (P == 7) ? 16384 : H;
         for (int i = threadIdx.x; i < HH; i += NT) hot[i] = x[i];
         __syncthreads();
@@ -111,11 +123,11 @@ __global__ void __launch_bounds__(NT) k(const int *col, const float *val, const 
 // big-row chunks (rows of degree > 128, 72% of C3's nnz): warp per chunk
 // V 0: scalar lanes k = zb + lane + 32t (product structure), 8 in flight
 // V 1: 16-byte vectors: lane covers 4 consecutive nnz, aligned groups, masked ends
-template <int V, int NT, int P = 0, int GQ = 8>
-__global__ void __launch_bounds__(NT) kc(const int *col, const float *val, const int4 *chunks, int nch,
+template <int V, int NT, int P = 0, int GQ = 8, int MB = 1>
+__global__ void __launch_bounds__(NT, MB) kc(const int *col, const float *val, const int4 *chunks, int nch,
                                          const float *x, double *y, int H) {
     extern __shared__ float hot[];
-    if (P == 2 || P == 3 || P == 6 || P == 7) {
+    if (P == 2 || P == 3 || P == 6 || P == 7 || P == 9 || P == 10) {
         const int HH = (P == 7) ? 16384 : H;
         for (int i = threadIdx.x; i < HH; i += NT) hot[i] = x[i];
         __syncthreads();
@@ -182,20 +194,33 @@ int main(int argc, char **argv) {
     long long sellnnz = (long long)pcol.size() - 0;
     printf("nbig %d nne %d n %d H %d nitems %d phys %zu\n", nbig, nne, n, H, nitems, pcol.size());
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    int Hs = H;
+    auto setH = [&](int h) { Hs = h; cudaMemcpyToSymbol(c_H, &h, 4); };
+    auto attr = [&](auto kern) { cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, kern); return fa.numRegs; };
     auto run = [&](const char *name, auto kern, int nt, int bpsm, size_t smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nsm * bpsm, nt, smem>>>(dcol, dval, dsell, ditems, nitems, nbig, nne, dx, H, dy);
+        kern<<<nsm * bpsm, nt, smem>>>(dcol, dval, dsell, ditems, nitems, nbig, nne, dx, Hs, dy);
         cudaDeviceSynchronize();
         cudaEventRecord(a);
-        for (int r = 0; r < 10; ++r) kern<<<nsm * bpsm, nt, smem>>>(dcol, dval, dsell, ditems, nitems, nbig, nne, dx, H, dy);
+        for (int r = 0; r < 10; ++r) kern<<<nsm * bpsm, nt, smem>>>(dcol, dval, dsell, ditems, nitems, nbig, nne, dx, Hs, dy);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); ms /= 10;
-        printf("%-40s %8.3f us   (%s)\n", name, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
+        printf("%-40s H %6d regs %3d %8.3f us   (%s)\n", name, Hs, attr(kern), ms * 1e3, cudaGetErrorString(cudaGetLastError()));
     };
-    run("SELL P0 ldg 256x8", k<0, 256>, 256, 8, 0);
+    setH(H);
+    run("SELL P0 ldg 256x3", k<0, 256>, 256, 3, 0);
+    run("SELL P0 ldg 256x4 mb4", k<0, 256, 0, 4>, 256, 4, 0);
+    run("SELL P0 ldg 256x5 mb5", k<0, 256, 0, 5>, 256, 5, 0);
+    run("SELL P0 ldg 256x6 mb6", k<0, 256, 0, 6>, 256, 6, 0);
     run("SELL P6 all-smem 1024x1", k<6, 1024>, 1024, 1, (size_t)H * 4);
-    run("SELL P2 smem/no_alloc 1024x1", k<2, 1024>, 1024, 1, (size_t)H * 4);
-    run("SELL P0 ldg 1024x1", k<0, 1024>, 1024, 1, 0);
+    setH(51200); run("SELL P10 pred-hybrid 768x1", k<10, 768>, 768, 1, 51200 * 4);
+    setH(51200); run("SELL P10 pred-hybrid 1024x1", k<10, 1024>, 1024, 1, 51200 * 4);
+    setH(27648); run("SELL P10 pred-hybrid 384x2", k<10, 384, 0, 2>, 384, 2, 27648 * 4);
+    setH(27648); run("SELL P10 pred-hybrid 512x2", k<10, 512, 0, 2>, 512, 2, 27648 * 4);
+    setH(18432); run("SELL P10 pred-hybrid 256x3", k<10, 256, 0, 3>, 256, 3, 18432 * 4);
+    setH(13824); run("SELL P10 pred-hybrid 256x4", k<10, 256, 0, 4>, 256, 4, 13824 * 4);
+    setH(8192); run("SELL P10 pred-hybrid 256x4 H8k", k<10, 256, 0, 4>, 256, 4, 8192 * 4);
+    setH(H);
     auto bcol = rd<int>(d + "/bcol.bin"); auto bval = rd<float>(d + "/bval.bin"); auto ch = rd<int>(d + "/chunks.bin");
     int *dbc; float *dbv; int4 *dch;
     CK(cudaMalloc(&dbc, bcol.size() * 4 + 4096)); CK(cudaMalloc(&dbv, bval.size() * 4 + 4096)); CK(cudaMalloc(&dch, ch.size() * 4));
@@ -206,20 +231,26 @@ int main(int argc, char **argv) {
     printf("big rows: nnz %zu chunks %d\n", bcol.size(), nch);
     auto runc = [&](const char *name, auto kern, int nt, int bpsm, size_t smem = 0) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nsm * bpsm, nt, smem>>>(dbc, dbv, dch, nch, dx, dy, H);
+        kern<<<nsm * bpsm, nt, smem>>>(dbc, dbv, dch, nch, dx, dy, Hs);
         cudaDeviceSynchronize();
         cudaEventRecord(a);
-        for (int r = 0; r < 10; ++r) kern<<<nsm * bpsm, nt, smem>>>(dbc, dbv, dch, nch, dx, dy, H);
+        for (int r = 0; r < 10; ++r) kern<<<nsm * bpsm, nt, smem>>>(dbc, dbv, dch, nch, dx, dy, Hs);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); ms /= 10;
-        printf("%-40s %8.3f us  %.0f GB/s algorithmic (%s)\n", name, ms * 1e3, bcol.size() * 8.0 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+        printf("%-40s H %6d regs %3d %8.3f us  %.0f GB/s algorithmic (%s)\n", name, Hs, attr(kern), ms * 1e3, bcol.size() * 8.0 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
-    runc("chunks scalar P0 256x8", kc<0, 256, 0>, 256, 8);
-    runc("chunks scalar P8 stream-only 256x8", kc<0, 256, 8>, 256, 8);
-    runc("chunks scalar P8 stream-only GQ16 256x8", kc<0, 256, 8, 16>, 256, 8);
-    runc("chunks scalar P0 GQ16 256x8", kc<0, 256, 0, 16>, 256, 8);
-    runc("chunks scalar P0 GQ4 256x8", kc<0, 256, 0, 4>, 256, 8);
-    runc("chunks vec4 P8 stream-only 256x8", kc<1, 256, 8>, 256, 8);
-    runc("chunks vec4 P6 all-smem 1024x1", kc<1, 1024, 6>, 1024, 1, (size_t)H * 4);
+    runc("chunks scalar P0 256x3", kc<0, 256, 0>, 256, 3);
+    runc("chunks scalar P0 256x4 mb4", kc<0, 256, 0, 8, 4>, 256, 4);
+    runc("chunks scalar P8 stream-only 256x3", kc<0, 256, 8>, 256, 3);
+    setH(51200); runc("chunks P10 pred-hybrid 768x1", kc<0, 768, 10>, 768, 1, 51200 * 4);
+    setH(51200); runc("chunks P10 pred-hybrid 1024x1", kc<0, 1024, 10>, 1024, 1, 51200 * 4);
+    setH(27648); runc("chunks P10 pred-hybrid 384x2", kc<0, 384, 10, 8, 2>, 384, 2, 27648 * 4);
+    setH(27648); runc("chunks P10 pred-hybrid 512x2", kc<0, 512, 10, 8, 2>, 512, 2, 27648 * 4);
+    setH(18432); runc("chunks P10 pred-hybrid 256x3", kc<0, 256, 10, 8, 3>, 256, 3, 18432 * 4);
+    setH(13824); runc("chunks P10 pred-hybrid 256x4", kc<0, 256, 10, 8, 4>, 256, 4, 13824 * 4);
+    setH(8192); runc("chunks P10 pred-hybrid 256x4 H8k", kc<0, 256, 10, 8, 4>, 256, 4, 8192 * 4);
+    runc("chunks scalar P0 256x5 mb5", kc<0, 256, 0, 8, 5>, 256, 5);
+    runc("chunks scalar P0 256x6 mb6", kc<0, 256, 0, 8, 6>, 256, 6);
+    setH(51200); runc("chunks scalar P6 all-smem 1024x1", kc<0, 1024, 6>, 1024, 1, 51200 * 4);
     return 0;
 }
