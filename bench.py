@@ -395,6 +395,24 @@ def time_to_topk(T, A, wl, kw, reps=5):
             r = h.solve(seed=1, vectors=False)
         conv = int(np.sum(r.residual_est <= 1e-5 * abs(r.eigenvalues[0])))
         out[f"m={m}"] = {"ms": round(ms, 3), "converged_of_K": conv}
+    # convergence-driven stop (reading Q25): m <= 8K, checked every c iterations
+    for c in (8, K):
+        with T.TopkEig(A, K, check_symmetry=False, conv_tol=1e-5, conv_check=c, **dict(kw, m=8 * K)) as h:
+            ev = torch.zeros(K, dtype=torch.float64, device="cuda")
+            h.solve_async(1, ev.data_ptr(), None)
+            h.sync()
+            stream = torch.cuda.ExternalStream(h.stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(reps):
+                h.solve_async(1, ev.data_ptr(), None)
+            e1.record(stream)
+            h.sync()
+            ms = e0.elapsed_time(e1) / reps
+            r = h.solve(seed=1, vectors=False)
+        conv = int(np.sum(r.residual_est <= 1e-5 * abs(r.eigenvalues[0])))
+        out[f"adaptive tol=1e-5 c={c}"] = {"ms": round(ms, 3), "iterations": r.info["iterations"],
+                                           "converged_of_K": conv, "stopped": bool(r.info["converged_stop"])}
     return out
 
 

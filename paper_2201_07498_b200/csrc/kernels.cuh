@@ -19,6 +19,8 @@
 // per-block slots summed in block order by the last-arriving block, and
 // cross-part sums in rank order (no floating-point atomics).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "device_common.cuh"
 #include "host_prep.h"
 
@@ -26,7 +28,6 @@ namespace topk {
 
 constexpr int kNT = 256;  // threads per block for the streaming kernels
 constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no shared memory)
-constexpr int kSpmvMinBlocks = 1;  // (256, 4) forces <= 64 registers: spills, measured 12% slower (r01s)
 constexpr int kRitzKB = 8;  // Ritz outputs per thread
 constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
 constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
@@ -203,7 +204,7 @@ __device__ __forceinline__ int ld_col_stream(const int32_t *p) {
 }
 
 template <typename VT, typename ST, typename CT>
-__global__ void __launch_bounds__(kSpmvNT, kSpmvMinBlocks) k_spmv(SpmvArgs a, int it) {
+__global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
     __shared__ CT red[kSpmvNT / 32];
     __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
@@ -997,11 +998,104 @@ struct JacArgs {
     double conv_tol;
 };
 
+// ||T||_F of the tridiagonal T_mm in the oracle's summation order (row-major);
+// only the nonzeros are added (adding the exact zeros leaves the sum unchanged).
+__device__ __forceinline__ double jac_fro(const LzState &st, int mm) {
+    double f = 0.0;
+    for (int r = 0; r < mm; ++r) {
+        if (r > 0) f += st.beta[r] * st.beta[r];
+        f += st.alpha[r] * st.alpha[r];
+        if (r + 1 < mm) f += st.beta[r + 1] * st.beta[r + 1];
+    }
+    return sqrt(f);
+}
+
+// One Jacobi rotation (reading Q10): skip negligible t_pq, else the stable
+// division-free (c, s) that zeroes it. Returns 1 if the rotation is applied.
+__device__ __forceinline__ int jac_rotation(double apq, double app, double aqq, double fro2, double &c,
+                                            double &sn) {
+    const double eps = 2.220446049250313e-16;
+    const double a2 = apq * apq;
+    c = 1.0;
+    sn = 0.0;
+    if (a2 <= eps * eps * fabs(app * aqq) || a2 <= fro2) return 0;
+    const double d = aqq - app;
+    const bool zpos = (d == 0.0) || ((d > 0.0) == (apq > 0.0));
+    const double x = d * d + 4.0 * a2;
+    const double D = fabs(d) + x * rsqrt(x);
+    const double ih = rsqrt(D * D + 4.0 * a2);
+    c = D * ih;
+    sn = (zpos ? 2.0 : -2.0) * fabs(apq) * ih;
+    return 1;
+}
+
 __device__ __forceinline__ int rr_player(int pos, int round, int M) {
     if (pos == 0) return 0;
     int x = pos - 1 + round;
     if (x >= M - 1) x -= M - 1;
     return 1 + x;
+}
+
+// a13 after the sweeps: selection by (-|theta|, -theta), sign, coefficients,
+// residual estimates, Ritz norms from the Gram matrix; in check mode (reading
+// Q25) the stop decision instead. T, S: row-major with leading dimension 1 << LS.
+__device__ void jac_finish(const JacArgs &a, const double *T, const double *S, int LS, int mm,
+                           int sweeps, int conv) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const LzState &st = a.st;
+    const int K = a.K;
+    const int kf = K < mm ? K : mm;
+    for (int c = tid; c < mm; c += nt) {
+        const double tc = T[(c << LS) + c];
+        st.theta_all[c] = tc;
+        int rank = 0;
+        for (int d = 0; d < mm; ++d) {
+            const double td = T[(d << LS) + d];
+            const bool before = (fabs(td) != fabs(tc)) ? (fabs(td) > fabs(tc))
+                                : (td != tc) ? (td > tc) : (d < c);
+            rank += before;
+        }
+        if (rank < kf) {
+            double sg = 1.0;
+            for (int j = 0; j < mm; ++j) {
+                const double sj = S[(j << LS) + c];
+                if (sj != 0.0) { sg = sj > 0.0 ? 1.0 : -1.0; break; }
+            }
+            st.evals[rank] = tc;
+            for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[(j << LS) + c] * st.scale[j];
+            st.resid[rank] = fabs(st.beta[mm] * S[((mm - 1) << LS) + c]);
+            if (a.check) continue;  // norms are the final solve's business
+            if (st.use_gram) {  // ||y_k||^2 = c^T G c with c_j = S[j,c] s_j (the sign cancels)
+                double nrm = 0.0;
+                for (int j = 0; j < mm; ++j) {
+                    const double cj = S[(j << LS) + c] * st.scale[j];
+                    double rowsum = 0.0;
+                    for (int l = 0; l < mm; ++l) rowsum += st.gram[(size_t)j * st.m + l] * (S[(l << LS) + c] * st.scale[l]);
+                    nrm += cj * rowsum;
+                }
+                st.rnrm2[rank] = nrm;
+            }
+        }
+    }
+    if (a.check) {
+        __syncthreads();
+        if (tid == 0 && kf == K) {
+            const double lim = a.conv_tol * fabs(st.evals[0]);
+            int ok = 1;
+            for (int k = 0; k < K; ++k) ok &= (st.resid[k] <= lim);
+            if (ok) *st.done = 2;
+        }
+        return;
+    }
+    for (int k = kf + tid; k < K; k += nt) {
+        st.evals[k] = __longlong_as_double(0x7ff8000000000000ll);
+        st.resid[k] = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    if (tid == 0) {
+        *st.k_found = kf;
+        *st.jac_sweeps = sweeps;
+        *st.jac_conv = conv;
+    }
 }
 
 template <bool kSmem>
@@ -1037,12 +1131,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
         S[i] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
-    if (tid == 0) {
-        double f = 0.0;  // ||T||_F in the oracle's summation order (row-major)
-        for (int r = 0; r < mm; ++r)
-            for (int c = 0; c < mm; ++c) f += T[(r << LS) + c] * T[(r << LS) + c];
-        s_fro = sqrt(f);
-    }
+    if (tid == 0) s_fro = jac_fro(st, mm);
     __syncthreads();
     const double eps = 2.220446049250313e-16;
     const double fro2 = (eps * eps * s_fro) * (eps * eps * s_fro);
@@ -1061,19 +1150,8 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
                 int doit = 0;
                 double c = 1.0, sn = 0.0;
                 if (q < mm) {
-                    const double apq = T[(p << LS) + q], app = T[(p << LS) + p], aqq = T[(q << LS) + q];
-                    const double a2 = apq * apq;
-                    if (!(a2 <= eps * eps * fabs(app * aqq) || a2 <= fro2)) {
-                        const double d = aqq - app;
-                        const bool zpos = (d == 0.0) || ((d > 0.0) == (apq > 0.0));
-                        const double x = d * d + 4.0 * a2;
-                        const double D = fabs(d) + x * rsqrt(x);
-                        const double ih = rsqrt(D * D + 4.0 * a2);
-                        c = D * ih;
-                        sn = (zpos ? 2.0 : -2.0) * fabs(apq) * ih;
-                        doit = 1;
-                        s_rot = 1;
-                    }
+                    doit = jac_rotation(T[(p << LS) + q], T[(p << LS) + p], T[(q << LS) + q], fro2, c, sn);
+                    if (doit) s_rot = 1;
                 }
                 cs[2 * k] = c;
                 cs[2 * k + 1] = sn;
@@ -1151,60 +1229,139 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
         conv = !s_rot;
         __syncthreads();
     }
-    // selection + sign + outputs
-    const int K = a.K;
-    const int kf = K < mm ? K : mm;
-    for (int c = tid; c < mm; c += nt) {
-        const double tc = T[(c << LS) + c];
-        st.theta_all[c] = tc;
-        int rank = 0;
-        for (int d = 0; d < mm; ++d) {
-            const double td = T[(d << LS) + d];
-            const bool before = (fabs(td) != fabs(tc)) ? (fabs(td) > fabs(tc))
-                                : (td != tc) ? (td > tc) : (d < c);
-            rank += before;
-        }
-        if (rank < kf) {
-            double sg = 1.0;
-            for (int j = 0; j < mm; ++j) {
-                const double sj = S[(j << LS) + c];
-                if (sj != 0.0) { sg = sj > 0.0 ? 1.0 : -1.0; break; }
-            }
-            st.evals[rank] = tc;
-            for (int j = 0; j < mm; ++j) st.coefS[(size_t)j * K + rank] = sg * S[(j << LS) + c] * st.scale[j];
-            st.resid[rank] = fabs(st.beta[mm] * S[((mm - 1) << LS) + c]);
-            if (a.check) continue;  // norms are the final solve's business
-            if (st.use_gram) {  // ||y_k||^2 = c^T G c with c_j = S[j,c] s_j (the sign cancels)
-                double nrm = 0.0;
-                for (int j = 0; j < mm; ++j) {
-                    const double cj = S[(j << LS) + c] * st.scale[j];
-                    double rowsum = 0.0;
-                    for (int l = 0; l < mm; ++l) rowsum += st.gram[(size_t)j * st.m + l] * (S[(l << LS) + c] * st.scale[l]);
-                    nrm += cj * rowsum;
-                }
-                st.rnrm2[rank] = nrm;
-            }
-        }
+    jac_finish(a, T, S, LS, mm, sweeps, conv);
+}
+
+// ---------------------------------------------------------------------------
+// a12 for large m (T and S of one part do not fit one SM's shared memory): the
+// same round-robin rounds and rotation formula as k_jacobi (reading Q10), on a
+// thread-block cluster. CTA b owns rows [bR, (b+1)R) of T (two buffers: the row
+// op of a round writes the other one) and of S, in its shared memory. Per round:
+//  (A) every CTA derives all M/2 rotations from t_pp, t_qq, t_pq (distributed
+//      shared memory reads; identical results in every CTA, so the stop test
+//      needs no exchange);
+//  (B) column op T <- T J and S <- S J on its own rows; cluster barrier;
+//  (C) row op T <- J^T T into the other buffer, the partner row read remotely;
+//      the rotated pair's (p, q) entries set to exact zero; cluster barrier.
+// Then T's diagonal and S go to the global workspace and CTA 0 finishes.
+constexpr int kJacClNT = 1024;
+
+__global__ void __launch_bounds__(kJacClNT, 1) k_jacobi_cl(JacArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double jsm[];
+    __shared__ int s_rot;
+    __shared__ double s_fro;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int br = (int)cl.block_rank(), CL = (int)cl.num_blocks();
+    const LzState &st = a.st;
+    if (a.check && *(volatile int *)st.done) return;  // same value in every CTA
+    const int mm = *st.m_found;
+    if (br == 0 && tid == 0 && !*st.done) {
+        double sq = 0.0;
+        for (int q = 0; q < a.G; ++q) sq += __ldcg(a.ex.norm_part + q);
+        st.beta[mm] = sqrt(sq);  // beta_{m'+1} (reading Q6)
     }
-    if (a.check) {
+    const int M = mm + (mm & 1), half = M / 2;
+    const int R = (M + CL - 1) / CL, LDc = M;
+    const int r0 = br * R;
+    const int nloc = (r0 >= M) ? 0 : ((M - r0) < R ? (M - r0) : R);
+    double *T0 = jsm, *T1 = T0 + (size_t)R * LDc, *Sl = T1 + (size_t)R * LDc;
+    double *cs = Sl + (size_t)R * LDc;                  // [half][2]
+    int *pq = reinterpret_cast<int *>(cs + 2 * half);  // [half][2]
+    int *rot = pq + 2 * half;                          // [half]
+    int *prow = rot + half;                            // [M]: 2 k + (row is the q of pair k)
+    for (int i = tid; i < nloc * LDc; i += nt) {
+        const int rl = i / LDc, c = i - rl * LDc, r = r0 + rl;
+        double t = 0.0;
+        if (r < mm && c < mm) {
+            if (r == c) t = st.alpha[r];
+            else if (r - c == 1 || c - r == 1) t = st.beta[r > c ? r : c];
+        }
+        T0[i] = t;
+        Sl[i] = (r == c) ? 1.0 : 0.0;
+    }
+    if (tid == 0) s_fro = jac_fro(st, mm);
+    __syncthreads();
+    const double eps = 2.220446049250313e-16;
+    const double fro2 = (eps * eps * s_fro) * (eps * eps * s_fro);
+    cl.sync();  // every CTA's rows are initialised before the first remote read
+    int sweeps = 0, conv = (M < 2) ? 1 : 0, cur = 0;
+    while (!conv && sweeps < a.max_sweeps) {
+        if (tid == 0) s_rot = 0;
         __syncthreads();
-        if (tid == 0 && kf == K) {
-            const double lim = a.conv_tol * fabs(st.evals[0]);
-            int ok = 1;
-            for (int k = 0; k < K; ++k) ok &= (st.resid[k] <= lim);
-            if (ok) *st.done = 2;
+        for (int round = 0; round < M - 1; ++round) {
+            double *Tc = cur ? T1 : T0, *Tn = cur ? T0 : T1;
+            // (A) rotations of this round
+            for (int k = tid; k < half; k += nt) {
+                int p = rr_player(k, round, M), q = rr_player(M - 1 - k, round, M);
+                if (p > q) { const int t = p; p = q; q = t; }
+                pq[2 * k] = p;
+                pq[2 * k + 1] = q;
+                prow[p] = 2 * k;
+                prow[q] = 2 * k + 1;
+                int doit = 0;
+                double c = 1.0, sn = 0.0;
+                if (q < mm) {
+                    const double *Rp = cl.map_shared_rank(Tc, p / R) + (size_t)(p % R) * LDc;
+                    const double *Rq = cl.map_shared_rank(Tc, q / R) + (size_t)(q % R) * LDc;
+                    doit = jac_rotation(Rp[q], Rp[p], Rq[q], fro2, c, sn);
+                    if (doit) s_rot = 1;
+                }
+                cs[2 * k] = c;
+                cs[2 * k + 1] = sn;
+                rot[k] = doit;
+            }
+            __syncthreads();
+            // (B) T <- T J, S <- S J on the own rows
+            for (int i = tid; i < nloc * half; i += nt) {
+                const int rl = i / half, k = i - rl * half;
+                if (!rot[k]) continue;
+                const int p = pq[2 * k], q = pq[2 * k + 1];
+                const double c = cs[2 * k], sn = cs[2 * k + 1];
+                double *tr = Tc + (size_t)rl * LDc, *sr = Sl + (size_t)rl * LDc;
+                const double tp = tr[p], tq = tr[q], sp = sr[p], sq = sr[q];
+                tr[p] = c * tp - sn * tq;
+                tr[q] = sn * tp + c * tq;
+                sr[p] = c * sp - sn * sq;
+                sr[q] = sn * sp + c * sq;
+            }
+            cl.sync();
+            // (C) T <- J^T T into the other buffer (batching several remote loads per
+            // thread measured slower: register-limited at 1024 threads)
+            for (int i = tid; i < nloc * M; i += nt) {
+                const int rl = i / M, col = i - rl * M, r = r0 + rl;
+                const int pk = prow[r], k = pk >> 1, isq = pk & 1;
+                double v = Tc[(size_t)rl * LDc + col];
+                if (rot[k]) {
+                    const int partner = pq[2 * k + (isq ^ 1)];
+                    const double w = cl.map_shared_rank(Tc, partner / R)[(size_t)(partner % R) * LDc + col];
+                    const double c = cs[2 * k], sn = cs[2 * k + 1];
+                    v = isq ? (sn * w + c * v) : (c * v - sn * w);
+                    if (col == partner) v = 0.0;  // the annihilated t_pq, t_qp
+                }
+                Tn[(size_t)rl * LDc + col] = v;
+            }
+            cl.sync();
+            cur ^= 1;
         }
-        return;
+        ++sweeps;
+        conv = !s_rot;
+        __syncthreads();
     }
-    for (int k = kf + tid; k < K; k += nt) {
-        st.evals[k] = __longlong_as_double(0x7ff8000000000000ll);
-        st.resid[k] = __longlong_as_double(0x7ff8000000000000ll);
+    // results to the global workspace (T diagonal, S rows), CTA 0 finishes
+    const int LS = a.ld_log2;
+    double *Tg = a.work, *Sg = a.work + ((size_t)M << LS);
+    const double *Tf = cur ? T1 : T0;
+    for (int i = tid; i < nloc * M; i += nt) {
+        const int rl = i / M, col = i - rl * M, r = r0 + rl;
+        Sg[((size_t)r << LS) + col] = Sl[(size_t)rl * LDc + col];
+        if (col == r) Tg[((size_t)r << LS) + r] = Tf[(size_t)rl * LDc + col];
     }
-    if (tid == 0) {
-        *st.k_found = kf;
-        *st.jac_sweeps = sweeps;
-        *st.jac_conv = conv;
-    }
+    __threadfence();
+    cl.sync();
+    if (br != 0) return;
+    jac_finish(a, Tg, Sg, LS, mm, sweeps, conv);
 }
 
 // ---------------------------------------------------------------------------

@@ -138,6 +138,8 @@ struct topk_eig_s {
     int jac_ld_log2 = 0, jac_hl_log2 = 0;
 
     int jac_threads = 32;
+    int jac_cl = 0;            // cluster size of k_jacobi_cl (0: single-CTA k_jacobi)
+    size_t jac_cl_smem = 0;
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     ncclComm_t comm = nullptr;
@@ -198,8 +200,25 @@ static void launch_jacobi(topk_eig_s *h, int check) {
         a.check = check;
         a.conv_tol = h->conv_tol;
         prof_begin(h, p, 4);
-        if (h->jac_work) k_jacobi<false><<<1, h->jac_threads, 0, h->stream>>>(a);
-        else k_jacobi<true><<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
+        if (h->jac_cl > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)h->jac_cl);
+            cfg.blockDim = dim3(kJacClNT);
+            cfg.dynamicSmemBytes = h->jac_cl_smem;
+            cfg.stream = h->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)h->jac_cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, k_jacobi_cl, a));
+        } else if (h->jac_work) {
+            k_jacobi<false><<<1, h->jac_threads, 0, h->stream>>>(a);
+        } else {
+            k_jacobi<true><<<1, h->jac_threads, h->jac_smem, h->stream>>>(a);
+        }
         CUDA_TRY(cudaGetLastError());
         prof_end(h, p);
         h->launches++;
@@ -656,13 +675,48 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             CUDA_TRY(cudaFuncGetAttributes(&fa, k_jacobi<true>));
             h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
         }
-        if (jbytes <= 200 * 1024) {
+        // single CTA in shared memory for M <= 40; above that the cluster path is
+        // faster (tools/jac_timing.py, profiles/r01_jacobi_timing.jsonl: m = 48 1.06 vs
+        // 1.27 ms, m = 96 2.7 vs 8.4 ms, m = 192 10.9 vs 106 ms)
+        const char *jf = std::getenv("TOPK_JAC_CLUSTER");  // 1: cluster path at any m (experiments)
+        if (jbytes <= 200 * 1024 && M <= 40 && !(jf && jf[0] == '1')) {
             h->jac_smem = jbytes;
             CUDA_TRY(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
         } else {
             h->jac_smem = 0;
             h->jac_bytes = (jbytes + 255) / 256 * 256;
             h->jac_work = h->alloc<double>((size_t)nlocal * h->jac_bytes / 8);
+            // T, S distributed over a thread-block cluster when they fit its shared memory
+            const char *ev = std::getenv("TOPK_NO_JAC_CLUSTER");
+            const char *ec = std::getenv("TOPK_JAC_CL");  // force a cluster size (experiments)
+            const int first = ec ? (std::atoi(ec) == 16 ? 16 : 8) : (M >= 96 ? 16 : 8);
+            for (int CL : {first, 24 - first}) {
+                if (ev && ev[0] == '1') break;
+                const size_t R = (size_t)(M + CL - 1) / CL;
+                const size_t cb = 3 * R * M * 8 + (size_t)M * 8 + (size_t)(2 * M + M) * 4 + 64;
+                if (cb > 200 * 1024) continue;
+                CUDA_TRY(cudaFuncSetAttribute(k_jacobi_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb));
+                if (CL > 8) CUDA_TRY(cudaFuncSetAttribute(k_jacobi_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)CL);
+                cfg.blockDim = dim3(kJacClNT);
+                cfg.dynamicSmemBytes = cb;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = (unsigned)CL;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, k_jacobi_cl, &cfg) != cudaSuccess || ncl < 1) {
+                    cudaGetLastError();
+                    continue;
+                }
+                h->jac_cl = CL;
+                h->jac_cl_smem = cb;
+                break;
+            }
         }
 
         h->parts.resize((size_t)nlocal);

@@ -343,3 +343,20 @@ def test_c3_full_size_parity_ddd(T):
     ref = O.solve(A.rowptr, A.col, A.val, K=24, m=24, seed=2)
     r = T.solve(A, 24, storage="f64", compute="f64", m=24, seed=2, check_symmetry=False)
     check_solve(r, ref, 1e-8)
+
+
+@pytest.mark.parametrize("m", [64, 130, 192, 300])
+@pytest.mark.parametrize("cluster", [True, False])
+def test_large_m_jacobi_paths(T, c3s, m, cluster, monkeypatch):
+    """Krylov dimensions whose T, S do not fit one SM's shared memory: the
+    cluster-distributed Jacobi (8 CTAs at m = 64; 16 at m = 130, 192, 300) and the
+    single-CTA global-memory fallback both match the oracle (reading Q10)."""
+    if not cluster:
+        monkeypatch.setenv("TOPK_NO_JAC_CLUSTER", "1")
+    ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=24, m=m, seed=8)
+    with T.TopkEig(c3s, 24, "f64", "f64", m=m) as h:
+        r = h.solve(seed=8)
+        _, _, th = h.tridiag()
+    assert r.info["jacobi_converged"] == 1
+    assert normwise(th, ref.theta_all) <= 1e-8
+    check_solve(r, ref, 1e-8)
