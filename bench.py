@@ -52,6 +52,9 @@ WORKLOADS = {
     "C4": dict(desc="R-MAT ids over 2^27 (Graph500 a,b,c=.57,.19,.19) rejected if >= n, n=100,000,000, "
                     "1.41e9 samples, seed 27, symmetric, deduplicated, bf16-exact weights",
                K=16, m=16, storage="f32", compute="f64"),
+    "C4X": dict(desc="R-MAT S=27 (n=2^27 = 134,217,728, GAP-kron's n, PAPER.md:180), 2.0e9 samples, seed 28, "
+                     "symmetric, deduplicated -> nnz ~2.2e9 > 2^31 (64-bit offsets, SURVEY 8(f) NEXT-4)",
+                K=16, m=16, storage="f32", compute="f64"),
 }
 
 

@@ -123,8 +123,8 @@ typedef struct {
  *             (F32,F32) "FFF", (BF16,F64); values_storage BF16 with F32 vectors.
  * Steps (DESIGN.md 8(a) rows a1-a4): canonicalise, check symmetry, partition by
  * nnz (rule P, reading Q15), build the per-part layout, upload to HBM.
- * Errors: TOPK_E_INVALID (K < 1, K > n, m < K, m > n, n >= 2^31, per-part nnz
- * >= 2^31, bad dtype pair, NULL pointers), TOPK_E_STRUCTURE, TOPK_E_NOT_SYMMETRIC,
+ * Errors: TOPK_E_INVALID (K < 1, K > n, m < K, m > n, n >= 2^31, G * n_pad >= 2^31,
+ * bad dtype pair, NULL pointers), TOPK_E_STRUCTURE, TOPK_E_NOT_SYMMETRIC,
  * TOPK_E_NOMEM, TOPK_E_CUDA, TOPK_E_NCCL, TOPK_E_NODEVICE. *out is NULL on error. */
 topk_status_t topk_eig_create(topk_eig_t *out, const topk_matrix_t *A, int32_t K,
                               topk_dtype_t storage, topk_dtype_t compute,
@@ -170,23 +170,24 @@ topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t
 
 /* Host-only per-part layout (rows a1, a3, a4 without a device): canonicalise A,
  * partition it by rule P into G parts and lay out part g exactly as
- * topk_eig_create uploads it for vector storage `storage` (the hot-row count
- * depends on it) and matrix values rounded to `values_storage`.
+ * topk_eig_create uploads it, matrix values rounded to `values_storage`
+ * (`storage` is validated only).
  *   sizes  (host, 9 int64 out): n_pad, n_rows, nnz, n_nonempty, nbig, nchunks,
  *          nslices, nitems, nphys
  *   logical CSR in degree order: rowptr (n_rows+1 int64), col (nnz int32 device
- *          column entries: cold q*n_pad+pos, hot bit31|hot index), val (nnz
- *          doubles = stored values), perm (n_rows int32: original part-local row
- *          at each position)
+ *          column entries q*n_pad+pos), val (nnz doubles = stored values), perm
+ *          (n_rows int32: original part-local row at each position)
  *   physical SpMV format: pcol (nphys int32), pval (nphys doubles), chunks (4
- *          int32 each: row, first, count, long id), sell (2 int32 per slice:
- *          base, width), items (2 int32 per SELL work item: first, end slice)
+ *          int64 each: row, first physical nonzero, count, long id), sell (2
+ *          int64 per slice: base, width), items (2 int32 per SELL work item:
+ *          first, end slice). Offsets are 64-bit: a part may hold >= 2^31
+ *          nonzeros.
  * Every array pointer may be NULL. Used by the multi-process CPU tests (each
  * rank plans its own part). Errors as in create. */
 topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g, topk_dtype_t storage,
                                    topk_dtype_t values_storage, int64_t *sizes, int64_t *rowptr,
                                    int32_t *col, double *val, int32_t *perm, int32_t *pcol, double *pval,
-                                   int32_t *chunks, int32_t *sell, int32_t *items);
+                                   int64_t *chunks, int64_t *sell, int32_t *items);
 
 /* Per kernel class device time of the last solve (requires opts.profile = 1):
  * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz pass 0 (norms), 6 ritz pass 1 (output),

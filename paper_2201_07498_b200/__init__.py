@@ -154,7 +154,7 @@ def plan_layout(A, G: int, g: int, storage: str = "f64", values_storage: str | N
                rowptr=np.zeros(nr + 1, np.int64), col=np.zeros(max(nz, 1), np.int32),
                val=np.zeros(max(nz, 1)), perm=np.zeros(max(nr, 1), np.int32),
                pcol=np.zeros(max(nph, 1), np.int32), pval=np.zeros(max(nph, 1)),
-               chunks=np.zeros((max(nch, 1), 4), np.int32), sell=np.zeros((max(nsl, 1), 2), np.int32),
+               chunks=np.zeros((max(nch, 1), 4), np.int64), sell=np.zeros((max(nsl, 1), 2), np.int64),
                items=np.zeros((max(nit, 1), 2), np.int32))
     _check(_lib.topk_eig_plan_layout(ctypes.byref(mat), G, g, st, vs, None, *[_ptr(out[k]) for k in (
         "rowptr", "col", "val", "perm", "pcol", "pval", "chunks", "sell", "items")]))

@@ -269,7 +269,7 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
     const int64_t r0 = b[g], r1 = b[g + 1];
     const int64_t z0 = m.rowptr[(size_t)r0], z1 = m.rowptr[(size_t)r1];
-    if (z1 - z0 >= (1ll << 31) - (1ll << 26)) { err = "per-part nnz must be < 2^31 - 2^26"; return TOPK_E_INVALID; }
+    (void)z0; (void)z1;  // any per-part nnz (64-bit offsets)
     if ((int64_t)G * npad >= (1ll << 31)) { err = "G * n_pad must be < 2^31"; return TOPK_E_INVALID; }
     (void)G;
     out.row0 = r0;
@@ -284,7 +284,7 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     for (int64_t p = 0; p < ng; ++p) {
         const int64_t r = r0 + out.perm[(size_t)p];
         const int64_t len = m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r];
-        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + (int32_t)len;
+        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + len;
         if (len > 0) nne = p + 1;
     }
     out.nnonempty = nne;
@@ -295,12 +295,13 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     out.chunks.clear();
     out.longrows.clear();
     for (int64_t p = 0; p < nbig; ++p) {
-        const int32_t rb = out.rowptr[(size_t)p], len = out.rowptr[(size_t)p + 1] - rb;
-        const int32_t nch = (len + kChunkNnz - 1) / kChunkNnz;
+        const int64_t rb = out.rowptr[(size_t)p], len = out.rowptr[(size_t)p + 1] - rb;
+        const int32_t nch = (int32_t)((len + kChunkNnz - 1) / kChunkNnz);
         const int32_t lid = nch > 1 ? (int32_t)out.longrows.size() : -1;
         if (nch > 1) out.longrows.push_back(LongRow{(int32_t)p, (int32_t)out.chunks.size(), nch, 0});
         for (int32_t c = 0; c < nch; ++c)
-            out.chunks.push_back(Chunk{(int32_t)p, rb + c * kChunkNnz, std::min(kChunkNnz, len - c * kChunkNnz), lid});
+            out.chunks.push_back(Chunk{rb + (int64_t)c * kChunkNnz, (int32_t)p,
+                                       (int32_t)std::min<int64_t>(kChunkNnz, len - (int64_t)c * kChunkNnz), lid, 0});
     }
     const int64_t zbig = out.rowptr[(size_t)nbig];
     const int64_t nsl = (nne - nbig + 31) / 32;
@@ -308,12 +309,11 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     int64_t phys = zbig;
     for (int64_t sl = 0; sl < nsl; ++sl) {
         const int64_t p0 = nbig + 32 * sl;
-        const int32_t w = out.rowptr[(size_t)p0 + 1] - out.rowptr[(size_t)p0];
-        out.sell[(size_t)(2 * sl)] = (int32_t)phys;
+        const int64_t w = out.rowptr[(size_t)p0 + 1] - out.rowptr[(size_t)p0];
+        out.sell[(size_t)(2 * sl)] = phys;
         out.sell[(size_t)(2 * sl + 1)] = w;
-        phys += 32 * (int64_t)w;
+        phys += 32 * w;
     }
-    if (phys >= (1ll << 31) - 256) { err = "padded per-part nnz must be < 2^31"; return TOPK_E_INVALID; }
     out.pcol.resize((size_t)phys);
     out.pval.resize((size_t)phys);
     // every entry straight from the canonical CSR to its physical slot (rows in

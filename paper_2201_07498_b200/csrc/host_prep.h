@@ -82,11 +82,12 @@ constexpr int kSellMaxLen = 128;
 constexpr int kChunkNnz = 2048;
 constexpr int kSellItemWidth = 64;
 
-struct Chunk {       // big-row chunk
+struct Chunk {       // big-row chunk (24 bytes; z0 is 64-bit: parts may hold >= 2^31 nonzeros)
+    int64_t z0;      // first physical nonzero
     int32_t row;     // position of the row
-    int32_t z0;      // first physical nonzero
     int32_t cnt;     // nonzeros (<= kChunkNnz)
     int32_t long_id; // -1: the chunk is the whole row; else index into longrows
+    int32_t pad;
 };
 struct LongRow {
     int32_t row;
@@ -97,7 +98,7 @@ struct LongRow {
 
 struct PartLayout {
     int64_t row0 = 0, nrows = 0, npad = 0, nnonempty = 0;
-    std::vector<int32_t> rowptr;    // nrows+1, logical CSR in degree order
+    std::vector<int64_t> rowptr;    // nrows+1, logical CSR in degree order
     std::vector<int32_t> perm;      // nrows: part-local original row at each position
     // physical SpMV format
     int32_t nbig = 0;
@@ -105,7 +106,7 @@ struct PartLayout {
     hvec<double> pval;              // physical values
     std::vector<Chunk> chunks;
     std::vector<LongRow> longrows;
-    std::vector<int32_t> sell;      // 2 per slice: base, width
+    std::vector<int64_t> sell;      // 2 per slice: base (physical index), width
     std::vector<int32_t> items;     // 2 per SELL work item: first slice, end slice
 };
 

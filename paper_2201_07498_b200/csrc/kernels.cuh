@@ -174,9 +174,9 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
 struct SpmvArgs {
     const int32_t *col;   // physical
     const void *val;      // physical
-    const int4 *chunks;   // [nchunks] Chunk
+    const Chunk *chunks;  // [nchunks] (64-bit first nonzero: parts may hold >= 2^31 nonzeros)
     const int4 *longrows; // [nlong] LongRow
-    const int2 *sell;     // [nslices] (base, width)
+    const longlong2 *sell; // [nslices] (base, width)
     const int2 *items;    // [nitems] (first slice, end slice)
     int nchunks, nitems, nbig, nnonempty, nlong;
     double *long_parts;   // [nchunks]
@@ -227,15 +227,16 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
     for (int wi = gwarp; wi < nwork; wi += nwarps) {
         if (wi < a.nchunks) {
             // ---- big-row chunk: lane stream k = zb + lane + 32 t, warp reduction
-            const int4 C = __ldg(a.chunks + wi);
-            const int zb = C.y, ze = C.y + C.z;
-            const int nt = (ze - zb - lane + 31) / 32;  // this lane's element count
+            const Chunk *Cp = a.chunks + wi;
+            const int64_t zb = __ldg(&Cp->z0);
+            const int crow = __ldg(&Cp->row), ccnt = __ldg(&Cp->cnt), clid = __ldg(&Cp->long_id);
+            const int nt = (ccnt - lane + 31) / 32;  // this lane's element count
             CT acc0 = CT(0), acc1 = CT(0);
             int cc[GQ];
             VT vv[GQ];
 #pragma unroll
             for (int q = 0; q < GQ; ++q) {
-                const int k = zb + lane + 32 * q;
+                const int64_t k = zb + lane + 32 * q;
                 cc[q] = q < nt ? ld_col_stream(col + k) : 0;
                 vv[q] = q < nt ? ld_val_stream<VT>(val + k) : VT(0);
             }
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
                 for (int q = 0; q < GQ; ++q) {
                     vc[q] = vv[q];
                     const int t = t0 + GQ + q;
-                    const int k = zb + lane + 32 * t;
+                    const int64_t k = zb + lane + 32 * t;
                     cc[q] = t < nt ? ld_col_stream(col + k) : 0;
                     vv[q] = t < nt ? ld_val_stream<VT>(val + k) : VT(0);
                 }
@@ -260,25 +261,25 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
             }
             CT part = warp_sum(acc0 + acc1);
             if (lane == 0) {
-                if (C.w < 0) {
+                if (clid < 0) {
                     const CT yv = s * part;
-                    y[C.x] = rnd_ct<ST, CT>(yv);
-                    alpha_acc += yv * (s * cvt<CT>(ui[C.x]));
-                    if (a.y_dbg) a.y_dbg[C.x] = (double)part;
+                    y[crow] = rnd_ct<ST, CT>(yv);
+                    alpha_acc += yv * (s * cvt<CT>(ui[crow]));
+                    if (a.y_dbg) a.y_dbg[crow] = (double)part;
                 } else {
-                    const int4 L = __ldg(a.longrows + C.w);
+                    const int4 L = __ldg(a.longrows + clid);
                     a.long_parts[wi] = (double)part;
                     __threadfence();
-                    const unsigned prev = atomicAdd(a.long_cnt + C.w, 1u);
+                    const unsigned prev = atomicAdd(a.long_cnt + clid, 1u);
                     if (prev == (unsigned)L.z - 1) {
                         __threadfence();
                         CT sum = CT(0);
                         for (int q = 0; q < L.z; ++q) sum += (CT)__ldcg(a.long_parts + L.y + q);
                         const CT yv = s * sum;
                         y[L.x] = rnd_ct<ST, CT>(yv);
-                        a.alpha_long[C.w] = (double)(yv * (s * cvt<CT>(ui[L.x])));
+                        a.alpha_long[clid] = (double)(yv * (s * cvt<CT>(ui[L.x])));
                         if (a.y_dbg) a.y_dbg[L.x] = (double)sum;
-                        a.long_cnt[C.w] = 0u;
+                        a.long_cnt[clid] = 0u;
                     }
                 }
             }
@@ -287,17 +288,17 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
             // streams base + 32 t + l for t = 0 .. sum(w) - 1; slice boundaries are
             // warp-uniform (row result emitted, accumulator reset)
             const int2 I = __ldg(a.items + (wi - a.nchunks));
-            const int base = __ldg(a.sell + I.x).x;
-            const int2 Sl = __ldg(a.sell + (I.y - 1));
-            const int ntot = (Sl.x - base) / 32 + Sl.y;  // total width of the item
+            const int64_t base = __ldg(a.sell + I.x).x;
+            const longlong2 Sl = __ldg(a.sell + (I.y - 1));
+            const int ntot = (int)((Sl.x - base) / 32 + Sl.y);  // total width of the item
             int sl = I.x;
-            int bound = __ldg(a.sell + sl).y;  // t at which slice sl ends
+            int bound = (int)__ldg(a.sell + sl).y;  // t at which slice sl ends
             CT acc = CT(0);
             int cc[GQ];
             VT vv[GQ];
 #pragma unroll
             for (int q = 0; q < GQ; ++q) {
-                const int k = base + lane + 32 * q;
+                const int64_t k = base + lane + 32 * q;
                 cc[q] = q < ntot ? ld_col_stream(col + k) : 0;
                 vv[q] = q < ntot ? ld_val_stream<VT>(val + k) : VT(0);
             }
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
                 for (int q = 0; q < GQ; ++q) {
                     vc[q] = vv[q];
                     const int t = t0 + GQ + q;
-                    const int k = base + lane + 32 * t;
+                    const int64_t k = base + lane + 32 * t;
                     cc[q] = t < ntot ? ld_col_stream(col + k) : 0;
                     vv[q] = t < ntot ? ld_val_stream<VT>(val + k) : VT(0);
                 }
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
                             }
                             acc = CT(0);
                             ++sl;
-                            if (sl < I.y) bound += __ldg(a.sell + sl).y;
+                            if (sl < I.y) bound += (int)__ldg(a.sell + sl).y;
                         }
                     }
                 }

@@ -87,12 +87,13 @@ struct Part {
     int32_t *col = nullptr, *perm = nullptr;
     std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
     int32_t *inv = nullptr;         // original part-local row -> position
-    std::vector<int32_t> h_sell;    // host copy of the SELL table (export_layout)
-    std::vector<int32_t> h_rowptr;  // host copy (export_layout)
+    std::vector<int64_t> h_sell;    // host copy of the SELL table (export_layout)
+    std::vector<int64_t> h_rowptr;  // host copy (export_layout)
     void *val = nullptr;
     Chunk *chunks = nullptr;
     LongRow *longrows = nullptr;
-    int32_t *sell = nullptr, *items = nullptr;
+    int64_t *sell = nullptr;
+    int32_t *items = nullptr;
     void *yt = nullptr;            // Ritz output in position order, K values per row
     double *long_parts = nullptr, *alpha_long = nullptr;
     unsigned *long_cnt = nullptr;
@@ -262,8 +263,8 @@ template <typename VT, typename ST, typename CT>
 static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     SpmvArgs a;
     a.col = p.col; a.val = p.val;
-    a.chunks = reinterpret_cast<const int4 *>(p.chunks); a.longrows = reinterpret_cast<const int4 *>(p.longrows);
-    a.sell = reinterpret_cast<const int2 *>(p.sell); a.items = reinterpret_cast<const int2 *>(p.items);
+    a.chunks = p.chunks; a.longrows = reinterpret_cast<const int4 *>(p.longrows);
+    a.sell = reinterpret_cast<const longlong2 *>(p.sell); a.items = reinterpret_cast<const int2 *>(p.items);
     a.nchunks = p.nchunks; a.nitems = p.nitems; a.nbig = p.nbig; a.nnonempty = (int)p.nnonempty;
     a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
     a.alpha_long = p.alpha_long; a.nlong = p.nlong;
@@ -741,7 +742,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.inv = h->alloc<int32_t>(L.perm.size());
             p.chunks = h->alloc<Chunk>(L.chunks.size());
             p.longrows = h->alloc<LongRow>(L.longrows.size());
-            p.sell = h->alloc<int32_t>(L.sell.size());
+            p.sell = h->alloc<int64_t>(L.sell.size());
             p.items = h->alloc<int32_t>(L.items.size());
             p.long_parts = h->alloc<double>(L.chunks.size());
             p.long_cnt = h->alloc<unsigned>(L.longrows.size());
@@ -756,7 +757,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             if (!L.pcol.empty()) CUDA_TRY(cudaMemcpy(p.col, L.pcol.data(), L.pcol.size() * 4, cudaMemcpyHostToDevice));
             if (!L.chunks.empty()) CUDA_TRY(cudaMemcpy(p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
-            if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
             if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
             upload_values(h.get(), p, L);
             clk.mark("upload (H2D)");
@@ -993,8 +994,8 @@ topk_status_t topk_eig_plan_partition(const int64_t *row_ptr, int64_t n, int32_t
 
 topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g, topk_dtype_t storage,
                                    topk_dtype_t values_storage, int64_t *sizes, int64_t *rowptr, int32_t *col,
-                                   double *val, int32_t *perm, int32_t *pcol, double *pval, int32_t *chunks,
-                                   int32_t *sell, int32_t *items) {
+                                   double *val, int32_t *perm, int32_t *pcol, double *pval, int64_t *chunks,
+                                   int64_t *sell, int32_t *items) {
     if (!A) return fail(TOPK_E_INVALID, "A must be non-NULL");
     if (G < 1 || G > 64 || g < 0 || g >= G) return fail(TOPK_E_INVALID, "need 1 <= G <= 64 and 0 <= g < G");
     if (values_storage < TOPK_F64 || values_storage > TOPK_BF16 || storage < TOPK_F64 || storage > TOPK_BF16)
@@ -1040,8 +1041,14 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
         if (pcol) std::memcpy(pcol, L.pcol.data(), L.pcol.size() * 4);
         if (pval)
             for (size_t k = 0; k < L.pval.size(); ++k) pval[k] = rv(L.pval[k]);
-        if (chunks) std::memcpy(chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk));
-        if (sell) std::memcpy(sell, L.sell.data(), L.sell.size() * 4);
+        if (chunks)
+            for (size_t c = 0; c < L.chunks.size(); ++c) {
+                chunks[4 * c] = L.chunks[c].row;
+                chunks[4 * c + 1] = L.chunks[c].z0;
+                chunks[4 * c + 2] = L.chunks[c].cnt;
+                chunks[4 * c + 3] = L.chunks[c].long_id;
+            }
+        if (sell) std::memcpy(sell, L.sell.data(), L.sell.size() * 8);
         if (items) std::memcpy(items, L.items.data(), L.items.size() * 4);
     } catch (std::bad_alloc &) {
         return fail(TOPK_E_NOMEM, "host allocation failed");

@@ -161,6 +161,8 @@ def config_matrix(name: str):
     C3S: R-MAT S=16 (n=65,536), 491,520 samples, seed 16 (C3 shape, oracle-fast).
     C4: R-MAT ids over 2^27 rejected if >= n = 100,000,000, 1,410,000,000 samples,
         seed 27 -> nnz ~ 1.5e9 (host RAM ~45 GB while generating).
+    C4X: R-MAT S=27, n = 2^27 (GAP-kron's n), 2.0e9 samples, seed 28 ->
+        nnz ~ 2.2e9 > 2^31 (host RAM ~70 GB while generating).
     """
     if name == "C1":
         return er_coo(10_000, 50_000, 1)
@@ -174,4 +176,6 @@ def config_matrix(name: str):
         return rmat(16, 491_520, 16)
     if name == "C4":
         return rmat(27, 1_410_000_000, 27, n=100_000_000)
+    if name == "C4X":
+        return rmat(27, 2_000_000_000, 28)
     raise KeyError(name)

@@ -18,8 +18,7 @@ import pytest
 import oracle as O
 import synthgen as S
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(os.environ.get("TOPK_C4") != "1", reason="opt-in: TOPK_C4=1")]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 @pytest.fixture(scope="module")
@@ -28,15 +27,16 @@ def T():
     return T
 
 
-def run_c4(T, parts):
-    out = {"config": "C4", "parts": parts}
+def run_c4(T, parts, name="C4"):
+    out = {"config": name, "parts": parts}
     t0 = time.time()
-    A = S.config_matrix("C4")
+    A = S.config_matrix(name)
     out.update(n=int(A.n), nnz=int(A.nnz), gen_s=round(time.time() - t0, 1))
     t0 = time.time()
     K, m = 16, 16
     with T.TopkEig(A, K, storage="f32", compute="f64", m=m, parts=parts, check_symmetry=False) as h:
         out["create_s"] = round(time.time() - t0, 1)
+        out["_b"] = h.partition().tolist()
         # SpMV parity, every row
         x = np.random.default_rng(4).standard_normal(A.n)
         y = h.debug_spmv(x)
@@ -67,15 +67,30 @@ def run_c4(T, parts):
     res = float(np.linalg.norm(O.spmv(A.rowptr, A.col, av, y0) - th * y0) / abs(th))
     out.update(theta1=th, residual_true_rel=res, residual_est_rel=float(r.residual_est[0] / abs(th)),
                k_found=int(r.info["k_found"]), iterations=int(r.info["iterations"]))
+    b = np.asarray(out.pop("_b"))
+    out["max_part_nnz"] = int(np.diff(A.rowptr[b]).max())
     print("C4CHECK " + json.dumps(out), flush=True)
     return out
 
 
 
 
+@pytest.mark.skipif(os.environ.get("TOPK_C4") != "1", reason="opt-in: TOPK_C4=1")
 @pytest.mark.parametrize("parts", [1, 8])
 def test_c4_full_size(T, parts):
     out = run_c4(T, parts)
+    assert out["spmv_bound_violations"] == 0
+    assert out["alpha1_rel_err"] <= 1e-6
+    assert out["k_found"] == 16
+    assert abs(out["residual_true_rel"] - out["residual_est_rel"]) <= 1e-4 + 1e-2 * out["residual_est_rel"]
+
+
+@pytest.mark.skipif(os.environ.get("TOPK_BIG") != "1", reason="opt-in: TOPK_BIG=1 (~4 min, ~100 GB host RAM)")
+def test_over_2g_nonzeros_one_part(T):
+    """one part holding more than 2^31 nonzeros (64-bit
+    physical offsets), n = 2^27 (GAP-kron's n), same sampled-parity checks."""
+    out = run_c4(T, 1, "C4X")
+    assert out["nnz"] > 2 ** 31 and out["max_part_nnz"] > 2 ** 31
     assert out["spmv_bound_violations"] == 0
     assert out["alpha1_rel_err"] <= 1e-6
     assert out["k_found"] == 16
