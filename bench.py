@@ -416,6 +416,26 @@ def time_to_topk(T, A, wl, kw, reps=5):
         conv = int(np.sum(r.residual_est <= 1e-5 * abs(r.eigenvalues[0])))
         out[f"adaptive tol=1e-5 c={c}"] = {"ms": round(ms, 3), "iterations": r.info["iterations"],
                                            "converged_of_K": conv, "stopped": bool(r.info["converged_stop"])}
+    # thick restart (reading Q26): basis of m = 3K (2K+1 .. 3K steps per cycle), stop at tol
+    for mr, keep in ((3 * K, 3 * K // 2), (4 * K, 2 * K)):
+        with T.TopkEig(A, K, check_symmetry=False, conv_tol=1e-5, restart_keep=keep, max_restarts=40,
+                       **dict(kw, m=mr)) as h:
+            ev = torch.zeros(K, dtype=torch.float64, device="cuda")
+            h.solve_async(1, ev.data_ptr(), None)
+            h.sync()
+            stream = torch.cuda.ExternalStream(h.stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(reps):
+                h.solve_async(1, ev.data_ptr(), None)
+            e1.record(stream)
+            h.sync()
+            ms = e0.elapsed_time(e1) / reps
+            r = h.solve(seed=1, vectors=False)
+        conv = int(np.sum(r.residual_est <= 1e-5 * abs(r.eigenvalues[0])))
+        out[f"thick restart m={mr} keep={keep} tol=1e-5"] = {
+            "ms": round(ms, 3), "iterations": r.info["iterations"], "restarts": r.info["restarts"],
+            "converged_of_K": conv, "stopped": bool(r.info["converged_stop"])}
     return out
 
 

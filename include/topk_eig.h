@@ -99,6 +99,14 @@ typedef struct {
      * the remaining launches of the graph see the stop flag and return at once. */
     double conv_tol;         /* 0 -> off (fixed krylov_dim iterations)                             */
     int32_t conv_check;      /* check period c; 0 -> K                                             */
+    /* thick-restart Lanczos (Wu & Simon 2000, reading Q26; not in the
+     * paper): with restart_keep = k > 0 the basis holds krylov_dim = m vectors; after each cycle the
+     * k Ritz pairs of largest |theta| are kept (T becomes [[diag(theta), b], [b^T, tridiag]]) and the
+     * iteration continues with steps k+1 .. m, up to max_restarts restarts; with conv_tol > 0 it stops
+     * at the end of the first cycle whose K selected pairs meet the residual test. Requires
+     * reorthogonalisation; K <= k <= min(m - 2, 256). Periodic conv_check tests are not used. */
+    int32_t restart_keep;    /* 0 -> off                                                            */
+    int32_t max_restarts;    /* restarts at most (the graph holds max_restarts + 1 cycles)           */
 } topk_eig_opts_t;
 
 typedef struct {
@@ -112,8 +120,10 @@ typedef struct {
     double ms_solve;          /* device time of the whole solve (CUDA events)                       */
     int64_t bytes_model;      /* algorithmic HBM bytes of the solve on this part        */
     int64_t gpu_launches;     /* kernels launched by the solve (this part)                          */
-    int32_t converged_stop;   /* 1 if conv_tol stopped the iteration at m' < krylov_dim             */
+    int32_t converged_stop;   /* 1 if conv_tol stopped the iteration early                         */
     int32_t conv_checks;      /* convergence checks enqueued per solve                             */
+    int32_t restarts;         /* thick restarts done (iterations then counts every Lanczos step)   */
+    int32_t reserved_;
 } topk_eig_info_t;
 
 /* Create a solver for M, K eigenpairs, storage/compute precision pair.

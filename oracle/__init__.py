@@ -324,3 +324,86 @@ def solve_adaptive(rowptr, col, val, K: int, m_max: int, tol: float, check: int 
     rest = np.abs(lz.beta[mm] * S[mm - 1, idx]) if mm > 0 else np.zeros(0)
     return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, rest,
                     extra={"converged_stop": stop is not None})
+
+
+def solve_thick_restart(rowptr, col, val, K: int, m: int, keep: int, max_restarts: int,
+                        tol: float = 0.0, seed: int = 1, v1vec=None, tau: float = 1e-12,
+                        want_vectors: bool = True) -> SolveOut:
+    """Thick-restart Lanczos (Wu & Simon, SIAM J. Matrix Anal. Appl. 22(2), 2000;
+    SURVEY 8(f) NEXT-2, reading Q26) around the paper's iteration
+    (Alg.1 l.5-18 with full MGS reorthogonalisation, O4-O5) and Jacobi (O7):
+      cycle: Lanczos steps i = k+1 .. m on V (k = 0 in the first cycle);
+      end of cycle: T_m = S diag(theta) S^T (O7); stop if max_restarts restarts
+        were done, or (tol > 0) all K selected pairs (O8) have residual estimate
+        |beta_{m+1} s_{m,k}| <= tol |theta_1| (O10);
+      restart: keep the `keep` Ritz pairs of largest |theta| (order O8):
+        V[0:keep] = (V_m S_J)^T, V[keep] = v_{m+1},
+        T = [[diag(theta_J), b], [b^T, .]] with b_j = beta_{m+1} s_{m,j};
+        the first step after a restart subtracts sum_j b_j y_j instead of the
+        beta_i v_{i-1} term (the arrowhead coupling), then MGS as usual.
+    Plain numpy vector algebra + the oracle's C SpMV, fp64, no blocking."""
+    n = len(rowptr) - 1
+    if v1vec is None:
+        v1vec = v1(seed, n)
+    u = np.asarray(v1vec, np.float64)
+    V = np.zeros((m + 1, n), np.float64)
+    V[0] = u / np.sqrt(np.dot(u, u))
+    T = np.zeros((m, m), np.float64)
+    k = 0
+    restarts = 0
+    total = 0
+    tscale = 0.0
+    breakdown = False
+    mm = m
+    beta_next = 0.0
+    while True:
+        for i in range(k, m):                       # column i holds v_{i+1}
+            y = spmv(rowptr, col, val, V[i])        # l.9
+            a = float(np.dot(V[i], y))              # l.10
+            T[i, i] = a
+            tscale = max(tscale, abs(a))
+            w = y - a * V[i]                        # l.11
+            if i > k:
+                w -= T[i, i - 1] * V[i - 1]
+            elif k > 0:                             # first step after a restart
+                for j in range(k):
+                    w -= T[j, k] * V[j]
+            for j in range(i + 1):                  # l.12-18 full reorth (MGS, Q3)
+                w -= np.dot(V[j], w) * V[j]
+            b = float(np.sqrt(np.dot(w, w)))        # l.6
+            total += 1
+            if i + 1 < m:
+                if b <= tau * tscale:               # Q7
+                    breakdown = True
+                    mm = i + 1
+                    beta_next = b
+                    break
+                T[i + 1, i] = T[i, i + 1] = b
+                tscale = max(tscale, b)
+            V[i + 1] = w / b                        # l.7
+            beta_next = b
+        Tm = T[:mm, :mm]
+        theta, S, sw, conv = jacobi(Tm)
+        idx = select(theta, K)
+        res = np.abs(beta_next * S[mm - 1, idx])
+        done = breakdown or restarts == max_restarts or (
+            tol > 0 and len(idx) == K and bool(np.all(res <= tol * abs(theta[idx[0]]))))
+        if done:
+            break
+        J = select(theta, keep)
+        Y = S[:, J].T @ V[:m]                       # Ritz vectors (O9 without normalisation)
+        bvec = beta_next * S[m - 1, J]
+        V[keep] = V[m]
+        V[:keep] = Y
+        T = np.zeros((m, m), np.float64)
+        for j in range(keep):
+            T[j, j] = theta[J[j]]
+            T[j, keep] = T[keep, j] = bvec[j]
+        k = keep
+        restarts += 1
+    Y = ritz(V[:mm], S, idx) if want_vectors else None
+    lz = LanczosOut(np.diag(Tm).copy(), np.zeros(mm + 1), V[:mm].copy(), mm, breakdown)
+    lz.beta[mm] = beta_next
+    return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, res,
+                    extra={"restarts": restarts, "iterations": total, "T": Tm.copy(),
+                           "v_next": V[mm].copy() if mm < m + 1 else None})

@@ -49,7 +49,8 @@ class _Opts(ctypes.Structure):
                 ("breakdown_tol", ctypes.c_double), ("rank", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("profile", ctypes.c_int32), ("conv_tol", ctypes.c_double),
-                ("conv_check", ctypes.c_int32)]
+                ("conv_check", ctypes.c_int32), ("restart_keep", ctypes.c_int32),
+                ("max_restarts", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -58,7 +59,8 @@ class Info(ctypes.Structure):
                 ("jacobi_converged", ctypes.c_int32), ("num_parts", ctypes.c_int32),
                 ("beta_next", ctypes.c_double), ("ms_solve", ctypes.c_double),
                 ("bytes_model", ctypes.c_int64), ("gpu_launches", ctypes.c_int64),
-                ("converged_stop", ctypes.c_int32), ("conv_checks", ctypes.c_int32)]
+                ("converged_stop", ctypes.c_int32), ("conv_checks", ctypes.c_int32),
+                ("restarts", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -184,7 +186,8 @@ class TopkEig:
                  values_storage: str | None = None, use_graph: bool = True,
                  breakdown_tol: float = 0.0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, profile: bool = False,
-                 conv_tol: float = 0.0, conv_check: int = 0):
+                 conv_tol: float = 0.0, conv_check: int = 0, restart_keep: int = 0,
+                 max_restarts: int = 0):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -204,6 +207,8 @@ class TopkEig:
         o.profile = 1 if profile else 0
         o.conv_tol = float(conv_tol)
         o.conv_check = int(conv_check)
+        o.restart_keep = int(restart_keep)
+        o.max_restarts = int(max_restarts)
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

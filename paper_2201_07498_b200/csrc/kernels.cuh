@@ -51,6 +51,13 @@ struct LzState {
     int use_gram;       // 1: Ritz norms from the Gram matrix (k_step_tma path), 0: Ritz pass 0
     int m;
     double tau;
+    // thick restart (reading Q26): after a restart T is [[diag(theta), b], [b^T, tridiag]]
+    int *arrow_k;       // [1]     0: plain tridiagonal T; k: rows/cols [0, k) are the kept Ritz pairs
+    int *restarts;      // [1]     restarts done in this solve
+    double *arrow_theta;// [keep]  kept Ritz values (diagonal of T[0:k, 0:k])
+    double *arrow_b;    // [keep]  coupling b_j = beta_{m+1} s_{m,j} (T[j][k] = T[k][j])
+    double *coefR;      // [m*keep] S[l, J_j] * s_l: kept Ritz vectors in the stored basis
+    int keep;           // kept pairs per restart (0: off)
 };
 
 struct Exch {            // cross-part exchange buffers, slot g written by part g
@@ -58,6 +65,7 @@ struct Exch {            // cross-part exchange buffers, slot g written by part 
     double *hpart;       // [G][2 (m+1)]: reorth dots h_j at [0, m+1), Gram u_j . u_i at [m+1, 2 (m+1))
     double *norm_part;   // [G]
     double *ritz_part;   // [G][K]
+    double *rst_part;    // [G][keep] squared norms of the stored restart vectors
     void *replica;       // [G * npad] storage dtype (G > 1)
 };
 
@@ -118,6 +126,8 @@ __global__ void __launch_bounds__(kNT) k_v1(V1Args a) {
         *a.st.done = 0;
         *a.st.m_found = 0;
         *a.st.tscale = 0.0;
+        *a.st.arrow_k = 0;
+        *a.st.restarts = 0;
     }
     const uint64_t seed = *a.seed;
     const int use_v1 = *a.use_v1;
@@ -367,6 +377,7 @@ struct StepArgs {
     LzState st;
     Exch ex;
     int G, g, mode;
+    int no_prev;        // first step after a thick restart: no beta_i v_{i-1} term (reading Q26)
 };
 
 template <typename ST, typename CT, int JB>
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(kNT, 2) k_step(StepArgs a, int it) {
             *a.st.tscale = ts;
         }
         c1 = (CT)(al * a.st.scale[it - 1]);                       // alpha_i * s_i
-        c2 = (it > 1) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);    // beta_i * s_{i-1}
+        c2 = (it > 1 && !a.no_prev) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);    // beta_i * s_{i-1}
     }
     const ST *ucur = V + (size_t)(it - 1) * a.npad;
     const ST *uprev = V + (size_t)(it > 1 ? it - 2 : 0) * a.npad;
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(kNT, 2) k_stepw(StepArgs a, int it, int j0) {
             *a.st.tscale = ts;
         }
         c1 = (CT)(al * a.st.scale[it - 1]);                       // alpha_i * s_i
-        c2 = (it > 1) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);    // beta_i * s_{i-1}
+        c2 = (it > 1 && !a.no_prev) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);    // beta_i * s_{i-1}
     }
     const ST *ucur = V + (size_t)(it - 1) * a.npad;
     const ST *uprev = V + (size_t)(it > 1 ? it - 2 : 0) * a.npad;
@@ -753,7 +764,7 @@ __global__ void __launch_bounds__(256 * kStepNG, 1) k_step_tma(StepArgs a, int i
             *a.st.tscale = ts;
         }
         c1 = (CT)(al * a.st.scale[it - 1]);
-        c2 = (it > 1) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);
+        c2 = (it > 1 && !a.no_prev) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);
     }
     const ST *V = reinterpret_cast<const ST *>(a.V);
     ST *wv = reinterpret_cast<ST *>(a.w);
@@ -992,19 +1003,44 @@ struct JacArgs {
     double *work;  // global workspace when T, S do not fit in shared memory
     int ld_log2;   // LD = 1 << ld_log2 >= m + (m & 1)
     int hl_log2;   // 1 << hl_log2 >= (m + (m & 1)) / 2
-    // convergence check (reading Q25): 0 -> the final solve of T_m'; > 0 -> a check
-    // on T_i (i = m_found): if the K selected pairs all have residual estimate
-    // <= conv_tol |theta_1|, set *done = 2 (every later kernel returns at once)
+    // 0 -> the final solve of T_m'; 1 -> convergence check on T_i (i = m_found,
+    // reading Q25): if the K selected pairs all have residual estimate
+    // <= conv_tol |theta_1|, set *done = 2 (every later kernel returns at once);
+    // 2 -> end of a thick-restart cycle (reading Q26): the same test, else the
+    // restart data (coefR, arrow_theta, arrow_b) of the `keep` largest pairs
     int check;
     double conv_tol;
 };
 
-// ||T||_F of the tridiagonal T_mm in the oracle's summation order (row-major);
-// only the nonzeros are added (adding the exact zeros leaves the sum unchanged).
+// Entry (r, c) of T_mm: tridiagonal (alpha, beta), or after a thick restart
+// (reading Q26) the arrowhead [[diag(theta), b], [b^T, alpha_k]] followed by the
+// tridiagonal part (rows/cols >= k).
+__device__ __forceinline__ double jac_t(const LzState &st, int ak, int r, int c) {
+    if (r < ak || c < ak) {
+        if (r == c) return st.arrow_theta[r];
+        if (c == ak) return st.arrow_b[r];
+        if (r == ak) return st.arrow_b[c];
+        return 0.0;
+    }
+    if (r == c) return st.alpha[r];
+    if (r - c == 1 || c - r == 1) return (r > c ? r : c) > ak ? st.beta[r > c ? r : c] : 0.0;
+    return 0.0;
+}
+
+// ||T||_F of T_mm in the oracle's summation order (row-major); only the
+// nonzeros are added (adding the exact zeros leaves the sum unchanged).
 __device__ __forceinline__ double jac_fro(const LzState &st, int mm) {
+    const int ak = *st.arrow_k;
     double f = 0.0;
     for (int r = 0; r < mm; ++r) {
-        if (r > 0) f += st.beta[r] * st.beta[r];
+        if (r < ak) {  // arrow rows: (r, r), (r, ak)
+            f += st.arrow_theta[r] * st.arrow_theta[r];
+            if (ak < mm) f += st.arrow_b[r] * st.arrow_b[r];
+            continue;
+        }
+        if (r == ak && ak > 0)
+            for (int c = 0; c < ak; ++c) f += st.arrow_b[c] * st.arrow_b[c];
+        if (r > ak) f += st.beta[r] * st.beta[r];
         f += st.alpha[r] * st.alpha[r];
         if (r + 1 < mm) f += st.beta[r + 1] * st.beta[r + 1];
     }
@@ -1046,6 +1082,7 @@ __device__ void jac_finish(const JacArgs &a, const double *T, const double *S, i
     const LzState &st = a.st;
     const int K = a.K;
     const int kf = K < mm ? K : mm;
+    const int keep = st.keep;
     for (int c = tid; c < mm; c += nt) {
         const double tc = T[(c << LS) + c];
         st.theta_all[c] = tc;
@@ -1079,12 +1116,37 @@ __device__ void jac_finish(const JacArgs &a, const double *T, const double *S, i
         }
     }
     if (a.check) {
+        __shared__ int s_stop;
         __syncthreads();
-        if (tid == 0 && kf == K) {
-            const double lim = a.conv_tol * fabs(st.evals[0]);
-            int ok = 1;
-            for (int k = 0; k < K; ++k) ok &= (st.resid[k] <= lim);
-            if (ok) *st.done = 2;
+        if (tid == 0) {
+            int ok = 0;
+            if (kf == K && a.conv_tol > 0.0) {
+                const double lim = a.conv_tol * fabs(st.evals[0]);
+                ok = 1;
+                for (int k = 0; k < K; ++k) ok &= (st.resid[k] <= lim);
+                if (ok) *st.done = 2;
+            }
+            s_stop = ok;
+        }
+        __syncthreads();
+        if (a.check == 2 && !s_stop) {
+            // restart data (reading Q26), written only when the iteration goes on: the
+            // arrowhead arrays still describe the T a stopped solve finishes with
+            for (int c = tid; c < mm; c += nt) {
+                const double tc = T[(c << LS) + c];
+                int rank = 0;
+                for (int d = 0; d < mm; ++d) {
+                    const double td = T[(d << LS) + d];
+                    const bool before = (fabs(td) != fabs(tc)) ? (fabs(td) > fabs(tc))
+                                        : (td != tc) ? (td > tc) : (d < c);
+                    rank += before;
+                }
+                if (rank < keep) {  // y_j = sum_l S[l][c] v_l
+                    for (int l = 0; l < mm; ++l) st.coefR[(size_t)l * keep + rank] = S[(l << LS) + c] * st.scale[l];
+                    st.arrow_theta[rank] = tc;
+                    st.arrow_b[rank] = st.beta[mm] * S[((mm - 1) << LS) + c];
+                }
+            }
         }
         return;
     }
@@ -1121,13 +1183,10 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
     double *cs = S + (size_t)M * LD;                      // [M/2][2]
     int *pq = reinterpret_cast<int *>(cs + (size_t)M);    // [M/2][2]
     int *rot = pq + M;                                    // [M/2]
+    const int ak = *st.arrow_k;
     for (int i = tid; i < M * LD; i += nt) {
         const int r = i >> LS, c = i & (LD - 1);
-        double t = 0.0;
-        if (r < mm && c < mm) {
-            if (r == c) t = st.alpha[r];
-            else if (r - c == 1 || c - r == 1) t = st.beta[r > c ? r : c];
-        }
+        const double t = (r < mm && c < mm) ? jac_t(st, ak, r, c) : 0.0;
         T[i] = t;
         S[i] = (r == c) ? 1.0 : 0.0;
     }
@@ -1272,13 +1331,10 @@ __global__ void __launch_bounds__(kJacClNT, 1) k_jacobi_cl(JacArgs a) {
     int *pq = reinterpret_cast<int *>(cs + 2 * half);  // [half][2]
     int *rot = pq + 2 * half;                          // [half]
     int *prow = rot + half;                            // [M]: 2 k + (row is the q of pair k)
+    const int ak = *st.arrow_k;
     for (int i = tid; i < nloc * LDc; i += nt) {
         const int rl = i / LDc, c = i - rl * LDc, r = r0 + rl;
-        double t = 0.0;
-        if (r < mm && c < mm) {
-            if (r == c) t = st.alpha[r];
-            else if (r - c == 1 || c - r == 1) t = st.beta[r > c ? r : c];
-        }
+        const double t = (r < mm && c < mm) ? jac_t(st, ak, r, c) : 0.0;
         T0[i] = t;
         Sl[i] = (r == c) ? 1.0 : 0.0;
     }
@@ -1521,6 +1577,142 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
         __syncthreads();
         if (tid == 0) a.counter[grp] = 0u;
     }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Thick restart (reading Q26; not in the paper):
+// Y_j = sum_l coefR[l][j] u_l (coefR = S_J diag(s), the kept Ritz vectors of the
+// cycle's T), rounded to the storage dtype into the scratch columns, with the
+// squared norm of each stored y_j (fp64 partials, last block per output group
+// sums them in block order -> ex.rst_part[g][j]). One pass over the basis per
+// group of KB kept vectors.
+struct RestartArgs {
+    void *V;             // basis (mm + 1 columns used)
+    void *Vs;            // scratch: keep columns of npad
+    int64_t npad;
+    int keep, G, g, mm;
+    double *slots;       // [gridDim.x][KB]
+    unsigned *counter;   // [ceil(keep / KB)]
+    LzState st;
+    Exch ex;
+};
+
+template <typename ST, typename CT, int KB>
+__global__ void __launch_bounds__(kNT, 2) k_restart_proj(RestartArgs a) {
+    constexpr int VW = Vw<ST>::N;
+    extern __shared__ double rsm[];  // coef[mm][KB]
+    __shared__ CT part[kNT / 32][KB];
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int mm = a.mm, keep = a.keep;
+    const int ngroups = (keep + KB - 1) / KB;
+    const int grp = (int)(blockIdx.x % (unsigned)ngroups);
+    const int rblk = (int)(blockIdx.x / (unsigned)ngroups), nrblk = (int)(gridDim.x / (unsigned)ngroups);
+    const int k0 = grp * KB;
+    CT *coef = reinterpret_cast<CT *>(rsm);
+    for (int i = tid; i < mm * KB; i += kNT) {
+        const int j = i / KB, q = i - j * KB;
+        coef[i] = (k0 + q < keep) ? (CT)a.st.coefR[(size_t)j * keep + k0 + q] : CT(0);
+    }
+    __syncthreads();
+    const ST *V = reinterpret_cast<const ST *>(a.V);
+    ST *Vs = reinterpret_cast<ST *>(a.Vs);
+    const int64_t nvec = a.npad / VW;
+    CT nrm[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) nrm[q] = CT(0);
+    for (int64_t v = (int64_t)rblk * kNT + tid; v < nvec; v += (int64_t)nrblk * kNT) {
+        CT acc[VW][KB];
+#pragma unroll
+        for (int e = 0; e < VW; ++e)
+#pragma unroll
+            for (int q = 0; q < KB; ++q) acc[e][q] = CT(0);
+        constexpr int JU = 4;
+        for (int j0 = 0; j0 < mm; j0 += JU) {
+            int4 raw[JU];
+#pragma unroll
+            for (int t = 0; t < JU; ++t)
+                raw[t] = (j0 + t < mm) ? ld_stream(reinterpret_cast<const int4 *>(V + (size_t)(j0 + t) * a.npad + v * VW))
+                                       : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int t = 0; t < JU; ++t) {
+                if (j0 + t >= mm) break;
+                const ST *ue = reinterpret_cast<const ST *>(&raw[t]);
+                CT u[VW];
+#pragma unroll
+                for (int e = 0; e < VW; ++e) u[e] = cvt<CT>(ue[e]);
+                const CT *cj = coef + (j0 + t) * KB;
+#pragma unroll
+                for (int q = 0; q < KB; ++q) {
+                    const CT c = cj[q];
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) acc[e][q] += c * u[e];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+            if (k0 + q >= keep) break;
+            CT yq[VW];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) yq[e] = acc[e][q];
+            vstore_back<ST, CT>(Vs + (size_t)(k0 + q) * a.npad + v * VW, yq);  // rounded once
+#pragma unroll
+            for (int e = 0; e < VW; ++e) nrm[q] += yq[e] * yq[e];             // norm of what is stored
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+        const CT rr = warp_sum(nrm[q]);
+        if (lane == 0) part[wid][q] = rr;
+    }
+    __syncthreads();
+    if (tid < KB) {
+        CT rr = CT(0);
+#pragma unroll
+        for (int w8 = 0; w8 < kNT / 32; ++w8) rr += part[w8][tid];
+        a.slots[(size_t)blockIdx.x * KB + tid] = (double)rr;
+    }
+    if (arrive_last_n(a.counter + grp, (unsigned)nrblk, &sflag)) {
+        if (tid < KB && k0 + tid < keep) {
+            double rr = 0.0;
+            for (int b = 0; b < nrblk; ++b) rr += __ldcg(a.slots + ((size_t)b * ngroups + grp) * KB + tid);
+            a.ex.rst_part[(size_t)a.g * keep + k0 + tid] = rr;
+        }
+        __syncthreads();
+        if (tid == 0) a.counter[grp] = 0u;
+    }
+}
+
+// Restart bookkeeping: V[0..keep) <- the stored Ritz vectors, V[keep] <- u_{m+1}
+// (the cycle's last, unnormalised residual vector; its norm is still in the norm
+// partials, so the next SpMV prologue sets beta and s for it), s_j = 1/||y_j||
+// (norm partials summed over parts in rank order), the arrowhead size k.
+template <typename ST>
+__global__ void __launch_bounds__(kNT) k_restart_copy(RestartArgs a) {
+    if (*(volatile int *)a.st.done) return;
+    const int keep = a.keep;
+    if (blockIdx.x == 0 && threadIdx.x < keep) {
+        const int j = threadIdx.x;
+        double s = 0.0;
+        for (int q = 0; q < a.G; ++q) s += __ldcg(a.ex.rst_part + (size_t)q * keep + j);
+        a.st.scale[j] = 1.0 / sqrt(s);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.st.arrow_k = keep;
+        *a.st.m_found = keep;
+        *a.st.restarts += 1;
+    }
+    // 16-byte words (n_pad is a multiple of 64 rows)
+    const int64_t nw = a.npad * (int64_t)sizeof(ST) / 16;
+    const uint4 *Vs = reinterpret_cast<const uint4 *>(a.Vs);
+    uint4 *V = reinterpret_cast<uint4 *>(a.V);
+    const int64_t tot = nw * (keep + 1);
+    for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < tot; i += (int64_t)gridDim.x * kNT) {
+        const int64_t j = i / nw, w = i - j * nw;
+        V[j * nw + w] = (j < keep) ? Vs[j * nw + w] : V[(int64_t)a.mm * nw + w];
     }
 }
 

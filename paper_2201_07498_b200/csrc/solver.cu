@@ -95,6 +95,7 @@ struct Part {
     int64_t *sell = nullptr;
     int32_t *items = nullptr;
     void *yt = nullptr;            // Ritz output in position order, K values per row
+    void *Vs = nullptr;            // thick restart scratch: keep columns (reading Q26)
     double *long_parts = nullptr, *alpha_long = nullptr;
     unsigned *long_cnt = nullptr;
     void *V = nullptr, *y = nullptr, *w = nullptr;
@@ -118,6 +119,8 @@ struct topk_eig_s {
     int reorth = 1;
     double tau = 1e-12;
     double conv_tol = 0.0;   // reading Q25 (0: fixed m)
+    int keep = 0;            // reading Q26: Ritz pairs kept per thick restart (0: off)
+    int max_restarts = 0;
     int conv_check = 0;      // check period c
     int conv_checks = 0;     // checks enqueued per solve
     int use_graph = 1;
@@ -310,8 +313,9 @@ static void stepw_grids(topk_eig_s *h) {
 }
 
 template <typename ST, typename CT>
-static void launch_step(topk_eig_s *h, Part &p, int it, int mode) {
+static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 0) {
     StepArgs a;
+    a.no_prev = no_prev;
     a.y = p.y; a.w = p.w; a.V = p.V;
     a.vout = (char *)p.V + (size_t)it * p.npad * sizeof(ST);
     a.rep_slot = (mode == 1) ? rep_slot(h, p) : nullptr;
@@ -361,6 +365,44 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
     h->launches++;
 }
 
+// thick restart (reading Q26): Jacobi on the cycle's T (convergence test + the
+// kept pairs), projection of the kept Ritz vectors, norm exchange, basis rewrite
+static void exch_rst(topk_eig_s *h) {
+    if (!h->comm) return;
+    NCCL_TRY(ncclAllGather(h->ex.rst_part + (size_t)h->rank * h->keep, h->ex.rst_part, h->keep, ncclFloat64,
+                           h->comm, h->stream));
+}
+template <typename ST, typename CT>
+static void launch_restart(topk_eig_s *h) {
+    launch_jacobi(h, 2);
+    const int ng = (h->keep + kRitzKB - 1) / kRitzKB;
+    for (Part &p : h->parts) {
+        RestartArgs a;
+        a.V = p.V; a.Vs = p.Vs; a.npad = p.npad; a.keep = h->keep; a.G = h->G; a.g = p.g; a.mm = h->m;
+        a.slots = p.slots; a.counter = p.counters + 8;
+        a.st = p.st; a.ex = h->ex;
+        const int nrb = std::max(1, h->grid_ritz / ng);
+        const size_t smem = (size_t)h->m * kRitzKB * sizeof(CT);
+        prof_begin(h, p, 5);
+        k_restart_proj<ST, CT, kRitzKB><<<nrb * ng, kNT, smem, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+    exch_rst(h);
+    for (Part &p : h->parts) {
+        RestartArgs a;
+        a.V = p.V; a.Vs = p.Vs; a.npad = p.npad; a.keep = h->keep; a.G = h->G; a.g = p.g; a.mm = h->m;
+        a.slots = p.slots; a.counter = p.counters + 8;
+        a.st = p.st; a.ex = h->ex;
+        prof_begin(h, p, 5);
+        k_restart_copy<ST><<<h->grid_stream, kNT, 0, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        prof_end(h, p);
+        h->launches++;
+    }
+}
+
 template <typename VT, typename ST, typename CT>
 static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // a5: v1
@@ -378,7 +420,12 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
         h->launches++;
     }
     exch_vec_norm(h);
-    for (int it = 1; it <= h->m; ++it) {
+    // cycles: the paper's fixed m iterations (cycle 0 only), or thick-restart cycles
+    // (reading Q26): restart after cycles 0 .. R-1, then steps keep+1 .. m again
+    const int R = h->keep > 0 ? h->max_restarts : 0;
+    for (int cyc = 0; cyc <= R; ++cyc) {
+    const int it0 = (cyc == 0) ? 1 : h->keep + 1;
+    for (int it = it0; it <= h->m; ++it) {
         for (Part &p : h->parts) launch_spmv<VT, ST, CT>(h, p, it, nullptr);
         exch_alpha(h);
         if (h->reorth < 0) {
@@ -386,7 +433,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             exch_vec_norm(h);
             continue;
         }
-        for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 0);
+        for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 0, (cyc > 0 && it == it0) ? 1 : 0);
         exch_h(h);
         for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, -1);
         if (h->reorth == 2) {
@@ -396,9 +443,11 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it);
         }
         exch_vec_norm(h);
-        if (h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0) {
+        if (h->keep == 0 && h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0) {
             launch_jacobi(h, 1);  // reading Q25: may set done = 2 (later launches return at once)
         }
+    }
+    if (cyc < R) launch_restart<ST, CT>(h);
     }
     // a12-a13: Jacobi (redundant on every part, identical inputs)
     launch_jacobi(h, 0);
@@ -469,7 +518,7 @@ static void set_kernels(topk_eig_s *h) {
         const char *e = std::getenv("TOPK_NO_TMA");
         h->use_tma = !(e && e[0] == '1');
         // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed
-        h->use_gram = h->reorth != -1;
+        h->use_gram = h->reorth != -1 && h->keep == 0;  // restarts replace basis columns: explicit norm pass
         const char *e2 = std::getenv("TOPK_TMA_CORRECT");
         h->tma_correct = e2 && e2[0] == '1';
         const char *e3 = std::getenv("TOPK_TMA_STEP");
@@ -479,6 +528,8 @@ static void set_kernels(topk_eig_s *h) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);
     h->grid_ritz = h->nsm * std::max(1, std::min(occ3, 2));
     CUDA_TRY(cudaFuncSetAttribute(k_correct<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(k_restart_proj<ST, CT, kRitzKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(1024 * kRitzKB * sizeof(double))));
     CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(1024 * kRitzKB * sizeof(double))));
     CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -516,6 +567,8 @@ static void carve_state(topk_eig_s *h, Part &p) {
     p.st.k_found = ints + 2;
     p.st.jac_sweeps = ints + 3;
     p.st.jac_conv = ints + 4;
+    p.st.arrow_k = ints + 5;
+    p.st.restarts = ints + 6;
     p.st.tscale = reinterpret_cast<double *>(b + o_ts);
     p.st.alpha = reinterpret_cast<double *>(b + o_alpha);
     p.st.beta = reinterpret_cast<double *>(b + o_beta);
@@ -530,6 +583,11 @@ static void carve_state(topk_eig_s *h, Part &p) {
     p.st.rnrm2 = h->alloc<double>((size_t)K);
     p.st.m = m;
     p.st.use_gram = h->use_gram ? 1 : 0;
+    // thick restart (reading Q26): arrowhead part of T and the kept Ritz coefficients
+    p.st.keep = h->keep;
+    p.st.arrow_theta = h->alloc<double>((size_t)std::max(h->keep, 1));
+    p.st.arrow_b = h->alloc<double>((size_t)std::max(h->keep, 1));
+    p.st.coefR = h->alloc<double>((size_t)m * std::max(h->keep, 1));
 }
 
 template <typename T> static T hget(const Part &p, const void *devptr) {
@@ -603,6 +661,14 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (compute == TOPK_F32 && storage == TOPK_F64) return fail(TOPK_E_INVALID, "compute must be at least as precise as storage");
     if (!(o.conv_tol >= 0.0) || o.conv_check < 0) return fail(TOPK_E_INVALID, "conv_tol must be >= 0 and conv_check >= 0");
     h->conv_tol = o.conv_tol;
+    if (o.restart_keep < 0 || o.max_restarts < 0) return fail(TOPK_E_INVALID, "restart_keep and max_restarts must be >= 0");
+    if (o.restart_keep > 0) {
+        if (o.restart_keep < K || o.restart_keep > m - 2 || o.restart_keep > 256)
+            return fail(TOPK_E_INVALID, "restart_keep must be in [K, min(krylov_dim - 2, 256)]");
+        if (h->reorth < 0) return fail(TOPK_E_INVALID, "thick restart needs reorthogonalisation (reorth 1 or 2)");
+        h->keep = o.restart_keep;
+        h->max_restarts = o.max_restarts;
+    }
     h->conv_check = o.conv_check > 0 ? o.conv_check : K;
     if (h->conv_tol > 0.0)
         for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
@@ -650,6 +716,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->ex.norm_part = h->alloc<double>((size_t)G);
         h->ex.hpart = h->alloc<double>((size_t)G * 2 * (m + 1));
         h->ex.ritz_part = h->alloc<double>((size_t)G * K);
+        h->ex.rst_part = h->alloc<double>((size_t)G * std::max(h->keep, 1));
 
         if (G > 1) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
         h->ex.replica = h->replica;
@@ -765,6 +832,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
             p.y = h->alloc<char>((size_t)npad * vsz);
             p.w = h->alloc<char>((size_t)npad * vsz);
+            if (h->keep > 0) p.Vs = h->alloc<char>((size_t)h->keep * npad * vsz);
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
             p.yt = h->alloc<double>((size_t)((K + kRitzKB - 1) / kRitzKB) * kRitzKB * std::max<int64_t>(p.npad, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
@@ -856,6 +924,10 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     info->iterations = hget<int>(p, p.st.m_found);
     info->k_found = hget<int>(p, p.st.k_found);
     const int done = hget<int>(p, p.st.done);
+    const int nrst = hget<int>(p, p.st.restarts);
+    info->restarts = nrst;
+    if (nrst > 0)  // total Lanczos steps over the thick-restart cycles (reading Q26)
+        info->iterations = h->m + (nrst - 1) * (h->m - h->keep) + (info->iterations - h->keep);
     info->breakdown = done == 1;
     info->converged_stop = done == 2;
     info->conv_checks = h->conv_checks;

@@ -94,6 +94,12 @@ def test_create_argument_errors_precede_device():
     with pytest.raises(T.TopkError) as e:
         T.TopkEig(asym, 1, "f64", "f64")
     assert e.value.status == 3
+    # thick restart / adaptive options (readings Q25, Q26)
+    for kw in (dict(m=20, restart_keep=3), dict(m=20, restart_keep=19), dict(m=20, restart_keep=8, reorth=-1),
+               dict(m=20, restart_keep=-1), dict(m=20, max_restarts=-2), dict(m=20, conv_tol=-1.0)):
+        with pytest.raises(T.TopkError) as e:
+            T.TopkEig(A, 4, "f64", "f64", **kw)
+        assert e.value.status == 1, kw
 
 
 # ---------------------------------------------------------------- host layout (no device)

@@ -440,3 +440,40 @@ def test_p11_adaptive_stop_kahan_and_minimal():
     r2 = O.solve_adaptive(A.rowptr, A.col, A.val, K, m_max=24, tol=1e-300, check=c, seed=2,
                           want_vectors=False)
     assert r2.lanczos.m_found == 24 and not r2.extra["converged_stop"]
+
+
+# ---------------------------------------------------------------- P12 (thick restart)
+def test_p12_thick_restart_relation_and_convergence():
+    """solve_thick_restart (reading Q26): after restarts the basis stays
+    orthonormal and the Lanczos relation A V_m = V_m T_m + beta v_{m+1} e_m^T
+    holds with the arrowhead T (a wrong coupling b_j, sign or index breaks it);
+    run to convergence, the K pairs match dense eigvalsh (brute force) and obey
+    the Kahan bound; zero restarts is the plain solve."""
+    A = S.rmat(11, 12_000, 5)
+    n = A.n
+    D = dense(n, A.rowptr, A.col, A.val)
+    lam = np.linalg.eigvalsh(D)
+    lam_top = lam[np.argsort(-np.abs(lam))]
+    nrmA = np.abs(lam).max()
+    K, m, keep = 6, 24, 12
+    r = O.solve_thick_restart(A.rowptr, A.col, A.val, K, m, keep, max_restarts=3, seed=2)
+    assert r.extra["restarts"] == 3 and r.extra["iterations"] == m + 3 * (m - keep)
+    Vm, Tm, vn = r.lanczos.V, r.extra["T"], r.extra["v_next"]
+    assert np.abs(Vm @ Vm.T - np.eye(m)).max() <= 1e-12
+    assert abs(np.dot(Vm[0], vn)) <= 1e-12 and abs(np.linalg.norm(vn) - 1) <= 1e-12
+    R = (D @ Vm.T) - Vm.T @ Tm
+    R[:, m - 1] -= r.lanczos.beta[m] * vn
+    assert np.abs(R).max() <= 1e-11 * nrmA
+    assert np.count_nonzero(np.abs(Tm[:keep, :keep] - np.diag(np.diag(Tm[:keep, :keep]))) > 0) == 0
+    # converged run
+    rc = O.solve_thick_restart(A.rowptr, A.col, A.val, K, m, keep, max_restarts=50, tol=1e-10, seed=2)
+    assert rc.extra["restarts"] < 50
+    assert np.allclose(rc.eigenvalues, lam_top[:K], rtol=0, atol=1e-8 * nrmA)
+    for kk in range(K):
+        y = rc.eigenvectors[kk]
+        true = np.linalg.norm(D @ y - rc.eigenvalues[kk] * y)
+        assert np.min(np.abs(lam - rc.eigenvalues[kk])) <= true + 1e-12 * nrmA
+    # no restart = the plain solve
+    r0 = O.solve_thick_restart(A.rowptr, A.col, A.val, K, m, keep, max_restarts=0, seed=2)
+    p = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=2)
+    assert np.allclose(np.sort(r0.theta_all), np.sort(p.theta_all), rtol=0, atol=1e-12 * nrmA)
