@@ -199,6 +199,12 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
                                    int32_t *col, double *val, int32_t *perm, int32_t *pcol, double *pval,
                                    int64_t *chunks, int64_t *sell, int32_t *items);
 
+/* Memory runtime (mem_pool.h): device blocks freed by topk_eig_destroy are cached
+ * per device and reused by later handles (no cudaMalloc/cudaFree on the create/
+ * destroy path after the first handle). Returns every cached, unused block to the
+ * driver; returns the bytes released. Thread-safe; live handles are unaffected. */
+size_t topk_eig_trim_pool(void);
+
 /* Per kernel class device time of the last solve (requires opts.profile = 1):
  * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz pass 0 (norms), 6 ritz pass 1 (output),
  * 7 unpermute (output back to the original row order).

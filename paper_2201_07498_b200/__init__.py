@@ -76,6 +76,7 @@ _SIGS = {
     "topk_eig_stream": (_P, [_P]),
     "topk_eig_kernel_times": (_S, [_P, _P, _P]),
     "topk_eig_destroy": (None, [_P]),
+    "topk_eig_trim_pool": (ctypes.c_size_t, []),
     "topk_eig_last_error": (ctypes.c_char_p, []),
     "topk_eig_nccl_id": (_S, [_P]),
     "topk_eig_plan_partition": (_S, [_P, _I64, _I32, _P]),
@@ -105,6 +106,11 @@ def nccl_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.topk_eig_nccl_id(buf))
     return buf.raw
+
+
+def trim_pool() -> int:
+    """Return the library's cached device blocks to the driver (topk_eig_trim_pool)."""
+    return int(_lib.topk_eig_trim_pool())
 
 
 def plan_partition(rowptr, G: int) -> np.ndarray:

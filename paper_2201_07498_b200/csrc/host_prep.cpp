@@ -2,6 +2,9 @@
 // the input (COO as in the paper's Table I, or CSR), check
 // symmetry, partition rows by nnz, and lay out each partition
 // for the device (rows of M_g, replicated v_i).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "host_prep.h"
 
 #include <algorithm>
@@ -14,6 +17,17 @@
 #endif
 
 namespace topk {
+
+// TOPK_TRACE=1: host-preparation sub-stage times on stderr
+static void hp_mark(const char *what) {
+    static const bool on = [] { const char *e = std::getenv("TOPK_TRACE"); return e && e[0] == '1'; }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  [host_prep] %-26s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+}
+
 
 static double load_value(const topk_matrix_t &A, int64_t k) {
     if (!A.values) return 1.0;
@@ -76,13 +90,15 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
                 if (A.col_idx[k] <= A.col_idx[k - 1]) { unsorted = 1; break; }
         if (!unsorted) {
             out.n = n;
-            out.rowptr.assign(A.row_ptr, A.row_ptr + n + 1);
-            out.col.resize((size_t)nnz);
-            out.val.resize((size_t)nnz);
+            out.rowptr = {A.row_ptr, (size_t)n + 1};
+            out.col = {A.col_idx, (size_t)nnz};
+            if (A.values && A.values_dtype == TOPK_F64) {
+                out.val = {static_cast<const double *>(A.values), (size_t)nnz};  // borrowed, no copy
+            } else {
+                out.val_own.resize((size_t)nnz);
 #pragma omp parallel for schedule(static)
-            for (int64_t k = 0; k < nnz; ++k) {
-                out.col[(size_t)k] = A.col_idx[k];
-                out.val[(size_t)k] = load_value(A, k);
+                for (int64_t k = 0; k < nnz; ++k) out.val_own[(size_t)k] = load_value(A, k);
+                out.val = {out.val_own.data(), out.val_own.size()};
             }
             return TOPK_OK;
         }
@@ -120,8 +136,8 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
     // Per row: stable sort by column, sum duplicates; then compact.
     std::vector<int64_t> cnt((size_t)n, 0);
     out.n = n;
-    out.col.resize((size_t)nnz);
-    out.val.resize((size_t)nnz);
+    out.col_own.resize((size_t)nnz);
+    out.val_own.resize((size_t)nnz);
 #pragma omp parallel
     {
         std::vector<int64_t> perm;
@@ -129,22 +145,23 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
         for (int64_t r = 0; r < n; ++r) {
             int64_t b = start[(size_t)r], len = start[(size_t)r + 1] - b;
             cnt[(size_t)r] = sort_row_sum(gcol.data() + b, gval.data() + b, len,
-                                          out.col.data() + b, out.val.data() + b, perm);
+                                          out.col_own.data() + b, out.val_own.data() + b, perm);
         }
     }
-    out.rowptr.assign((size_t)n + 1, 0);
-    for (int64_t r = 0; r < n; ++r) out.rowptr[(size_t)r + 1] = out.rowptr[(size_t)r] + cnt[(size_t)r];
-    if (out.rowptr[(size_t)n] != nnz) {  // duplicates were merged: compact in place
+    out.rowptr_own.assign((size_t)n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) out.rowptr_own[(size_t)r + 1] = out.rowptr_own[(size_t)r] + cnt[(size_t)r];
+    if (out.rowptr_own[(size_t)n] != nnz) {  // duplicates were merged: compact in place
         for (int64_t r = 0; r < n; ++r) {
-            int64_t src = start[(size_t)r], dst = out.rowptr[(size_t)r];
+            int64_t src = start[(size_t)r], dst = out.rowptr_own[(size_t)r];
             if (src != dst) {
-                std::memmove(out.col.data() + dst, out.col.data() + src, (size_t)cnt[(size_t)r] * sizeof(int32_t));
-                std::memmove(out.val.data() + dst, out.val.data() + src, (size_t)cnt[(size_t)r] * sizeof(double));
+                std::memmove(out.col_own.data() + dst, out.col_own.data() + src, (size_t)cnt[(size_t)r] * sizeof(int32_t));
+                std::memmove(out.val_own.data() + dst, out.val_own.data() + src, (size_t)cnt[(size_t)r] * sizeof(double));
             }
         }
-        out.col.resize((size_t)out.rowptr[(size_t)n]);
-        out.val.resize((size_t)out.rowptr[(size_t)n]);
+        out.col_own.resize((size_t)out.rowptr_own[(size_t)n]);
+        out.val_own.resize((size_t)out.rowptr_own[(size_t)n]);
     }
+    out.bind_owned();
     return TOPK_OK;
 }
 
@@ -265,10 +282,11 @@ std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t 
     return cm;
 }
 
-topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
-                         const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
+topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
+                                const int32_t *pos, PartLayout &out, std::string &err) {
     const int64_t r0 = b[g], r1 = b[g + 1];
     const int64_t z0 = m.rowptr[(size_t)r0], z1 = m.rowptr[(size_t)r1];
+    hp_mark("build_part: start");
     (void)z0; (void)z1;  // any per-part nnz (64-bit offsets)
     if ((int64_t)G * npad >= (1ll << 31)) { err = "G * n_pad must be < 2^31"; return TOPK_E_INVALID; }
     (void)G;
@@ -276,18 +294,23 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
     out.nrows = r1 - r0;
     out.npad = npad;
     const int64_t ng = r1 - r0;
-    out.perm.assign((size_t)ng, 0);
+    out.perm.resize((size_t)ng);
+#pragma omp parallel for schedule(static)
     for (int64_t r = r0; r < r1; ++r) out.perm[(size_t)pos[(size_t)r]] = (int32_t)(r - r0);
     out.rowptr.resize((size_t)(ng + 1));
     out.rowptr[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < ng; ++p) {  // row lengths in degree order (random reads, parallel)
+        const int64_t r = r0 + out.perm[(size_t)p];
+        out.rowptr[(size_t)p + 1] = m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r];
+    }
     int64_t nne = 0;
     for (int64_t p = 0; p < ng; ++p) {
-        const int64_t r = r0 + out.perm[(size_t)p];
-        const int64_t len = m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r];
-        out.rowptr[(size_t)p + 1] = out.rowptr[(size_t)p] + len;
-        if (len > 0) nne = p + 1;
+        if (out.rowptr[(size_t)p + 1] > 0) nne = p + 1;
+        out.rowptr[(size_t)p + 1] += out.rowptr[(size_t)p];
     }
     out.nnonempty = nne;
+    hp_mark("perm + rowptr");
     // physical format: big rows (CSR prefix, chunked), then SELL-32 slices
     int64_t nbig = 0;
     while (nbig < nne && out.rowptr[(size_t)nbig + 1] - out.rowptr[(size_t)nbig] > kSellMaxLen) ++nbig;
@@ -314,6 +337,29 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
         out.sell[(size_t)(2 * sl + 1)] = w;
         phys += 32 * w;
     }
+    out.items.clear();
+    for (int64_t sl = 0; sl < nsl;) {
+        int64_t e = sl, width = 0;
+        while (e < nsl && (e == sl || width + out.sell[(size_t)(2 * e + 1)] <= kSellItemWidth)) {
+            width += out.sell[(size_t)(2 * e + 1)];
+            ++e;
+        }
+        out.items.push_back((int32_t)sl);
+        out.items.push_back((int32_t)e);
+        sl = e;
+    }
+    out.nphys = phys;
+    hp_mark("chunks + slices + items");
+    return TOPK_OK;
+}
+
+topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
+                         const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
+    topk_status_t s = build_part_tables(m, b, G, g, npad, pos, out, err);
+    if (s != TOPK_OK) return s;
+    const int64_t r0 = b[g];
+    const int64_t nne = out.nnonempty, nbig = out.nbig, phys = out.nphys;
+    const int64_t nsl = (int64_t)out.sell.size() / 2;
     out.pcol.resize((size_t)phys);
     out.pval.resize((size_t)phys);
     // every entry straight from the canonical CSR to its physical slot (rows in
@@ -336,6 +382,7 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
             out.pval[dst] = m.val[(size_t)(kb + e)];
         }
     }
+    hp_mark("scatter");
     // SELL padding: (column 0, value 0) past each row's length
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t sl = 0; sl < nsl; ++sl) {
@@ -349,17 +396,7 @@ topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, i
             }
         }
     }
-    out.items.clear();
-    for (int64_t sl = 0; sl < nsl;) {
-        int64_t e = sl, width = 0;
-        while (e < nsl && (e == sl || width + out.sell[(size_t)(2 * e + 1)] <= kSellItemWidth)) {
-            width += out.sell[(size_t)(2 * e + 1)];
-            ++e;
-        }
-        out.items.push_back((int32_t)sl);
-        out.items.push_back((int32_t)e);
-        sl = e;
-    }
+    hp_mark("padding");
     return TOPK_OK;
 }
 

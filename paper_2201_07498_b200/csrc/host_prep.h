@@ -23,11 +23,34 @@ template <class T> struct NoInitAlloc : std::allocator<T> {
 };
 template <class T> using hvec = std::vector<T, NoInitAlloc<T>>;
 
+// Read-only view of a host array (borrowed from the caller's matrix, or of the
+// Csr's own storage).
+template <class T> struct Span {
+    const T *p = nullptr;
+    size_t n = 0;
+    const T &operator[](size_t i) const { return p[i]; }
+    const T *data() const { return p; }
+    size_t size() const { return n; }
+    bool empty() const { return n == 0; }
+    const T &back() const { return p[n - 1]; }
+};
+
+// Canonical CSR. A CSR input that is already canonical with fp64 values is
+// borrowed as is (no copy: the caller's arrays stay valid during create); any
+// other input is rebuilt into the owned storage.
 struct Csr {
     int64_t n = 0;
-    std::vector<int64_t> rowptr;  // n+1
-    hvec<int32_t> col;            // nnz, sorted strictly increasing within each row
-    hvec<double> val;             // nnz
+    Span<int64_t> rowptr;  // n+1
+    Span<int32_t> col;     // nnz, sorted strictly increasing within each row
+    Span<double> val;      // nnz
+    std::vector<int64_t> rowptr_own;
+    hvec<int32_t> col_own;
+    hvec<double> val_own;
+    void bind_owned() {
+        rowptr = {rowptr_own.data(), rowptr_own.size()};
+        col = {col_own.data(), col_own.size()};
+        val = {val_own.data(), val_own.size()};
+    }
     int64_t nnz() const { return rowptr.empty() ? 0 : rowptr.back(); }
 };
 
@@ -102,6 +125,7 @@ struct PartLayout {
     std::vector<int32_t> perm;      // nrows: part-local original row at each position
     // physical SpMV format
     int32_t nbig = 0;
+    int64_t nphys = 0;              // physical entries (big-row CSR + padded SELL)
     hvec<int32_t> pcol;             // physical col (big-row CSR prefix, then SELL slices)
     hvec<double> pval;              // physical values
     std::vector<Chunk> chunks;
@@ -112,6 +136,11 @@ struct PartLayout {
 
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err);
+// The same layout without the physical arrays (perm, rowptr, chunks, long rows,
+// SELL table, items, nphys): topk_eig_create scatters the nonzeros on the device
+// (k_layout_big / k_layout_sell) with exactly the host rule of build_part.
+topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
+                                const int32_t *pos, PartLayout &out, std::string &err);
 
 // The logical CSR (degree order; device column entries, values) read back out of
 // the physical arrays (exports and tests).

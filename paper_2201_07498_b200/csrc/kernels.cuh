@@ -1717,6 +1717,56 @@ __global__ void __launch_bounds__(kNT) k_restart_copy(RestartArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// a4 on the device: the physical SpMV arrays from the part's canonical CSR slice
+// (uploaded as is, values already rounded to the value storage dtype), with the
+// host rule of build_part (host_prep.cpp): position p holds original part row
+// perm[p]; entry e of a big row goes to rowptr_deg[p] + e, entry e of SELL slice
+// row i to base + 32 e + i, padding (column 0, value 0); columns through colmap.
+template <typename VT>
+__global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const int32_t *scol, const VT *sval,
+                                                    const int32_t *perm, const int64_t *drp, const int32_t *colmap,
+                                                    int nbig, int32_t *pcol, VT *pval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = w; p < nbig; p += nw) {
+        const int r = perm[p];
+        const int64_t k0 = srp[r], len = srp[r + 1] - k0, d0 = drp[p];
+        for (int64_t e = lane; e < len; e += 32) {
+            pcol[d0 + e] = colmap[scol[k0 + e]];
+            pval[d0 + e] = sval[k0 + e];
+        }
+    }
+}
+
+template <typename VT>
+__global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const int32_t *scol, const VT *sval,
+                                                     const int32_t *perm, const int64_t *drp, const int32_t *colmap,
+                                                     const longlong2 *sell, int64_t nbig, int64_t nne, int64_t nsl,
+                                                     int32_t *pcol, VT *pval) {
+    const int64_t tot = 32 * nsl;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sl = i >> 5, lane = i & 31, p = nbig + i;
+        const longlong2 S = sell[sl];
+        int64_t len = 0, k0 = 0;
+        if (p < nne) {
+            len = drp[p + 1] - drp[p];
+            k0 = srp[perm[p]];
+        }
+        for (int64_t e = 0; e < S.y; ++e) {
+            const int64_t d = S.x + 32 * e + lane;
+            if (e < len) {
+                pcol[d] = colmap[scol[k0 + e]];
+                pval[d] = sval[k0 + e];
+            } else {
+                pcol[d] = 0;
+                pval[d] = VT(0);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // a15: eigenvectors back to the original row order: out[k][r] = yt[inv[r]][k]
 // (the caller's K x n_local buffer, vector k contiguous).
 struct UnpermArgs {

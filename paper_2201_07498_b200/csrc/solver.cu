@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "host_prep.h"
+#include "mem_pool.h"
 #include "kernels.cuh"
 #include "topk_eig.h"
 
@@ -136,7 +137,9 @@ struct topk_eig_s {
     Exch ex{};
     char *exch_block = nullptr;
     void *replica = nullptr;
-    SolveParams *dparams = nullptr, *hparams = nullptr;
+    SolveParams *dparams = nullptr, *hparams = nullptr;  // hparams: pageable (a pinned block's free
+                                                          // measured up to 380 ms on destroy)
+    std::vector<SolveParams> hparams_own;
     double *jac_work = nullptr;
     size_t jac_smem = 0, jac_bytes = 0;
     int jac_ld_log2 = 0, jac_hl_log2 = 0;
@@ -160,9 +163,9 @@ struct topk_eig_s {
     std::vector<void *> allocs;
 
     template <typename T> T *alloc(size_t count) {
-        void *p = nullptr;
         size_t bytes = std::max<size_t>(count * sizeof(T), 256);
-        CUDA_TRY(cudaMalloc(&p, bytes));
+        void *p = pool_dev_alloc(bytes);  // caching allocator (mem_pool.h)
+        if (!p) CUDA_TRY(cudaErrorMemoryAllocation);
         allocs.push_back(p);
         CUDA_TRY(cudaMemsetAsync(p, 0, bytes, stream));
         return reinterpret_cast<T *>(p);
@@ -599,22 +602,73 @@ static const double *hptr(const Part &p, const double *devptr) {
     return reinterpret_cast<const double *>(p.hstate.data() + ((const char *)devptr - p.state));
 }
 
-static void upload_values(topk_eig_s *h, Part &p, const PartLayout &L) {
-    const size_t z = L.pval.size();
-    if (z == 0) return;
-    if (h->ms == TOPK_F64) {
-        CUDA_TRY(cudaMemcpy(p.val, L.pval.data(), z * 8, cudaMemcpyHostToDevice));
-    } else if (h->ms == TOPK_F32) {
-        hvec<float> t(z);
+// a4 on the device: the part's canonical CSR slice goes up as is (values rounded to
+// the value storage dtype on the way, RNE straight from f64, reading Q22, converted
+// chunk by chunk into the pinned staging buffers, mem_pool.h), then k_layout_big /
+// k_layout_sell scatter it into the physical SpMV arrays (the rule of build_part).
+template <typename VT>
+static void device_layout_t(topk_eig_s *h, Part &p, const Csr &csr, const PartLayout &L, const int32_t *d_colmap) {
+    const int64_t r0 = L.row0, ng = L.nrows;
+    const int64_t z0 = csr.rowptr[(size_t)r0], z = csr.rowptr[(size_t)(r0 + ng)] - z0;
+    const size_t es = sizeof(VT);
+    auto dalloc = [&](size_t bytes) {
+        void *q = pool_dev_alloc(std::max<size_t>(bytes, 256));
+        if (!q) CUDA_TRY(cudaErrorMemoryAllocation);
+        return q;
+    };
+    int64_t *d_srp = static_cast<int64_t *>(dalloc((size_t)(ng + 1) * 8));
+    int64_t *d_drp = static_cast<int64_t *>(dalloc((size_t)(ng + 1) * 8));
+    int32_t *d_scol = static_cast<int32_t *>(dalloc((size_t)z * 4));
+    VT *d_sval = static_cast<VT *>(dalloc((size_t)z * es));
+    const int64_t *srp = csr.rowptr.data() + r0;
+    auto fill_srp = [&](char *dst, size_t off, size_t nb) {
+        const size_t i0 = off / 8, cnt = nb / 8;
+        int64_t *d = reinterpret_cast<int64_t *>(dst);
 #pragma omp parallel for schedule(static)
-        for (size_t k = 0; k < z; ++k) t[k] = round_f32(L.pval[k]);
-        CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 4, cudaMemcpyHostToDevice));
-    } else {
-        hvec<uint16_t> t(z);
+        for (size_t i = 0; i < cnt; ++i) d[i] = srp[i0 + i] - z0;
+    };
+    CUDA_TRY(staged_h2d(d_srp, (size_t)(ng + 1) * 8, fill_srp, h->stream));
+    const char *drp = reinterpret_cast<const char *>(L.rowptr.data());
+    CUDA_TRY(staged_h2d(d_drp, (size_t)(ng + 1) * 8, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, drp + off, nb); },
+                        h->stream));
+    const char *sc = reinterpret_cast<const char *>(csr.col.data() + z0);
+    CUDA_TRY(staged_h2d(d_scol, (size_t)z * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, sc + off, nb); },
+                        h->stream));
+    const double *sv = csr.val.data() + z0;
+    const topk_dtype_t ms = h->ms;
+    auto fill_val = [&](char *dst, size_t off, size_t nb) {
+        const size_t k0 = off / es, cnt = nb / es;
 #pragma omp parallel for schedule(static)
-        for (size_t k = 0; k < z; ++k) t[k] = round_bf16_bits(L.pval[k]);
-        CUDA_TRY(cudaMemcpy(p.val, t.data(), z * 2, cudaMemcpyHostToDevice));
+        for (size_t k = 0; k < cnt; ++k) {
+            const double x = sv[k0 + k];
+            if (ms == TOPK_F64) reinterpret_cast<double *>(dst)[k] = x;
+            else if (ms == TOPK_F32) reinterpret_cast<float *>(dst)[k] = round_f32(x);
+            else reinterpret_cast<uint16_t *>(dst)[k] = round_bf16_bits(x);
+        }
+    };
+    CUDA_TRY(staged_h2d(d_sval, (size_t)z * es, fill_val, h->stream));
+    if (L.nbig > 0) {
+        k_layout_big<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d_srp, d_scol, d_sval, p.perm, d_drp, d_colmap, L.nbig,
+                                                           p.col, reinterpret_cast<VT *>(p.val));
+        CUDA_TRY(cudaGetLastError());
     }
+    const int64_t nsl = (int64_t)L.sell.size() / 2;
+    if (nsl > 0) {
+        k_layout_sell<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d_srp, d_scol, d_sval, p.perm, d_drp, d_colmap,
+                                                            reinterpret_cast<const longlong2 *>(p.sell), (int64_t)L.nbig,
+                                                            L.nnonempty, nsl, p.col, reinterpret_cast<VT *>(p.val));
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    pool_dev_free(d_srp);
+    pool_dev_free(d_drp);
+    pool_dev_free(d_scol);
+    pool_dev_free(d_sval);
+}
+static void device_layout(topk_eig_s *h, Part &p, const Csr &csr, const PartLayout &L, const int32_t *d_colmap) {
+    if (h->ms == TOPK_F64) device_layout_t<double>(h, p, csr, L, d_colmap);
+    else if (h->ms == TOPK_F32) device_layout_t<float>(h, p, csr, L, d_colmap);
+    else device_layout_t<uint16_t>(h, p, csr, L, d_colmap);
 }
 
 static int64_t model_bytes(topk_eig_s *h, const Part &p) {
@@ -701,15 +755,18 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (h->device < 0 || h->device >= ndev) return fail(TOPK_E_INVALID, "bad device ordinal");
     try {
         CUDA_TRY(cudaSetDevice(h->device));
-        cudaDeviceProp prop;
-        CUDA_TRY(cudaGetDeviceProperties(&prop, h->device));
-        if (prop.major != 10 || prop.minor != 0)
+        int major = 0, minor = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
+        CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, h->device));
+        if (major != 10 || minor != 0)
             return fail(TOPK_E_NODEVICE, "device is not sm_100 (B200); this library is built for sm_100a only");
-        h->nsm = prop.multiProcessorCount;
+        CUDA_TRY(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
         CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreate(&h->ev0));
         CUDA_TRY(cudaEventCreate(&h->ev1));
+        clk.mark("device init");
         if (!select_kernels(h.get())) return fail(TOPK_E_INVALID, "unsupported (values, storage, compute) dtype combination");
+        clk.mark("kernel attributes");
 
         // exchange buffers (shared by the local parts)
         h->ex.alpha_part = h->alloc<double>((size_t)G);
@@ -722,8 +779,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->ex.replica = h->replica;
         const int nlocal = (world > 1) ? 1 : G;
         h->dparams = h->alloc<SolveParams>(1 + (size_t)nlocal);
-        CUDA_TRY(cudaMallocHost(&h->hparams, sizeof(SolveParams) * (1 + nlocal)));
-        std::memset(h->hparams, 0, sizeof(SolveParams) * (1 + nlocal));
+        h->hparams_own.assign((size_t)(1 + nlocal), SolveParams{});
+        h->hparams = h->hparams_own.data();
         // Jacobi workspace: T and S with a power-of-two leading dimension, + rotations
         const int M = m + (m & 1);
         int ls = 0, hs = 0;
@@ -787,21 +844,29 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             }
         }
 
+        // column map (global column -> device column entry), shared by the local parts
+        int32_t *d_colmap = static_cast<int32_t *>(pool_dev_alloc((size_t)n * 4));
+        if (!d_colmap) CUDA_TRY(cudaErrorMemoryAllocation);
+        {
+            const char *cm = reinterpret_cast<const char *>(colmap.data());
+            CUDA_TRY(staged_h2d(d_colmap, (size_t)n * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },
+                                h->stream));
+        }
         h->parts.resize((size_t)nlocal);
         for (int lp = 0; lp < nlocal; ++lp) {
             Part &p = h->parts[(size_t)lp];
             p.g = (world > 1) ? h->rank : lp;
             PartLayout L;
-            s = build_part(csr, h->bounds.data(), G, p.g, npad, pos.data(), colmap.data(), L, err);
+            s = build_part_tables(csr, h->bounds.data(), G, p.g, npad, pos.data(), L, err);
             if (s != TOPK_OK) return fail(s, err);
-            clk.mark("build_part");
+            clk.mark("layout tables");
             p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.rowptr.back();
             p.nchunks = (int)L.chunks.size(); p.nlong = (int)L.longrows.size();
             p.nitems = (int)L.items.size() / 2; p.nbig = L.nbig; p.nnonempty = L.nnonempty;
-            p.nphys = (int64_t)L.pcol.size();
+            p.nphys = L.nphys;
             // physical col/val padded by 128 entries
-            p.col = h->alloc<int32_t>(L.pcol.size() + 128);
-            p.val = h->alloc<char>((L.pval.size() + 128) * dsize(ms));
+            p.col = h->alloc<int32_t>((size_t)L.nphys + 128);
+            p.val = h->alloc<char>(((size_t)L.nphys + 128) * dsize(ms));
             p.h_rowptr = L.rowptr;
             p.h_perm = L.perm;
             p.h_sell = L.sell;
@@ -816,18 +881,18 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.alpha_long = h->alloc<double>(L.longrows.size());
             CUDA_TRY(cudaStreamSynchronize(h->stream));
             if (!L.perm.empty()) {
-                std::vector<int32_t> inv(L.perm.size());
+                hvec<int32_t> inv(L.perm.size());
+#pragma omp parallel for schedule(static)
                 for (size_t q = 0; q < L.perm.size(); ++q) inv[(size_t)L.perm[q]] = (int32_t)q;
                 CUDA_TRY(cudaMemcpy(p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
                 CUDA_TRY(cudaMemcpy(p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
             }
-            if (!L.pcol.empty()) CUDA_TRY(cudaMemcpy(p.col, L.pcol.data(), L.pcol.size() * 4, cudaMemcpyHostToDevice));
             if (!L.chunks.empty()) CUDA_TRY(cudaMemcpy(p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
             if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
             if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
-            upload_values(h.get(), p, L);
-            clk.mark("upload (H2D)");
+            device_layout(h.get(), p, csr, L, d_colmap);
+            clk.mark("CSR upload + device layout");
             const size_t vsz = dsize(storage);
             p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
             p.y = h->alloc<char>((size_t)npad * vsz);
@@ -840,7 +905,9 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.counters = h->alloc<unsigned>(8 + 64);
             carve_state(h.get(), p);
             h->bytes_model += model_bytes(h.get(), p);
+            clk.mark("allocations");
         }
+        pool_dev_free(d_colmap);
         if (world > 1) {
             ncclUniqueId id;
             std::memcpy(&id, o.nccl_id, sizeof(id));
@@ -860,17 +927,23 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
 
 static void free_handle(topk_eig_s *h) {
     if (!h) return;
+    StageClock clk;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    clk.mark("destroy: stream sync");
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    clk.mark("destroy: graph");
     if (h->comm) ncclCommDestroy(h->comm);
-    for (void *p : h->allocs) cudaFree(p);
-    if (h->hparams) cudaFreeHost(h->hparams);
+    for (void *p : h->allocs) pool_dev_free(p);  // back to the cache (the stream is idle)
+    clk.mark("destroy: pool");
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     for (auto &q : h->prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
+    clk.mark("destroy: events");
     if (h->stream) cudaStreamDestroy(h->stream);
+    clk.mark("destroy: stream");
     delete h;
+    clk.mark("destroy: host state");
 }
 
 // Enqueue one full solve on h->stream (graph replay or eager launches).
@@ -979,7 +1052,14 @@ topk_status_t topk_eig_solve(topk_eig_t h, uint64_t seed, const double *v1, doub
         const int kf = hget<int>(p0, p0.st.k_found);
         std::memcpy(eigenvalues, hptr(p0, p0.st.evals), (size_t)h->K * 8);
         if (residual_est) std::memcpy(residual_est, hptr(p0, p0.st.resid), (size_t)h->K * 8);
-        if (eigenvectors) {
+        if (eigenvectors && h->parts.size() == 1 && h->parts[0].nrows == h->n && kf > 0) {
+            // one part holding every row: the K x n block is contiguous on both sides
+            const size_t es = vec_dtype == TOPK_F32 ? 4 : 8;
+            char *dst = static_cast<char *>(eigenvectors);
+            CUDA_TRY(staged_d2h(h->parts[0].out, (size_t)kf * h->n * es,
+                                [&](const char *src, size_t off, size_t nb) { par_memcpy(dst + off, src, nb); },
+                                h->stream));
+        } else if (eigenvectors) {
             const size_t es = vec_dtype == TOPK_F32 ? 4 : 8;
             for (Part &p : h->parts) {
                 if (p.nrows == 0 || kf == 0) continue;
@@ -1263,5 +1343,7 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
     CATCH(h)
     return TOPK_OK;
 }
+
+size_t topk_eig_trim_pool(void) { return topk::pool_trim(); }
 
 }  // extern "C"

@@ -360,3 +360,15 @@ def test_large_m_jacobi_paths(T, c3s, m, cluster, monkeypatch):
     assert r.info["jacobi_converged"] == 1
     assert normwise(th, ref.theta_all) <= 1e-8
     check_solve(r, ref, 1e-8)
+
+
+def test_memory_pool_reuse_and_trim(T, c3s):
+    """Handles created after a destroy reuse the cached device blocks (same
+    results), and topk_eig_trim_pool releases them."""
+    with T.TopkEig(c3s, 8, "f32", "f64", m=16) as h:
+        a = h.solve(seed=2)
+    with T.TopkEig(c3s, 8, "f32", "f64", m=16) as h:
+        b = h.solve(seed=2)
+    assert np.array_equal(a.eigenvalues, b.eigenvalues) and np.array_equal(a.eigenvectors, b.eigenvectors)
+    assert T.trim_pool() > 0
+    assert T.trim_pool() == 0

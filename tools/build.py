@@ -34,7 +34,7 @@ def nccl_root() -> str:
 
 
 def sources():
-    return [os.path.join(CSRC, f) for f in ("host_prep.cpp", "solver.cu")]
+    return [os.path.join(CSRC, f) for f in ("host_prep.cpp", "mem_pool.cpp", "solver.cu")]
 
 
 def deps():
