@@ -259,16 +259,38 @@ double bf16_bits_to_double(uint16_t b) {
 
 void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos) {
     // stable counting sort by degree, descending (ties keep ascending row index)
-    pos.assign((size_t)m.n, 0);
+    pos.resize((size_t)m.n);
     auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
-#pragma omp parallel for schedule(dynamic, 1)
     for (int32_t q = 0; q < G; ++q) {
+        const int64_t a = b[q], e = b[q + 1], nr = e - a;
         int64_t dmax = 0;
-        for (int64_t r = b[q]; r < b[q + 1]; ++r) dmax = std::max(dmax, deg(r));
-        std::vector<int64_t> start((size_t)dmax + 2, 0);  // start[d] = first position of degree d
-        for (int64_t r = b[q]; r < b[q + 1]; ++r) start[(size_t)(dmax - deg(r)) + 1]++;
-        for (size_t d = 1; d < start.size(); ++d) start[d] += start[d - 1];
-        for (int64_t r = b[q]; r < b[q + 1]; ++r) pos[(size_t)r] = (int32_t)start[(size_t)(dmax - deg(r))]++;
+#pragma omp parallel for schedule(static) reduction(max : dmax)
+        for (int64_t r = a; r < e; ++r) dmax = std::max(dmax, deg(r));
+        const int64_t nb = dmax + 1;  // key = dmax - degree
+        const int T = (nr >= (1 << 16) && nb <= (1 << 22)) ? std::max(1, omp_get_max_threads()) : 1;
+        // per-thread histograms over contiguous row chunks; positions = (key, thread, row) order
+        std::vector<int64_t> cnt((size_t)T * (size_t)nb, 0);
+        const int64_t per = (nr + T - 1) / T;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+        for (int t = 0; t < T; ++t) {
+            int64_t *c = cnt.data() + (size_t)t * nb;
+            const int64_t r1 = std::min(e, a + (t + 1) * per);
+            for (int64_t r = a + t * per; r < r1; ++r) c[dmax - deg(r)]++;
+        }
+        int64_t run = 0;
+        for (int64_t k = 0; k < nb; ++k)
+            for (int t = 0; t < T; ++t) {
+                int64_t &c = cnt[(size_t)t * nb + (size_t)k];
+                const int64_t v = c;
+                c = run;
+                run += v;
+            }
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+        for (int t = 0; t < T; ++t) {
+            int64_t *c = cnt.data() + (size_t)t * nb;
+            const int64_t r1 = std::min(e, a + (t + 1) * per);
+            for (int64_t r = a + t * per; r < r1; ++r) pos[(size_t)r] = (int32_t)c[dmax - deg(r)]++;
+        }
     }
 }
 

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -602,40 +603,41 @@ static const double *hptr(const Part &p, const double *devptr) {
     return reinterpret_cast<const double *>(p.hstate.data() + ((const char *)devptr - p.state));
 }
 
-// a4 on the device: the part's canonical CSR slice goes up as is (values rounded to
-// the value storage dtype on the way, RNE straight from f64, reading Q22, converted
-// chunk by chunk into the pinned staging buffers, mem_pool.h), then k_layout_big /
-// k_layout_sell scatter it into the physical SpMV arrays (the rule of build_part).
-template <typename VT>
-static void device_layout_t(topk_eig_s *h, Part &p, const Csr &csr, const PartLayout &L, const int32_t *d_colmap) {
-    const int64_t r0 = L.row0, ng = L.nrows;
+// a4 on the device, in two halves:
+//  upload_csr_slice: the part's canonical CSR slice goes up as is (row pointers rebased,
+//    values rounded to the value storage dtype on the way, RNE straight from f64,
+//    reading Q22, chunk by chunk into the pinned staging buffers, mem_pool.h). It
+//    needs only the partition, so create runs it on a helper thread while the host
+//    builds the degree order and the layout tables.
+//  device_layout: k_layout_big / k_layout_sell scatter the slice into the physical
+//    SpMV arrays with the rule of build_part.
+struct DevCsr {
+    int64_t *srp = nullptr;
+    int32_t *scol = nullptr;
+    void *sval = nullptr;
+};
+static void *dalloc_or_throw(size_t bytes) {
+    void *q = pool_dev_alloc(std::max<size_t>(bytes, 256));
+    if (!q) CUDA_TRY(cudaErrorMemoryAllocation);
+    return q;
+}
+static void upload_csr_slice(const Csr &csr, int64_t r0, int64_t ng, topk_dtype_t ms, DevCsr &d, cudaStream_t st) {
     const int64_t z0 = csr.rowptr[(size_t)r0], z = csr.rowptr[(size_t)(r0 + ng)] - z0;
-    const size_t es = sizeof(VT);
-    auto dalloc = [&](size_t bytes) {
-        void *q = pool_dev_alloc(std::max<size_t>(bytes, 256));
-        if (!q) CUDA_TRY(cudaErrorMemoryAllocation);
-        return q;
-    };
-    int64_t *d_srp = static_cast<int64_t *>(dalloc((size_t)(ng + 1) * 8));
-    int64_t *d_drp = static_cast<int64_t *>(dalloc((size_t)(ng + 1) * 8));
-    int32_t *d_scol = static_cast<int32_t *>(dalloc((size_t)z * 4));
-    VT *d_sval = static_cast<VT *>(dalloc((size_t)z * es));
+    const size_t es = dsize(ms);
+    d.srp = static_cast<int64_t *>(dalloc_or_throw((size_t)(ng + 1) * 8));
+    d.scol = static_cast<int32_t *>(dalloc_or_throw((size_t)z * 4));
+    d.sval = dalloc_or_throw((size_t)z * es);
     const int64_t *srp = csr.rowptr.data() + r0;
     auto fill_srp = [&](char *dst, size_t off, size_t nb) {
         const size_t i0 = off / 8, cnt = nb / 8;
-        int64_t *d = reinterpret_cast<int64_t *>(dst);
+        int64_t *dd = reinterpret_cast<int64_t *>(dst);
 #pragma omp parallel for schedule(static)
-        for (size_t i = 0; i < cnt; ++i) d[i] = srp[i0 + i] - z0;
+        for (size_t i = 0; i < cnt; ++i) dd[i] = srp[i0 + i] - z0;
     };
-    CUDA_TRY(staged_h2d(d_srp, (size_t)(ng + 1) * 8, fill_srp, h->stream));
-    const char *drp = reinterpret_cast<const char *>(L.rowptr.data());
-    CUDA_TRY(staged_h2d(d_drp, (size_t)(ng + 1) * 8, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, drp + off, nb); },
-                        h->stream));
+    CUDA_TRY(staged_h2d(d.srp, (size_t)(ng + 1) * 8, fill_srp, st));
     const char *sc = reinterpret_cast<const char *>(csr.col.data() + z0);
-    CUDA_TRY(staged_h2d(d_scol, (size_t)z * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, sc + off, nb); },
-                        h->stream));
+    CUDA_TRY(staged_h2d(d.scol, (size_t)z * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, sc + off, nb); }, st));
     const double *sv = csr.val.data() + z0;
-    const topk_dtype_t ms = h->ms;
     auto fill_val = [&](char *dst, size_t off, size_t nb) {
         const size_t k0 = off / es, cnt = nb / es;
 #pragma omp parallel for schedule(static)
@@ -646,29 +648,41 @@ static void device_layout_t(topk_eig_s *h, Part &p, const Csr &csr, const PartLa
             else reinterpret_cast<uint16_t *>(dst)[k] = round_bf16_bits(x);
         }
     };
-    CUDA_TRY(staged_h2d(d_sval, (size_t)z * es, fill_val, h->stream));
+    CUDA_TRY(staged_h2d(d.sval, (size_t)z * es, fill_val, st));
+}
+static void free_dev_csr(DevCsr &d) {
+    pool_dev_free(d.srp);
+    pool_dev_free(d.scol);
+    pool_dev_free(d.sval);
+    d = DevCsr{};
+}
+template <typename VT>
+static void device_layout_t(topk_eig_s *h, Part &p, const PartLayout &L, const DevCsr &d, const int32_t *d_colmap) {
+    const int64_t ng = L.nrows;
+    int64_t *d_drp = static_cast<int64_t *>(dalloc_or_throw((size_t)(ng + 1) * 8));
+    const char *drp = reinterpret_cast<const char *>(L.rowptr.data());
+    CUDA_TRY(staged_h2d(d_drp, (size_t)(ng + 1) * 8, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, drp + off, nb); },
+                        h->stream));
+    const VT *sval = static_cast<const VT *>(d.sval);
     if (L.nbig > 0) {
-        k_layout_big<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d_srp, d_scol, d_sval, p.perm, d_drp, d_colmap, L.nbig,
+        k_layout_big<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap, L.nbig,
                                                            p.col, reinterpret_cast<VT *>(p.val));
         CUDA_TRY(cudaGetLastError());
     }
     const int64_t nsl = (int64_t)L.sell.size() / 2;
     if (nsl > 0) {
-        k_layout_sell<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d_srp, d_scol, d_sval, p.perm, d_drp, d_colmap,
+        k_layout_sell<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap,
                                                             reinterpret_cast<const longlong2 *>(p.sell), (int64_t)L.nbig,
                                                             L.nnonempty, nsl, p.col, reinterpret_cast<VT *>(p.val));
         CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
-    pool_dev_free(d_srp);
     pool_dev_free(d_drp);
-    pool_dev_free(d_scol);
-    pool_dev_free(d_sval);
 }
-static void device_layout(topk_eig_s *h, Part &p, const Csr &csr, const PartLayout &L, const int32_t *d_colmap) {
-    if (h->ms == TOPK_F64) device_layout_t<double>(h, p, csr, L, d_colmap);
-    else if (h->ms == TOPK_F32) device_layout_t<float>(h, p, csr, L, d_colmap);
-    else device_layout_t<uint16_t>(h, p, csr, L, d_colmap);
+static void device_layout(topk_eig_s *h, Part &p, const PartLayout &L, const DevCsr &d, const int32_t *d_colmap) {
+    if (h->ms == TOPK_F64) device_layout_t<double>(h, p, L, d, d_colmap);
+    else if (h->ms == TOPK_F32) device_layout_t<float>(h, p, L, d, d_colmap);
+    else device_layout_t<uint16_t>(h, p, L, d, d_colmap);
 }
 
 static int64_t model_bytes(topk_eig_s *h, const Part &p) {
@@ -743,10 +757,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     s = partition_rule_p(csr.rowptr.data(), n, G, h->bounds.data());
     if (s != TOPK_OK) return fail(s, "partition failed");
     const int64_t npad = padded_rows(h->bounds.data(), G);
-    std::vector<int32_t> pos;
-    degree_order(csr, h->bounds.data(), G, pos);
-    const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
-    clk.mark("partition + order");
+    clk.mark("partition");
 
     // device
     int ndev = 0;
@@ -765,6 +776,40 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         CUDA_TRY(cudaEventCreate(&h->ev0));
         CUDA_TRY(cudaEventCreate(&h->ev1));
         clk.mark("device init");
+        // a4, first half, in the background: the local parts' CSR slices go up on a
+        // helper thread (own stream) while this thread builds the degree order and tables
+        const int nloc = (world > 1) ? 1 : G;
+        std::vector<DevCsr> dcsr((size_t)nloc);
+        std::string up_err;
+        std::thread uploader([&] {
+            cudaStream_t st = nullptr;
+            try {
+                CUDA_TRY(cudaSetDevice(h->device));
+                CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                for (int lp = 0; lp < nloc; ++lp) {
+                    const int g = (world > 1) ? h->rank : lp;
+                    upload_csr_slice(csr, h->bounds[(size_t)g], h->bounds[(size_t)g + 1] - h->bounds[(size_t)g], ms,
+                                     dcsr[(size_t)lp], st);
+                }
+            } catch (CudaFail &e) {
+                up_err = e.msg;
+            } catch (std::bad_alloc &) {
+                up_err = "host allocation failed";
+            }
+            if (st) cudaStreamDestroy(st);
+        });
+        struct Joiner {
+            std::thread &t;
+            std::vector<DevCsr> &d;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+                for (DevCsr &x : d) free_dev_csr(x);
+            }
+        } joiner{uploader, dcsr};
+        std::vector<int32_t> pos;
+        degree_order(csr, h->bounds.data(), G, pos);
+        const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
+        clk.mark("degree order + column map");
         if (!select_kernels(h.get())) return fail(TOPK_E_INVALID, "unsupported (values, storage, compute) dtype combination");
         clk.mark("kernel attributes");
 
@@ -891,8 +936,14 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
             if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
             if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
-            device_layout(h.get(), p, csr, L, d_colmap);
-            clk.mark("CSR upload + device layout");
+            if (uploader.joinable()) {
+                uploader.join();
+                clk.mark("wait for CSR upload");
+                if (!up_err.empty()) throw CudaFail(up_err);
+            }
+            device_layout(h.get(), p, L, dcsr[(size_t)lp], d_colmap);
+            free_dev_csr(dcsr[(size_t)lp]);
+            clk.mark("device layout");
             const size_t vsz = dsize(storage);
             p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
             p.y = h->alloc<char>((size_t)npad * vsz);

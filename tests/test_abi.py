@@ -120,6 +120,20 @@ def test_plan_layout_bit_exact_vs_oracle(G, storage, dtype):
         assert np.array_equal(L["val"].view(np.uint64), oval.view(np.uint64))
 
 
+@pytest.mark.parametrize("G", [1, 2])
+def test_plan_layout_parallel_degree_order_vs_oracle(G):
+    """Parts with >= 2^16 rows take the multi-threaded counting sort (per-thread
+    histograms over row chunks): same stable degree order as the oracle."""
+    A = S.rmat(18, 1_200_000, 9)
+    b = O.partition(A.rowptr, G)
+    for g in range(G):
+        assert b[g + 1] - b[g] >= 2 ** 16
+        L = T.plan_layout(A, G, g, "f32", "f32")
+        orp, ocol, oval, onpad, operm = O.layout(A.rowptr, A.col, A.val, G, b, g, "f32", with_perm=True)
+        assert np.array_equal(L["perm"], operm)
+        assert np.array_equal(L["rowptr"], orp) and np.array_equal(L["col"], ocol)
+
+
 @pytest.mark.parametrize("G", [1, 3])
 def test_physical_format_unpacks_to_logical(G):
     """The SpMV physical format (big-row CSR chunks + SELL-32 slices, host_prep.h)
