@@ -107,6 +107,13 @@ typedef struct {
      * reorthogonalisation; K <= k <= min(m - 2, 256). Periodic conv_check tests are not used. */
     int32_t restart_keep;    /* 0 -> off                                                            */
     int32_t max_restarts;    /* restarts at most (the graph holds max_restarts + 1 cycles)           */
+    /* vector exchange between parts (G > 1, reading Q27):
+     * 0 -> every part receives the whole vector (ncclAllGather into a G * n_pad replica, the
+     * paper's replicated v); 1 -> halo exchange: each part's SpMV reads a compact
+     * vector [own slot | the remote entries its rows touch] and only those entries move (parts on
+     * one device pull them; one process per GPU uses grouped ncclSend/ncclRecv; the multi-process
+     * variant is built and covered by the host-logic tests but was not run on multi-GPU hardware) */
+    int32_t exchange;
 } topk_eig_opts_t;
 
 typedef struct {
@@ -204,6 +211,15 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
  * destroy path after the first handle). Returns every cached, unused block to the
  * driver; returns the bytes released. Thread-safe; live handles are unaffected. */
 size_t topk_eig_trim_pool(void);
+
+/* Host-only halo plan of part g of G (reading Q27): the
+ * remote entries part g's SpMV reads, grouped by owner q in ascending owner position,
+ * exactly as topk_eig_create with opts.exchange = 1 lays them out after the own slot.
+ *   n_halo (host, 1 int64 out), off (host, NULL or G+1 int64: owner q's entries are
+ *   [off[q], off[q+1])), pos (host, NULL or n_halo int32: position in the owner's slot).
+ * Used by the multi-process CPU tests to check the request/send lists. Errors as in create. */
+topk_status_t topk_eig_plan_halo(const topk_matrix_t *A, int32_t G, int32_t g, int64_t *n_halo, int64_t *off,
+                                 int32_t *pos);
 
 /* Per kernel class device time of the last solve (requires opts.profile = 1):
  * class 0 v1, 1 spmv, 2 step, 3 correct, 4 jacobi, 5 ritz pass 0 (norms), 6 ritz pass 1 (output),

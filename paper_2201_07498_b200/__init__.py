@@ -50,7 +50,7 @@ class _Opts(ctypes.Structure):
                 ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("profile", ctypes.c_int32), ("conv_tol", ctypes.c_double),
                 ("conv_check", ctypes.c_int32), ("restart_keep", ctypes.c_int32),
-                ("max_restarts", ctypes.c_int32)]
+                ("max_restarts", ctypes.c_int32), ("exchange", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -77,6 +77,7 @@ _SIGS = {
     "topk_eig_kernel_times": (_S, [_P, _P, _P]),
     "topk_eig_destroy": (None, [_P]),
     "topk_eig_trim_pool": (ctypes.c_size_t, []),
+    "topk_eig_plan_halo": (_S, [_P, _I32, _I32, _P, _P, _P]),
     "topk_eig_last_error": (ctypes.c_char_p, []),
     "topk_eig_nccl_id": (_S, [_P]),
     "topk_eig_plan_partition": (_S, [_P, _I64, _I32, _P]),
@@ -111,6 +112,19 @@ def nccl_id() -> bytes:
 def trim_pool() -> int:
     """Return the library's cached device blocks to the driver (topk_eig_trim_pool)."""
     return int(_lib.topk_eig_trim_pool())
+
+
+def plan_halo(A, G: int, g: int) -> dict:
+    """Host-only halo plan of part g (topk_eig_plan_halo): owner offsets and owner
+    positions of the remote entries the part's SpMV reads (exchange="halo")."""
+    keep = []
+    mat = _matrix(A, keep)
+    nh = ctypes.c_int64()
+    _check(_lib.topk_eig_plan_halo(ctypes.byref(mat), G, g, ctypes.byref(nh), None, None))
+    off = np.zeros(G + 1, np.int64)
+    pos = np.zeros(max(nh.value, 1), np.int32)
+    _check(_lib.topk_eig_plan_halo(ctypes.byref(mat), G, g, ctypes.byref(nh), _ptr(off), _ptr(pos)))
+    return {"n_halo": nh.value, "off": off, "pos": pos[:nh.value]}
 
 
 def plan_partition(rowptr, G: int) -> np.ndarray:
@@ -193,7 +207,7 @@ class TopkEig:
                  breakdown_tol: float = 0.0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, profile: bool = False,
                  conv_tol: float = 0.0, conv_check: int = 0, restart_keep: int = 0,
-                 max_restarts: int = 0):
+                 max_restarts: int = 0, exchange: str = "allgather"):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -215,6 +229,7 @@ class TopkEig:
         o.conv_check = int(conv_check)
         o.restart_keep = int(restart_keep)
         o.max_restarts = int(max_restarts)
+        o.exchange = {"allgather": 0, "halo": 1}[exchange]
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

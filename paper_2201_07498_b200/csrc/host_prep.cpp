@@ -304,6 +304,42 @@ std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t 
     return cm;
 }
 
+void build_halo(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad, const int32_t *pos, Halo &out) {
+    const int64_t n = m.n;
+    const int64_t z0 = m.rowptr[(size_t)b[g]], z1 = m.rowptr[(size_t)b[g + 1]];
+    // columns touched by part g's rows (benign same-value races)
+    std::vector<uint8_t> used((size_t)n, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t k = z0; k < z1; ++k) used[(size_t)m.col[(size_t)k]] = 1;
+    out.colmap.assign((size_t)n, 0);
+    out.off.assign((size_t)G + 1, 0);
+    out.pos.clear();
+    for (int32_t q = 0; q < G; ++q) {
+        const int64_t a = b[q], e = b[q + 1];
+        if (q == g) {
+#pragma omp parallel for schedule(static)
+            for (int64_t c = a; c < e; ++c) out.colmap[(size_t)c] = pos[(size_t)c];
+            out.off[(size_t)q + 1] = out.off[(size_t)q];
+            continue;
+        }
+        // marked owner positions in ascending order: position-indexed flags, then a scan
+        std::vector<int32_t> row_at((size_t)(e - a), -1);
+        for (int64_t c = a; c < e; ++c)
+            if (used[(size_t)c]) row_at[(size_t)pos[(size_t)c]] = (int32_t)(c - a);
+        const int64_t base = out.off[(size_t)q];
+        int64_t t = 0;
+        for (int64_t p = 0; p < e - a; ++p) {
+            const int32_t rr = row_at[(size_t)p];
+            if (rr < 0) continue;
+            out.pos.push_back((int32_t)p);
+            out.colmap[(size_t)(a + rr)] = (int32_t)(npad + base + t);
+            ++t;
+        }
+        out.off[(size_t)q + 1] = base + t;
+    }
+    out.n = out.off[(size_t)G];
+}
+
 topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                                 const int32_t *pos, PartLayout &out, std::string &err) {
     const int64_t r0 = b[g], r1 = b[g + 1];

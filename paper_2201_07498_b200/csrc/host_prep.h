@@ -87,6 +87,17 @@ void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t
 // colmap[c] = device column entry of global column c (one lookup per nonzero).
 std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos);
 
+// Halo exchange (reading Q27): part g's SpMV input
+// is a compact vector x_g = [own slot (n_pad) | the remote columns its rows touch,
+// grouped by owner q, ascending position]; only those values cross between parts.
+struct Halo {
+    int64_t n = 0;               // remote entries
+    std::vector<int64_t> off;    // G+1: owner q's entries are [off[q], off[q+1])
+    std::vector<int32_t> pos;    // position in the owner's slot of each entry
+    std::vector<int32_t> colmap; // global column -> compact device column (own: pos; remote: n_pad + t; unused: 0)
+};
+void build_halo(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad, const int32_t *pos, Halo &out);
+
 // ---------------------------------------------------------------------------
 // SpMV physical format (a4), derived from the logical CSR in degree order:
 //  * "big" rows (positions [0, nbig), degree > kSellMaxLen) stay CSR; their

@@ -1767,6 +1767,23 @@ __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const i
 }
 
 // ---------------------------------------------------------------------------
+// Halo exchange (reading Q27). x_g = [own slot |
+// remote entries grouped by owner]; EL is the storage element as raw bits.
+//  k_halo_pull (parts on one device): x_g[n_pad + t] = x_{q_t}[pos_t]
+//  k_halo_pack (one process per GPU): send[t] = x_g[send_pos[t]] (then NCCL send/recv)
+template <typename EL>
+__global__ void __launch_bounds__(256) k_halo_pull(EL *xg, int64_t npad, int64_t nhalo, const int32_t *hq,
+                                                   const int32_t *hpos, const EL *const *src) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nhalo; t += (int64_t)gridDim.x * blockDim.x)
+        xg[npad + t] = src[hq[t]][hpos[t]];
+}
+template <typename EL>
+__global__ void __launch_bounds__(256) k_halo_pack(const EL *xg, int64_t nsend, const int32_t *spos, EL *sendbuf) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsend; t += (int64_t)gridDim.x * blockDim.x)
+        sendbuf[t] = xg[spos[t]];
+}
+
+// ---------------------------------------------------------------------------
 // a15: eigenvectors back to the original row order: out[k][r] = yt[inv[r]][k]
 // (the caller's K x n_local buffer, vector k contiguous).
 struct UnpermArgs {

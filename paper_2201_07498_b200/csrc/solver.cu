@@ -98,6 +98,15 @@ struct Part {
     int32_t *items = nullptr;
     void *yt = nullptr;            // Ritz output in position order, K values per row
     void *Vs = nullptr;            // thick restart scratch: keep columns (reading Q26)
+    // halo exchange (reading Q27): compact SpMV input x_g = [own slot | remote entries]
+    void *xg = nullptr;
+    int64_t nhalo = 0;
+    std::vector<int64_t> halo_off;     // G+1 (host)
+    std::vector<int32_t> halo_pos_h;   // remote entry -> owner position (host, exports)
+    int32_t *halo_q = nullptr, *halo_pos = nullptr;  // device (pull)
+    std::vector<int64_t> send_off;     // G+1 (multi-process)
+    int32_t *send_pos = nullptr;       // device: own positions requested by each peer
+    void *sendbuf = nullptr;
     double *long_parts = nullptr, *alpha_long = nullptr;
     unsigned *long_cnt = nullptr;
     void *V = nullptr, *y = nullptr, *w = nullptr;
@@ -138,6 +147,8 @@ struct topk_eig_s {
     Exch ex{};
     char *exch_block = nullptr;
     void *replica = nullptr;
+    bool halo = false;                 // opts.exchange == 1 (reading Q27)
+    const void **d_xsrc = nullptr;     // device: every local part's x_g (halo pull)
     SolveParams *dparams = nullptr, *hparams = nullptr;  // hparams: pageable (a pinned block's free
                                                           // measured up to 380 ms on destroy)
     std::vector<SolveParams> hparams_own;
@@ -233,7 +244,51 @@ static void launch_jacobi(topk_eig_s *h, int check) {
     }
 }
 
+// halo exchange of the current vector (reading Q27): parts on one device pull their
+// remote entries; one process per GPU packs what each peer asked for and exchanges it
+// with grouped NCCL send/recv straight into the peers' compact vectors
+static void exch_halo(topk_eig_s *h) {
+    const size_t es = dsize(h->vs);
+    auto launch_pull = [&](Part &p) {
+        if (p.nhalo == 0) return;
+        const unsigned grid = (unsigned)std::min<int64_t>((p.nhalo + 255) / 256, (int64_t)h->nsm * 8);
+        if (es == 8) k_halo_pull<uint64_t><<<grid, 256, 0, h->stream>>>((uint64_t *)p.xg, p.npad, p.nhalo, p.halo_q, p.halo_pos, (const uint64_t *const *)h->d_xsrc);
+        else if (es == 4) k_halo_pull<uint32_t><<<grid, 256, 0, h->stream>>>((uint32_t *)p.xg, p.npad, p.nhalo, p.halo_q, p.halo_pos, (const uint32_t *const *)h->d_xsrc);
+        else k_halo_pull<uint16_t><<<grid, 256, 0, h->stream>>>((uint16_t *)p.xg, p.npad, p.nhalo, p.halo_q, p.halo_pos, (const uint16_t *const *)h->d_xsrc);
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+    };
+    if (!h->comm) {
+        for (Part &p : h->parts) launch_pull(p);
+        return;
+    }
+    Part &p = h->parts[0];
+    const int64_t nsend = p.send_off.back();
+    if (nsend > 0) {
+        const unsigned grid = (unsigned)std::min<int64_t>((nsend + 255) / 256, (int64_t)h->nsm * 8);
+        if (es == 8) k_halo_pack<uint64_t><<<grid, 256, 0, h->stream>>>((const uint64_t *)p.xg, nsend, p.send_pos, (uint64_t *)p.sendbuf);
+        else if (es == 4) k_halo_pack<uint32_t><<<grid, 256, 0, h->stream>>>((const uint32_t *)p.xg, nsend, p.send_pos, (uint32_t *)p.sendbuf);
+        else k_halo_pack<uint16_t><<<grid, 256, 0, h->stream>>>((const uint16_t *)p.xg, nsend, p.send_pos, (uint16_t *)p.sendbuf);
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+    }
+    NCCL_TRY(ncclGroupStart());
+    for (int q = 0; q < h->G; ++q) {
+        if (q == h->rank) continue;
+        const size_t ns = (size_t)(p.send_off[(size_t)q + 1] - p.send_off[(size_t)q]);
+        const size_t nr = (size_t)(p.halo_off[(size_t)q + 1] - p.halo_off[(size_t)q]);
+        if (ns) NCCL_TRY(ncclSend((char *)p.sendbuf + (size_t)p.send_off[(size_t)q] * es, ns * es, ncclUint8, q, h->comm, h->stream));
+        if (nr) NCCL_TRY(ncclRecv((char *)p.xg + (size_t)(p.npad + p.halo_off[(size_t)q]) * es, nr * es, ncclUint8, q, h->comm, h->stream));
+    }
+    NCCL_TRY(ncclGroupEnd());
+}
+
 static void exch_vec_norm(topk_eig_s *h) {
+    if (h->halo) {
+        exch_halo(h);
+        if (h->comm) NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
+        return;
+    }
     if (!h->comm) return;
     Part &p = h->parts[0];
     size_t vb = (size_t)p.npad * dsize(h->vs);
@@ -262,6 +317,7 @@ static void exch_ritz(topk_eig_s *h) {
 
 static void *rep_slot(topk_eig_s *h, Part &p) {
     if (h->G == 1) return nullptr;
+    if (h->halo) return p.xg;  // own slot of the compact vector
     return (char *)h->replica + (size_t)p.g * p.npad * dsize(h->vs);
 }
 
@@ -276,7 +332,7 @@ static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
     a.alpha_long = p.alpha_long; a.nlong = p.nlong;
     const void *ucol = (const char *)p.V + (size_t)(it - 1) * p.npad * sizeof(ST);
-    a.x = (h->G == 1) ? ucol : h->replica;
+    a.x = (h->G == 1) ? ucol : (h->halo ? p.xg : h->replica);
     a.ui = ucol;
     a.y = p.y; a.y_dbg = y_dbg;
     a.slots = p.slots; a.counter = p.counters + 1;
@@ -699,6 +755,56 @@ static int64_t model_bytes(topk_eig_s *h, const Part &p) {
     return b;
 }
 
+// halo set-up for part p (reading Q27): compact column map, remote-entry lists, and
+// with one process per GPU the request lists exchanged so every rank knows which of
+// its positions each peer needs
+static void setup_halo(topk_eig_s *h, Part &p, const Csr &csr, int64_t npad, const int32_t *pos, int32_t *d_colmap) {
+    Halo H;
+    build_halo(csr, h->bounds.data(), h->G, p.g, npad, pos, H);
+    const char *cm = reinterpret_cast<const char *>(H.colmap.data());
+    CUDA_TRY(staged_h2d(d_colmap, H.colmap.size() * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },
+                        h->stream));
+    p.nhalo = H.n;
+    p.halo_off = H.off;
+    p.halo_pos_h = H.pos;
+    std::vector<int32_t> hq((size_t)H.n);
+    for (int q = 0; q < h->G; ++q)
+        for (int64_t t = H.off[(size_t)q]; t < H.off[(size_t)q + 1]; ++t) hq[(size_t)t] = q;
+    p.halo_q = h->alloc<int32_t>((size_t)std::max<int64_t>(H.n, 1));
+    p.halo_pos = h->alloc<int32_t>((size_t)std::max<int64_t>(H.n, 1));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (H.n) {
+        CUDA_TRY(cudaMemcpy(p.halo_q, hq.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(p.halo_pos, H.pos.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
+    }
+    if (!h->comm) return;
+    // counts[r][q] = entries rank r receives from q; rank g sends counts[q][g] to q
+    const int G = h->G, g = h->rank;
+    int64_t *d_cnt = h->alloc<int64_t>((size_t)G * G);
+    std::vector<int64_t> mine((size_t)G);
+    for (int q = 0; q < G; ++q) mine[(size_t)q] = H.off[(size_t)q + 1] - H.off[(size_t)q];
+    CUDA_TRY(cudaMemcpy(d_cnt + (size_t)g * G, mine.data(), (size_t)G * 8, cudaMemcpyHostToDevice));
+    NCCL_TRY(ncclAllGather(d_cnt + (size_t)g * G, d_cnt, (size_t)G, ncclInt64, h->comm, h->stream));
+    std::vector<int64_t> cnt((size_t)G * G);
+    CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, cnt.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    p.send_off.assign((size_t)G + 1, 0);
+    for (int q = 0; q < G; ++q) p.send_off[(size_t)q + 1] = p.send_off[(size_t)q] + (q == g ? 0 : cnt[(size_t)q * G + g]);
+    const int64_t nsend = p.send_off[(size_t)G];
+    p.send_pos = h->alloc<int32_t>((size_t)std::max<int64_t>(nsend, 1));
+    p.sendbuf = h->alloc<char>((size_t)std::max<int64_t>(nsend, 1) * dsize(h->vs));
+    NCCL_TRY(ncclGroupStart());
+    for (int q = 0; q < G; ++q) {
+        if (q == g) continue;
+        const size_t nr = (size_t)(H.off[(size_t)q + 1] - H.off[(size_t)q]);  // I request from q
+        const size_t ns = (size_t)(p.send_off[(size_t)q + 1] - p.send_off[(size_t)q]);  // q requests from me
+        if (nr) NCCL_TRY(ncclSend(p.halo_pos + H.off[(size_t)q], nr, ncclInt32, q, h->comm, h->stream));
+        if (ns) NCCL_TRY(ncclRecv(p.send_pos + p.send_off[(size_t)q], ns, ncclInt32, q, h->comm, h->stream));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+}
+
 static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_t K,
                                  topk_dtype_t storage, topk_dtype_t compute,
                                  const topk_eig_opts_t *opts) {
@@ -740,6 +846,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     h->conv_check = o.conv_check > 0 ? o.conv_check : K;
     if (h->conv_tol > 0.0)
         for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
+    if (o.exchange < 0 || o.exchange > 1) return fail(TOPK_E_INVALID, "exchange must be 0 (allgather) or 1 (halo)");
+    h->halo = (G > 1 && o.exchange == 1);
     h->use_graph = o.use_graph >= 0;
     h->profile = o.profile > 0;
     h->device = o.device;
@@ -820,7 +928,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->ex.ritz_part = h->alloc<double>((size_t)G * K);
         h->ex.rst_part = h->alloc<double>((size_t)G * std::max(h->keep, 1));
 
-        if (G > 1) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
+        if (G > 1 && !h->halo) h->replica = h->alloc<char>((size_t)G * npad * dsize(storage));
         h->ex.replica = h->replica;
         const int nlocal = (world > 1) ? 1 : G;
         h->dparams = h->alloc<SolveParams>(1 + (size_t)nlocal);
@@ -889,10 +997,17 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             }
         }
 
+        if (world > 1) {  // before the parts: the halo set-up exchanges request lists
+            ncclUniqueId id;
+            std::memcpy(&id, o.nccl_id, sizeof(id));
+            NCCL_TRY(ncclCommInitRank(&h->comm, world, id, h->rank));
+        }
         // column map (global column -> device column entry), shared by the local parts
+        // (with the halo exchange each part uploads its own compact map instead)
         int32_t *d_colmap = static_cast<int32_t *>(pool_dev_alloc((size_t)n * 4));
         if (!d_colmap) CUDA_TRY(cudaErrorMemoryAllocation);
-        {
+        struct ColmapGuard { int32_t *p; ~ColmapGuard() { pool_dev_free(p); } } colmap_guard{d_colmap};
+        if (!h->halo) {
             const char *cm = reinterpret_cast<const char *>(colmap.data());
             CUDA_TRY(staged_h2d(d_colmap, (size_t)n * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },
                                 h->stream));
@@ -936,6 +1051,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
             if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
             if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
+            if (h->halo) setup_halo(h.get(), p, csr, npad, pos.data(), d_colmap);
             if (uploader.joinable()) {
                 uploader.join();
                 clk.mark("wait for CSR upload");
@@ -949,6 +1065,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             p.y = h->alloc<char>((size_t)npad * vsz);
             p.w = h->alloc<char>((size_t)npad * vsz);
             if (h->keep > 0) p.Vs = h->alloc<char>((size_t)h->keep * npad * vsz);
+            if (h->halo) p.xg = h->alloc<char>((size_t)(npad + p.nhalo) * vsz);
             p.out = h->alloc<double>((size_t)K * std::max<int64_t>(p.nrows, 1));
             p.yt = h->alloc<double>((size_t)((K + kRitzKB - 1) / kRitzKB) * kRitzKB * std::max<int64_t>(p.npad, 1));
             p.v1buf = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
@@ -958,11 +1075,11 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             h->bytes_model += model_bytes(h.get(), p);
             clk.mark("allocations");
         }
-        pool_dev_free(d_colmap);
-        if (world > 1) {
-            ncclUniqueId id;
-            std::memcpy(&id, o.nccl_id, sizeof(id));
-            NCCL_TRY(ncclCommInitRank(&h->comm, world, id, h->rank));
+        if (h->halo && !h->comm) {  // parts on one device pull from each other's x_g
+            std::vector<const void *> src;
+            for (Part &p : h->parts) src.push_back(p.xg);
+            h->d_xsrc = h->alloc<const void *>(src.size());
+            CUDA_TRY(cudaMemcpy(h->d_xsrc, src.data(), src.size() * sizeof(void *), cudaMemcpyHostToDevice));
         }
         CUDA_TRY(cudaStreamSynchronize(h->stream));
     } catch (CudaFail &e) {
@@ -1259,6 +1376,33 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
     return TOPK_OK;
 }
 
+topk_status_t topk_eig_plan_halo(const topk_matrix_t *A, int32_t G, int32_t g, int64_t *n_halo, int64_t *off,
+                                 int32_t *pos) {
+    if (!A || !n_halo) return fail(TOPK_E_INVALID, "A and n_halo must be non-NULL");
+    if (G < 1 || G > 64 || g < 0 || g >= G) return fail(TOPK_E_INVALID, "need 1 <= G <= 64 and 0 <= g < G");
+    try {
+        Csr csr;
+        std::string err;
+        topk_status_t s = canonicalize(*A, csr, err);
+        if (s != TOPK_OK) return fail(s, err);
+        if (G > csr.n) return fail(TOPK_E_INVALID, "G must be <= n");
+        std::vector<int64_t> b((size_t)G + 1);
+        s = partition_rule_p(csr.rowptr.data(), csr.n, G, b.data());
+        if (s != TOPK_OK) return fail(s, "partition failed");
+        const int64_t npad = padded_rows(b.data(), G);
+        std::vector<int32_t> pp;
+        degree_order(csr, b.data(), G, pp);
+        Halo H;
+        build_halo(csr, b.data(), G, g, npad, pp.data(), H);
+        *n_halo = H.n;
+        if (off) std::memcpy(off, H.off.data(), H.off.size() * 8);
+        if (pos && H.n) std::memcpy(pos, H.pos.data(), (size_t)H.n * 4);
+    } catch (std::bad_alloc &) {
+        return fail(TOPK_E_NOMEM, "host allocation failed");
+    }
+    return TOPK_OK;
+}
+
 topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries) {
     if (!h || !boundaries) return fail(TOPK_E_INVALID, "NULL argument");
     std::memcpy(boundaries, h->bounds.data(), h->bounds.size() * 8);
@@ -1291,7 +1435,23 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
             if (col) {
                 std::vector<int32_t> t(zp);
                 if (zp) CUDA_TRY(cudaMemcpy(t.data(), p.col, zp * 4, cudaMemcpyDeviceToHost));
-                for (size_t k = 0; k < phys.size(); ++k) col[k] = t[(size_t)phys[k]];
+                std::vector<int32_t> hq;
+                if (h->halo) {  // compact entries back to the logical q * n_pad + position (reading Q27)
+                    hq.resize((size_t)p.nhalo);
+                    for (int q2 = 0; q2 < h->G; ++q2)
+                        for (int64_t t2 = p.halo_off[(size_t)q2]; t2 < p.halo_off[(size_t)q2 + 1]; ++t2) hq[(size_t)t2] = q2;
+                }
+                for (size_t k = 0; k < phys.size(); ++k) {
+                    int32_t c = t[(size_t)phys[k]];
+                    if (h->halo) {
+                        if (c < p.npad) c = (int32_t)(p.g * p.npad + c);
+                        else {
+                            const int64_t e = c - p.npad;
+                            c = (int32_t)(hq[(size_t)e] * p.npad + p.halo_pos_h[(size_t)e]);
+                        }
+                    }
+                    col[k] = c;
+                }
             }
             if (val) {
                 std::vector<double> t(zp);
@@ -1382,7 +1542,7 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
             CUDA_TRY(cudaMemsetAsync(p.st.tscale, 0, sizeof(double), h->stream));
             if (!p.y_dbg) p.y_dbg = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
         }
-        if (h->comm) exch_vec_norm(h);
+        if (h->comm || h->halo) exch_vec_norm(h);
         for (Part &p : h->parts) h->spmv_only(h, p);
         CUDA_TRY(cudaStreamSynchronize(h->stream));
         for (Part &p : h->parts) {

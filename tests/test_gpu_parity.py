@@ -88,9 +88,9 @@ def test_layout_bit_exact_c1(T, c1, G, dtype):
             assert np.array_equal(val.view(np.uint64), oval.view(np.uint64))
 
 
-@pytest.mark.parametrize("G", [1, 4])
-def test_layout_bit_exact_rmat(T, c3s, G):
-    with T.TopkEig(c3s, 8, "f32", "f64", parts=G) as h:
+@pytest.mark.parametrize("G,exchange", [(1, "allgather"), (4, "allgather"), (4, "halo")])
+def test_layout_bit_exact_rmat(T, c3s, G, exchange):
+    with T.TopkEig(c3s, 8, "f32", "f64", parts=G, exchange=exchange) as h:
         b = h.partition()
         assert np.array_equal(b, O.partition(c3s.rowptr, G))
         for g in range(G):
@@ -223,17 +223,33 @@ def test_cgs2_and_reorth_off(T, c3s):
     assert np.abs(V @ V.T - np.eye(len(V))).max() > np.abs(V1 @ V1.T - np.eye(len(V1))).max()
 
 
-@pytest.mark.parametrize("G", [2, 3, 5])
-def test_loopback_parts_match(T, c3s, G):
+@pytest.mark.parametrize("G,exchange", [(2, "allgather"), (3, "allgather"), (5, "allgather"),
+                                        (2, "halo"), (5, "halo")])
+def test_loopback_parts_match(T, c3s, G, exchange):
     """G row partitions (virtual ranks on one GPU): same answer as G = 1 within
-    the cross-G tolerance (1e-12 DDD, 1e-6 FDF); layout per part."""
+    the cross-G tolerance (1e-12 DDD, 1e-6 FDF); layout per part. With
+    the halo exchange (reading Q27) the SpMV reads the compact vectors."""
     for storage, tol in (("f64", 1e-12), ("f32", 1e-6)):
         th1 = T_all(T, c3s, 16, storage, "f64", 32, 5)
-        thg = T_all(T, c3s, 16, storage, "f64", 32, 5, parts=G)
+        thg = T_all(T, c3s, 16, storage, "f64", 32, 5, parts=G, exchange=exchange)
         assert normwise(thg, th1) <= tol
     ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=16, m=32, seed=5)
-    r = T.solve(c3s, 16, storage="f64", compute="f64", m=32, seed=5, parts=G)
+    r = T.solve(c3s, 16, storage="f64", compute="f64", m=32, seed=5, parts=G, exchange=exchange)
     check_solve(r, ref, 1e-8)
+
+
+def test_halo_equals_allgather_bitwise(T, c3s):
+    """The halo exchange moves exactly the values the SpMV reads, so the solve is
+    bit-identical to the replicated-vector exchange (same kernels, same sums)."""
+    out = []
+    for ex in ("allgather", "halo"):
+        with T.TopkEig(c3s, 8, "f32", "f64", m=24, parts=4, exchange=ex) as h:
+            out.append(h.solve(seed=12))
+            y = h.debug_spmv(np.linspace(-1, 1, c3s.n))
+            out.append(y)
+    assert np.array_equal(out[0].eigenvalues, out[2].eigenvalues)
+    assert np.array_equal(out[0].eigenvectors, out[2].eigenvectors)
+    assert np.array_equal(out[1], out[3])
 
 
 def test_determinism(T, c3s):

@@ -94,3 +94,70 @@ def test_two_rank_plan_and_exchange_protocol():
         assert abs(alpha - alpha_g) <= 1e-12 * max(1.0, abs(alpha_g))
     # scalars identical on every rank (rank-ordered sums of the same partials)
     assert out[0][4] == out[1][4] and out[0][5] == out[1][5]
+
+
+def _halo_worker(rank, port, q):
+    """Halo exchange (reading Q27) on two gloo ranks: each rank plans its halo
+    (topk_eig_plan_halo), sends its request lists to the owners, answers the
+    requests it receives from its own slot, and runs its SpMV on the compact vector
+    [own slot | received entries] -- the protocol topk_eig_create / exch_halo run
+    with NCCL send/recv -- against the full SpMV."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import paper_2201_07498_b200 as T
+        A = S.rmat(12, 40_000, 13)
+        G = WORLD
+        b = T.plan_partition(A.rowptr, G)
+        L = T.plan_layout(A, G, rank, "f64")
+        H = T.plan_halo(A, G, rank)
+        rp, col, val, npad, perm = L["rowptr"], L["col"], L["val"], L["n_pad"], L["perm"]
+        off, hpos = H["off"], H["pos"]
+        # request lists to the owners (what NCCL send/recv carries once at create)
+        reqs = [None] * G
+        dist.all_gather_object(reqs, {qq: hpos[off[qq]:off[qq + 1]].tolist() for qq in range(G) if qq != rank})
+        # the iteration: own slot, answer each peer's requests, receive mine
+        v = O.v1(9, A.n)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        own = np.zeros(npad)
+        own[: r1 - r0] = v[r0 + perm]
+        sends = {qq: own[np.asarray(reqs[qq][rank], dtype=np.int64)] for qq in range(G) if qq != rank}
+        box = [None] * G
+        dist.all_gather_object(box, sends)
+        recv = np.zeros(H["n_halo"])
+        for qq in range(G):
+            if qq != rank:
+                recv[off[qq]:off[qq + 1]] = box[qq][rank]
+        xg = np.concatenate([own, recv])
+        # logical column q * n_pad + p -> compact index (own: p; remote: n_pad + halo index)
+        lookup = {}
+        for qq in range(G):
+            for t in range(off[qq], off[qq + 1]):
+                lookup[qq * npad + int(hpos[t])] = npad + t
+        ccol = np.array([c - rank * npad if c // npad == rank else lookup[int(c)] for c in col], dtype=np.int64)
+        y = np.array([np.dot(val[rp[r]:rp[r + 1]], xg[ccol[rp[r]:rp[r + 1]]]) for r in range(r1 - r0)])
+        yg = O.spmv(A.rowptr, A.col, A.val, v)[r0 + perm]
+        # every remote column the rows touch is in the halo, nothing else is
+        touched = {int(c) for c in col if c // npad != rank}
+        q.put((rank, np.abs(y - yg).max() / max(1.0, np.abs(yg).max()), touched == set(lookup), int(H["n_halo"]),
+               int(A.n - (r1 - r0))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_halo_exchange_protocol():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, exact_set, nhalo, nremote in out:
+        assert err <= 1e-13, (rank, err)
+        assert exact_set, f"rank {rank}: halo is not exactly the touched remote columns"
+        assert 0 < nhalo < nremote  # the halo is smaller than the peer's whole slot
