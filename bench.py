@@ -232,6 +232,8 @@ def main():
     ap.add_argument("--no-ttk", action="store_true", help="skip the time-to-Top-K m sweep")
     ap.add_argument("--sweep", action="store_true",
                     help="C5 precision sweep on the C3 matrix (report lines, not the bench line)")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+                    help="vector exchange between ranks (N > 1): replicated allgather or halo (reading Q27)")
     ap.add_argument("--quality", action="store_true",
                     help="Fig. 3b analogue: eigenvector orthogonality and L2 error vs K, reorth on/off")
     args = ap.parse_args()
@@ -265,7 +267,7 @@ def main():
         nid = obj[0]
     kw = dict(storage=wl["storage"], compute=wl["compute"], m=wl["m"], device=local)
     if N > 1:
-        kw.update(parts=N, rank=rank, world=N, nccl_id=nid)
+        kw.update(parts=N, rank=rank, world=N, nccl_id=nid, exchange=args.exchange)
     h = T.TopkEig(A, wl["K"], profile=True, **kw)
     rp, _, _, npad = h.layout(0)
     n_g, nnz_g = len(rp) - 1, int(rp[-1])
