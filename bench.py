@@ -268,7 +268,10 @@ def main():
     kw = dict(storage=wl["storage"], compute=wl["compute"], m=wl["m"], device=local)
     if N > 1:
         kw.update(parts=N, rank=rank, world=N, nccl_id=nid, exchange=args.exchange)
-    h = T.TopkEig(A, wl["K"], profile=True, **kw)
+    # the headline value is timed without per-kernel event brackets (they add ~0.6 ms to
+    # a C3 solve); the kernel breakdown and the roofline come from a second timed pass
+    # on a handle that records them (profile=True), right after
+    h = T.TopkEig(A, wl["K"], **kw)
     rp, _, _, npad = h.layout(0)
     n_g, nnz_g = len(rp) - 1, int(rp[-1])
     K, m = wl["K"], wl["m"]
@@ -299,9 +302,32 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    kt = h.kernel_times()  # last solve of the timed region, events inside the graph
     ms_step = ms / args.steps
     value = m * args.steps / (ms / 1e3)
+    h.close()
+    # kernel breakdown pass: same workload, CUDA events around every kernel of part 0
+    # recorded inside the graph on the solve stream
+    kwp = dict(kw)
+    if N > 1:  # a fresh NCCL unique id per communicator
+        obj = [T.nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        kwp["nccl_id"] = obj[0]
+    hp = T.TopkEig(A, wl["K"], profile=True, **kwp)
+    sp = torch.cuda.ExternalStream(hp.stream)
+    for i in range(args.warmup):
+        hp.solve_async(1 + i, ev.data_ptr(), Y.data_ptr(), "f32")
+        hp.sync()
+    nprof = max(1, min(args.steps, 20))
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(sp)
+    for i in range(nprof):
+        hp.solve_async(100 + i, ev.data_ptr(), Y.data_ptr(), "f32")
+    p1.record(sp)
+    hp.sync()
+    prof_ms_step = p0.elapsed_time(p1) / nprof
+    kt = hp.kernel_times()  # last solve of the breakdown pass
+    hp.close()
 
     s = 4 if wl["storage"] == "f32" else 8 if wl["storage"] == "f64" else 2
     sv = s
@@ -357,6 +383,9 @@ def main():
                              "launches_timed": spmv_n,
                              "gather_bound": gather_bound(nnz_g, t_spmv)},
                 "kernels": kernels,
+                "kernel_breakdown_pass": {"steps": nprof, "ms_per_step_with_events": round(prof_ms_step, 4),
+                                          "note": "per-kernel CUDA events inside the graph (part 0); "
+                                                  "the headline value is timed without them"},
                 "cpu_baseline": cpu,
                 "e2e": e2e,
                 "gpu_launches": int(info["gpu_launches"]) * args.steps,
@@ -367,7 +396,6 @@ def main():
                 "paper_context": "paper (V100, fp32): 67x vs 104-thread ARPACK, 1.9x vs Alveo U280 FPGA "
                                  "(PAPER.md:21,219); context only, not comparable"}
         print(json.dumps(line), flush=True)
-    h.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
