@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtopk_eig.so")
+LIB_PATH = os.environ.get("TOPK_LIB", os.path.join(_HERE, "libtopk_eig.so"))  # TOPK_LIB: dev override
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python tools/build.py` "

@@ -214,7 +214,19 @@ __device__ __forceinline__ int ld_col_stream(const int32_t *p) {
 }
 
 template <typename VT, typename ST, typename CT>
-__global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
+// dev knobs (tools/build.py build_variant): prefetch depth and an optional
+// min-blocks bound. Measured on C3 (tools/lab/spmv_variants.py): GQ 8 with the plain
+// bound (80 registers, 3 CTAs/SM) 229 us; GQ 4 / 6 at 4 CTAs/SM 229 / 232 us; an
+// explicit (256, 1) bound makes ptxas take 94 registers (2 CTAs/SM): 256 us.
+#ifndef TOPK_SPMV_GQ
+#define TOPK_SPMV_GQ 8
+#endif
+#ifdef TOPK_SPMV_MINB
+#define TOPK_SPMV_BOUNDS __launch_bounds__(kSpmvNT, TOPK_SPMV_MINB)
+#else
+#define TOPK_SPMV_BOUNDS __launch_bounds__(kSpmvNT)
+#endif
+__global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
     __shared__ CT red[kSpmvNT / 32];
     __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(kSpmvNT) k_spmv(SpmvArgs a, int it) {
     ST *__restrict__ y = reinterpret_cast<ST *>(a.y);
     CT alpha_acc = CT(0);
     const int nwork = a.nchunks + a.nitems;
-    constexpr int GQ = 8;  // nonzeros per lane per group; the next group's col/val are in flight
+    constexpr int GQ = TOPK_SPMV_GQ;  // nonzeros per lane per group; the next group's col/val are in flight
                            // while the current group's x gathers are
     for (int wi = gwarp; wi < nwork; wi += nwarps) {
         if (wi < a.nchunks) {

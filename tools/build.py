@@ -61,6 +61,20 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return SO
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """Dev: the library with extra -D defines (e.g. TOPK_SPMV_GQ=6) at `out`, for A/B
+    runs through TOPK_LIB=<out>."""
+    nr = nccl_root()
+    cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+           "-Xcompiler", "-fPIC,-fopenmp,-O3", "-shared", *[f"-D{d}" for d in defines],
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nr, "include"),
+           *sources(), "-o", out,
+           "-L", os.path.join(nr, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nr, "lib"),
+           "-lgomp"]
+    subprocess.check_call(cmd)
+    return out
+
+
 def build_all(force: bool = False, verbose: bool = False):
     sys.path.insert(0, ROOT)
     import oracle
