@@ -600,10 +600,10 @@ def run_quality(args):
     A = make_matrix("C3")
     arms = [a for a in SWEEP_ARMS if a[0] in ("DDD", "FDF", "FFF")]
     for name, st, ct, vs in arms:
-        for reorth in (1, -1):
+        for reorth, period in ((1, 1), (1, 4), (-1, 1)):
             for K in (8, 16, 24):
                 with T.TopkEig(A, K, storage=st, compute=ct, values_storage=vs, m=K, reorth=reorth,
-                               check_symmetry=False) as h:
+                               reorth_period=period, check_symmetry=False) as h:
                     r = h.solve(seed=1, vectors=True, vec_dtype="f64")
                 kf = len(r.eigenvectors)
                 q = eigen_quality(A, r.eigenvectors, r.eigenvalues[:kf])
@@ -611,7 +611,8 @@ def run_quality(args):
                 res = q.pop("residuals")
                 gap = float(np.max(np.abs(est - res)) / abs(r.eigenvalues[0]))
                 print(json.dumps({"kind": "quality", "workload": "C3", "arm": name,
-                                  "reorth": "cgs" if reorth == 1 else "off", "K": K, "m": K, "k_found": kf,
+                                  "reorth": ("cgs" if period == 1 else f"cgs every {period}") if reorth == 1 else "off",
+                                  "K": K, "m": K, "k_found": kf,
                                   **q, "residual_est_vs_measured_max_rel": gap}), flush=True)
     return 0
 

@@ -114,6 +114,11 @@ typedef struct {
      * one device pull them; one process per GPU uses grouped ncclSend/ncclRecv; the multi-process
      * variant is built and covered by the host-logic tests but was not run on multi-GPU hardware) */
     int32_t exchange;
+    /* periodic reorthogonalisation (reading Q28): with reorth = 1 and
+     * reorth_period = p > 1 the full reorthogonalisation runs at the two consecutive iterations
+     * kp and kp + 1 only (Grcar's periodic scheme); the others are the plain three-term step.
+     * 0/1 -> every iteration. Not with thick restart. */
+    int32_t reorth_period;
 } topk_eig_opts_t;
 
 typedef struct {

@@ -407,3 +407,39 @@ def solve_thick_restart(rowptr, col, val, K: int, m: int, keep: int, max_restart
     return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, res,
                     extra={"restarts": restarts, "iterations": total, "T": Tm.copy(),
                            "v_next": V[mm].copy() if mm < m + 1 else None})
+
+
+def solve_periodic(rowptr, col, val, K: int, m: int, period: int, seed: int = 1, v1vec=None,
+                   tau: float = 1e-12, want_vectors: bool = True) -> SolveOut:
+    """Periodic reorthogonalisation (reading Q28; the paper
+    makes reorthogonalisation optional, and weighs its O(nK^2/2) cost,
+    :260): Alg.1 with the full reorthogonalisation pass (l.12-18, O5) at the two
+    consecutive iterations i = k p and k p + 1 (k = 1, 2, ...; Grcar's periodic scheme:
+    reorthogonalising a single vector lets the three-term recurrence carry the lost
+    orthogonality of its predecessor straight back); every other iteration is the plain
+    three-term step. The same C iteration (orc_lanczos_iter) as O4, called with the
+    per-iteration flag; period 1 is O4 with reorth, period > m is O4 without."""
+    n = len(rowptr) - 1
+    if v1vec is None:
+        v1vec = v1(seed, n)
+    rp, c, v = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    u = _c(v1vec, np.float64)
+    V = np.zeros((m, n), np.float64)
+    V[0] = u / np.sqrt(np.add.accumulate(u * u)[-1])  # sequential sum, as in oracle.c
+    vt, vn = np.zeros(n), np.zeros(n)
+    alpha, beta, ts = np.zeros(m), np.zeros(m + 1), np.zeros(1)
+    mf, bd = m, False
+    for i in range(1, m + 1):
+        ro = 1 if (period >= 1 and (i % period == 0 or (i > 1 and (i - 1) % period == 0))) else 0
+        if _load().orc_lanczos_iter(n, _p(rp), _p(c), _p(v), i, ro, tau, _p(V), _p(vt), _p(vn),
+                                    _p(alpha), _p(beta), _p(ts)):
+            mf, bd = i - 1, True
+            break
+    if not bd:
+        beta[m] = np.sqrt(np.add.accumulate(vn * vn)[-1])
+    lz = LanczosOut(alpha[:mf].copy(), beta[:mf + 1].copy(), V[:mf].copy(), mf, bd)
+    theta, S, sw, conv = jacobi(tridiag_dense(lz.alpha, lz.beta))
+    idx = select(theta, K)
+    Y = ritz(lz.V, S, idx) if want_vectors else None
+    rest = np.abs(lz.beta[mf] * S[mf - 1, idx]) if mf > 0 else np.zeros(0)
+    return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, rest, extra={"period": period})

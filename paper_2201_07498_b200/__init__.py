@@ -50,7 +50,8 @@ class _Opts(ctypes.Structure):
                 ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("profile", ctypes.c_int32), ("conv_tol", ctypes.c_double),
                 ("conv_check", ctypes.c_int32), ("restart_keep", ctypes.c_int32),
-                ("max_restarts", ctypes.c_int32), ("exchange", ctypes.c_int32)]
+                ("max_restarts", ctypes.c_int32), ("exchange", ctypes.c_int32),
+                ("reorth_period", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -207,7 +208,7 @@ class TopkEig:
                  breakdown_tol: float = 0.0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, profile: bool = False,
                  conv_tol: float = 0.0, conv_check: int = 0, restart_keep: int = 0,
-                 max_restarts: int = 0, exchange: str = "allgather"):
+                 max_restarts: int = 0, exchange: str = "allgather", reorth_period: int = 0):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -230,6 +231,7 @@ class TopkEig:
         o.restart_keep = int(restart_keep)
         o.max_restarts = int(max_restarts)
         o.exchange = {"allgather": 0, "halo": 1}[exchange]
+        o.reorth_period = int(reorth_period)
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -74,6 +74,15 @@ struct NcclFail { std::string msg; explicit NcclFail(std::string m) : msg(std::m
 
 static size_t dsize(topk_dtype_t t) { return t == TOPK_F64 ? 8 : t == TOPK_F32 ? 4 : 2; }
 
+// Host <-> device copy ordered on the handle's (non-blocking) stream and waited for:
+// a plain cudaMemcpy runs on the legacy stream and would not wait for the stream's
+// pending work (e.g. the zero fill of a freshly allocated block).
+static cudaError_t scopy(cudaStream_t st, void *dst, const void *src, size_t n, cudaMemcpyKind k) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, n, k, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e;
+}
+
 struct SolveParams {
     uint64_t seed;
     int use_v1;
@@ -131,6 +140,7 @@ struct topk_eig_s {
     double tau = 1e-12;
     double conv_tol = 0.0;   // reading Q25 (0: fixed m)
     int keep = 0;            // reading Q26: Ritz pairs kept per thick restart (0: off)
+    int period = 1;          // reading Q28: reorthogonalise every period-th iteration
     int max_restarts = 0;
     int conv_check = 0;      // check period c
     int conv_checks = 0;     // checks enqueued per solve
@@ -488,7 +498,9 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     for (int it = it0; it <= h->m; ++it) {
         for (Part &p : h->parts) launch_spmv<VT, ST, CT>(h, p, it, nullptr);
         exch_alpha(h);
-        if (h->reorth < 0) {
+        // reorth off (the paper's optional mode), or an iteration between two periodic
+        // reorthogonalisations (reading Q28): the three-term step publishes u_{i+1}
+        if (h->reorth < 0 || (h->period > 1 && it % h->period != 0 && (it == 1 || (it - 1) % h->period != 0))) {
             for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 1);
             exch_vec_norm(h);
             continue;
@@ -578,7 +590,8 @@ static void set_kernels(topk_eig_s *h) {
         const char *e = std::getenv("TOPK_NO_TMA");
         h->use_tma = !(e && e[0] == '1');
         // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed
-        h->use_gram = h->reorth != -1 && h->keep == 0;  // restarts replace basis columns: explicit norm pass
+        // restarts replace basis columns and periodic reorth skips the dots: explicit norm pass
+        h->use_gram = h->reorth != -1 && h->keep == 0 && h->period == 1;
         const char *e2 = std::getenv("TOPK_TMA_CORRECT");
         h->tma_correct = e2 && e2[0] == '1';
         const char *e3 = std::getenv("TOPK_TMA_STEP");
@@ -749,7 +762,8 @@ static int64_t model_bytes(topk_eig_s *h, const Part &p) {
     int64_t b = 0;
     for (int i = 1; i <= h->m; ++i) {
         b += p.nnz * (4 + sv) + 4 * (p.nrows + 1) + s * nx + s * p.nrows;
-        b += (h->reorth < 0) ? 4 * p.nrows * s : (2 * i + 4) * p.nrows * s;
+        const bool ro = h->reorth > 0 && (h->period <= 1 || i % h->period == 0 || (i > 1 && (i - 1) % h->period == 0));
+        b += ro ? (2 * i + 4) * p.nrows * s : 4 * p.nrows * s;
     }
     b += (int64_t)(h->m + 3 * h->K) * p.nrows * s;
     return b;
@@ -774,8 +788,8 @@ static void setup_halo(topk_eig_s *h, Part &p, const Csr &csr, int64_t npad, con
     p.halo_pos = h->alloc<int32_t>((size_t)std::max<int64_t>(H.n, 1));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (H.n) {
-        CUDA_TRY(cudaMemcpy(p.halo_q, hq.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(p.halo_pos, H.pos.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(scopy(h->stream, p.halo_q, hq.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(scopy(h->stream, p.halo_pos, H.pos.data(), (size_t)H.n * 4, cudaMemcpyHostToDevice));
     }
     if (!h->comm) return;
     // counts[r][q] = entries rank r receives from q; rank g sends counts[q][g] to q
@@ -783,7 +797,7 @@ static void setup_halo(topk_eig_s *h, Part &p, const Csr &csr, int64_t npad, con
     int64_t *d_cnt = h->alloc<int64_t>((size_t)G * G);
     std::vector<int64_t> mine((size_t)G);
     for (int q = 0; q < G; ++q) mine[(size_t)q] = H.off[(size_t)q + 1] - H.off[(size_t)q];
-    CUDA_TRY(cudaMemcpy(d_cnt + (size_t)g * G, mine.data(), (size_t)G * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(scopy(h->stream, d_cnt + (size_t)g * G, mine.data(), (size_t)G * 8, cudaMemcpyHostToDevice));
     NCCL_TRY(ncclAllGather(d_cnt + (size_t)g * G, d_cnt, (size_t)G, ncclInt64, h->comm, h->stream));
     std::vector<int64_t> cnt((size_t)G * G);
     CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, cnt.size() * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -835,6 +849,10 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (compute == TOPK_F32 && storage == TOPK_F64) return fail(TOPK_E_INVALID, "compute must be at least as precise as storage");
     if (!(o.conv_tol >= 0.0) || o.conv_check < 0) return fail(TOPK_E_INVALID, "conv_tol must be >= 0 and conv_check >= 0");
     h->conv_tol = o.conv_tol;
+    if (o.reorth_period < 0) return fail(TOPK_E_INVALID, "reorth_period must be >= 0");
+    h->period = o.reorth_period > 1 ? o.reorth_period : 1;
+    if (h->period > 1 && h->reorth != 1) return fail(TOPK_E_INVALID, "reorth_period > 1 needs reorth = 1");
+    if (h->period > 1 && o.restart_keep > 0) return fail(TOPK_E_INVALID, "thick restart needs reorthogonalisation every iteration");
     if (o.restart_keep < 0 || o.max_restarts < 0) return fail(TOPK_E_INVALID, "restart_keep and max_restarts must be >= 0");
     if (o.restart_keep > 0) {
         if (o.restart_keep < K || o.restart_keep > m - 2 || o.restart_keep > 256)
@@ -1044,13 +1062,13 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 hvec<int32_t> inv(L.perm.size());
 #pragma omp parallel for schedule(static)
                 for (size_t q = 0; q < L.perm.size(); ++q) inv[(size_t)L.perm[q]] = (int32_t)q;
-                CUDA_TRY(cudaMemcpy(p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
-                CUDA_TRY(cudaMemcpy(p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(scopy(h->stream, p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(scopy(h->stream, p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
             }
-            if (!L.chunks.empty()) CUDA_TRY(cudaMemcpy(p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
-            if (!L.longrows.empty()) CUDA_TRY(cudaMemcpy(p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
-            if (!L.sell.empty()) CUDA_TRY(cudaMemcpy(p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
-            if (!L.items.empty()) CUDA_TRY(cudaMemcpy(p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
+            if (!L.chunks.empty()) CUDA_TRY(scopy(h->stream, p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+            if (!L.longrows.empty()) CUDA_TRY(scopy(h->stream, p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
+            if (!L.sell.empty()) CUDA_TRY(scopy(h->stream, p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
+            if (!L.items.empty()) CUDA_TRY(scopy(h->stream, p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
             if (h->halo) setup_halo(h.get(), p, csr, npad, pos.data(), d_colmap);
             if (uploader.joinable()) {
                 uploader.join();
@@ -1079,7 +1097,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             std::vector<const void *> src;
             for (Part &p : h->parts) src.push_back(p.xg);
             h->d_xsrc = h->alloc<const void *>(src.size());
-            CUDA_TRY(cudaMemcpy(h->d_xsrc, src.data(), src.size() * sizeof(void *), cudaMemcpyHostToDevice));
+            CUDA_TRY(scopy(h->stream, h->d_xsrc, src.data(), src.size() * sizeof(void *), cudaMemcpyHostToDevice));
         }
         CUDA_TRY(cudaStreamSynchronize(h->stream));
     } catch (CudaFail &e) {
@@ -1434,7 +1452,7 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
             const size_t zp = (size_t)p.nphys;
             if (col) {
                 std::vector<int32_t> t(zp);
-                if (zp) CUDA_TRY(cudaMemcpy(t.data(), p.col, zp * 4, cudaMemcpyDeviceToHost));
+                if (zp) CUDA_TRY(scopy(h->stream, t.data(), p.col, zp * 4, cudaMemcpyDeviceToHost));
                 std::vector<int32_t> hq;
                 if (h->halo) {  // compact entries back to the logical q * n_pad + position (reading Q27)
                     hq.resize((size_t)p.nhalo);
@@ -1456,14 +1474,14 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
             if (val) {
                 std::vector<double> t(zp);
                 if (h->ms == TOPK_F64) {
-                    if (zp) CUDA_TRY(cudaMemcpy(t.data(), p.val, zp * 8, cudaMemcpyDeviceToHost));
+                    if (zp) CUDA_TRY(scopy(h->stream, t.data(), p.val, zp * 8, cudaMemcpyDeviceToHost));
                 } else if (h->ms == TOPK_F32) {
                     std::vector<float> f(zp);
-                    if (zp) CUDA_TRY(cudaMemcpy(f.data(), p.val, zp * 4, cudaMemcpyDeviceToHost));
+                    if (zp) CUDA_TRY(scopy(h->stream, f.data(), p.val, zp * 4, cudaMemcpyDeviceToHost));
                     for (size_t k = 0; k < zp; ++k) t[k] = f[k];
                 } else {
                     std::vector<uint16_t> f(zp);
-                    if (zp) CUDA_TRY(cudaMemcpy(f.data(), p.val, zp * 2, cudaMemcpyDeviceToHost));
+                    if (zp) CUDA_TRY(scopy(h->stream, f.data(), p.val, zp * 2, cudaMemcpyDeviceToHost));
                     for (size_t k = 0; k < zp; ++k) t[k] = bf16_bits_to_double(f[k]);
                 }
                 for (size_t k = 0; k < phys.size(); ++k) val[k] = t[(size_t)phys[k]];
@@ -1504,7 +1522,7 @@ topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32
     try {
         const size_t es = dsize(h->vs);
         std::vector<char> t((size_t)nc * p.npad * es);
-        CUDA_TRY(cudaMemcpy(t.data(), p.V, t.size(), cudaMemcpyDeviceToHost));
+        CUDA_TRY(scopy(h->stream, t.data(), p.V, t.size(), cudaMemcpyDeviceToHost));
         const double *sc = hptr(p, p.st.scale);
         const double *bt = hptr(p, p.st.beta);
         for (int j = 0; j < nc; ++j) {
@@ -1534,10 +1552,10 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
                 else if (h->vs == TOPK_F32) reinterpret_cast<float *>(buf.data())[r] = round_f32(v);
                 else reinterpret_cast<uint16_t *>(buf.data())[r] = round_bf16_bits(v);
             }
-            CUDA_TRY(cudaMemcpy(p.V, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+            CUDA_TRY(scopy(h->stream, p.V, buf.data(), buf.size(), cudaMemcpyHostToDevice));
             if (h->G > 1 && h->comm == nullptr)
-                CUDA_TRY(cudaMemcpy(rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
-            if (h->comm) CUDA_TRY(cudaMemcpy(rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
+                CUDA_TRY(scopy(h->stream, rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
+            if (h->comm) CUDA_TRY(scopy(h->stream, rep_slot(h, p), buf.data(), buf.size(), cudaMemcpyHostToDevice));
             CUDA_TRY(cudaMemsetAsync(p.st.done, 0, sizeof(int), h->stream));
             CUDA_TRY(cudaMemsetAsync(p.st.tscale, 0, sizeof(double), h->stream));
             if (!p.y_dbg) p.y_dbg = h->alloc<double>((size_t)std::max<int64_t>(p.nrows, 1));
@@ -1547,7 +1565,7 @@ topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {
         CUDA_TRY(cudaStreamSynchronize(h->stream));
         for (Part &p : h->parts) {
             std::vector<double> t((size_t)p.nrows);
-            CUDA_TRY(cudaMemcpy(t.data(), p.y_dbg, (size_t)p.nrows * 8, cudaMemcpyDeviceToHost));
+            CUDA_TRY(scopy(h->stream, t.data(), p.y_dbg, (size_t)p.nrows * 8, cudaMemcpyDeviceToHost));
             for (int64_t r = 0; r < p.nrows; ++r) y[p.row0 + p.h_perm[(size_t)r]] = t[(size_t)r];
         }
     }

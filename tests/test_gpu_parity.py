@@ -388,3 +388,17 @@ def test_memory_pool_reuse_and_trim(T, c3s):
     assert np.array_equal(a.eigenvalues, b.eigenvalues) and np.array_equal(a.eigenvectors, b.eigenvectors)
     assert T.trim_pool() > 0
     assert T.trim_pool() == 0
+
+
+@pytest.mark.parametrize("storage,tol", [("f64", 1e-8), ("f32", 1e-4)])
+def test_periodic_reorth(T, c3s, storage, tol):
+    """Reading Q28: reorthogonalisation of the pairs of iterations (4k, 4k + 1) only,
+    against oracle.solve_periodic, within the north-star tolerances; period 1 is the
+    default path bit for bit."""
+    K, m, p = 16, 32, 4
+    ref = O.solve_periodic(c3s.rowptr, c3s.col, c3s.val, K, m, p, seed=6, tau=O.TAU[storage])
+    th = T_all(T, c3s, K, storage, "f64", m, 6, reorth_period=p)
+    assert normwise(th, ref.theta_all) <= tol
+    a = T_all(T, c3s, K, storage, "f64", m, 6, reorth_period=1)
+    b = T_all(T, c3s, K, storage, "f64", m, 6)
+    assert np.array_equal(a, b)

@@ -477,3 +477,25 @@ def test_p12_thick_restart_relation_and_convergence():
     r0 = O.solve_thick_restart(A.rowptr, A.col, A.val, K, m, keep, max_restarts=0, seed=2)
     p = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=2)
     assert np.allclose(np.sort(r0.theta_all), np.sort(p.theta_all), rtol=0, atol=1e-12 * nrmA)
+
+
+# ---------------------------------------------------------------- P13 (periodic reorth)
+def test_p13_periodic_reorth_special_cases():
+    """solve_periodic (reading Q28): period 1 is the full-reorthogonalisation oracle
+    bit for bit, a period beyond m is the no-reorthogonalisation oracle bit for bit,
+    and period 4 (pairs of reorthogonalised iterations) keeps the basis orthogonal to
+    1e-12 and the Ritz values within 1e-12 of full reorthogonalisation."""
+    A = S.rmat(12, 30_000, 3)
+    m, K = 40, 8
+    full = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=4, reorth=1)
+    none = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=4, reorth=0)
+    p1 = O.solve_periodic(A.rowptr, A.col, A.val, K, m, 1, seed=4)
+    pinf = O.solve_periodic(A.rowptr, A.col, A.val, K, m, m + 1, seed=4)
+    assert np.array_equal(p1.theta_all, full.theta_all) and np.array_equal(p1.eigenvectors, full.eigenvectors)
+    assert np.array_equal(pinf.theta_all, none.theta_all)
+    p4 = O.solve_periodic(A.rowptr, A.col, A.val, K, m, 4, seed=4)
+    orth = lambda V: np.abs(V @ V.T - np.eye(len(V))).max()
+    assert orth(full.lanczos.V) <= 1e-13
+    assert orth(p4.lanczos.V) <= 1e-12 < orth(none.lanczos.V)
+    nrm = np.abs(full.theta_all).max()
+    assert np.abs(np.sort(p4.theta_all) - np.sort(full.theta_all)).max() <= 1e-12 * nrm
