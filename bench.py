@@ -447,10 +447,9 @@ def time_to_topk(T, A, wl, kw, reps=5):
         out[f"adaptive tol=1e-5 c={c}"] = {"ms": round(ms, 3), "iterations": r.info["iterations"],
                                            "converged_of_K": conv, "stopped": bool(r.info["converged_stop"])}
     # thick restart (reading Q26): basis of m = 3K (2K+1 .. 3K steps per cycle), stop at tol;
-    # the graph holds max_restarts + 1 cycles and the launches of the cycles after the stop
-    # return at once (~2.5 us each), so the cap is kept near what the workload needs
+    # the restart cycles run in a CUDA-graph WHILE node, so the cap costs nothing
     for mr, keep in ((3 * K, 3 * K // 2), (4 * K, 2 * K)):
-        with T.TopkEig(A, K, check_symmetry=False, conv_tol=1e-5, restart_keep=keep, max_restarts=10,
+        with T.TopkEig(A, K, check_symmetry=False, conv_tol=1e-5, restart_keep=keep, max_restarts=40,
                        **dict(kw, m=mr)) as h:
             ev = torch.zeros(K, dtype=torch.float64, device="cuda")
             h.solve_async(1, ev.data_ptr(), None)

@@ -1022,6 +1022,7 @@ struct JacArgs {
     // restart data (coefR, arrow_theta, arrow_b) of the `keep` largest pairs
     int check;
     double conv_tol;
+    int max_restarts;  // check == 2: no restart decision once this many restarts were done
 };
 
 // Entry (r, c) of T_mm: tridiagonal (alpha, beta), or after a thick restart
@@ -1181,6 +1182,7 @@ __global__ void __launch_bounds__(1024, 1) k_jacobi(JacArgs a) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const LzState &st = a.st;
     if (a.check && *(volatile int *)st.done) return;  // stopped or broke down already
+    if (a.check == 2 && *st.restarts >= a.max_restarts) return;  // last cycle: the final solve follows
     const int mm = *st.m_found;
     if (tid == 0 && !*st.done) {
         double sq = 0.0;
@@ -1328,6 +1330,7 @@ __global__ void __launch_bounds__(kJacClNT, 1) k_jacobi_cl(JacArgs a) {
     const int br = (int)cl.block_rank(), CL = (int)cl.num_blocks();
     const LzState &st = a.st;
     if (a.check && *(volatile int *)st.done) return;  // same value in every CTA
+    if (a.check == 2 && *st.restarts >= a.max_restarts) return;
     const int mm = *st.m_found;
     if (br == 0 && tid == 0 && !*st.done) {
         double sq = 0.0;
@@ -1793,6 +1796,13 @@ template <typename EL>
 __global__ void __launch_bounds__(256) k_halo_pack(const EL *xg, int64_t nsend, const int32_t *spos, EL *sendbuf) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsend; t += (int64_t)gridDim.x * blockDim.x)
         sendbuf[t] = xg[spos[t]];
+}
+
+// Thick-restart loop condition of the CUDA graph's WHILE node (reading Q26): one more
+// restart cycle while the iteration has not stopped and fewer than R restarts are done.
+__global__ void k_restart_cond(cudaGraphConditionalHandle ch, const int *done, const int *restarts, int R) {
+    if (threadIdx.x == 0)
+        cudaGraphSetConditional(ch, (*(volatile const int *)done == 0 && *(volatile const int *)restarts < R) ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------------------

@@ -158,6 +158,7 @@ struct topk_eig_s {
     char *exch_block = nullptr;
     void *replica = nullptr;
     bool halo = false;                 // opts.exchange == 1 (reading Q27)
+    cudaStream_t body_stream = nullptr; // captures the thick-restart WHILE body (reading Q26)
     const void **d_xsrc = nullptr;     // device: every local part's x_g (halo pull)
     SolveParams *dparams = nullptr, *hparams = nullptr;  // hparams: pageable (a pinned block's free
                                                           // measured up to 380 ms on destroy)
@@ -228,6 +229,7 @@ static void launch_jacobi(topk_eig_s *h, int check) {
         a.hl_log2 = h->jac_hl_log2;
         a.check = check;
         a.conv_tol = h->conv_tol;
+        a.max_restarts = h->max_restarts;
         prof_begin(h, p, 4);
         if (h->jac_cl > 0) {
             cudaLaunchConfig_t cfg = {};
@@ -443,8 +445,8 @@ static void exch_rst(topk_eig_s *h) {
                            h->comm, h->stream));
 }
 template <typename ST, typename CT>
-static void launch_restart(topk_eig_s *h) {
-    launch_jacobi(h, 2);
+static void launch_restart(topk_eig_s *h, bool decide = true) {
+    if (decide) launch_jacobi(h, 2);  // the restart data (or the converged stop)
     const int ng = (h->keep + kRitzKB - 1) / kRitzKB;
     for (Part &p : h->parts) {
         RestartArgs a;
@@ -493,7 +495,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // cycles: the paper's fixed m iterations (cycle 0 only), or thick-restart cycles
     // (reading Q26): restart after cycles 0 .. R-1, then steps keep+1 .. m again
     const int R = h->keep > 0 ? h->max_restarts : 0;
-    for (int cyc = 0; cyc <= R; ++cyc) {
+    auto run_cycle = [&](int cyc) {
     const int it0 = (cyc == 0) ? 1 : h->keep + 1;
     for (int it = it0; it <= h->m; ++it) {
         for (Part &p : h->parts) launch_spmv<VT, ST, CT>(h, p, it, nullptr);
@@ -519,7 +521,63 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             launch_jacobi(h, 1);  // reading Q25: may set done = 2 (later launches return at once)
         }
     }
-    if (cyc < R) launch_restart<ST, CT>(h);
+    };
+    // thick restart inside a captured graph: cycle 0, then a WHILE node whose body is one
+    // restart + cycle, looping on the device (no unrolled cycles, no host round trip).
+    // Unrolled cycles (finished ones return at once) when not capturing, when profiling
+    // (event nodes are not allowed in conditional bodies), with several processes, or
+    // with TOPK_NO_COND=1.
+    const char *nc = std::getenv("TOPK_NO_COND");
+    const bool use_while = R > 0 && h->capturing && !h->profile && h->world == 1 && !(nc && nc[0] == '1');
+    if (!use_while) {
+        for (int cyc = 0; cyc <= R; ++cyc) {
+            run_cycle(cyc);
+            if (cyc < R) launch_restart<ST, CT>(h);
+        }
+    } else {
+        run_cycle(0);
+        launch_jacobi(h, 2);
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t ndep = 0;
+        CUDA_TRY(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &g, &deps, &ndep));
+        cudaGraphConditionalHandle ch;
+        CUDA_TRY(cudaGraphConditionalHandleCreate(&ch, g, 0, 0));
+        Part &p0 = h->parts[0];
+        k_restart_cond<<<1, 32, 0, h->stream>>>(ch, p0.st.done, p0.st.restarts, R);
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+        CUDA_TRY(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &g, &deps, &ndep));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = ch;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        CUDA_TRY(cudaGraphAddNode(&cn, g, deps, ndep, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CUDA_TRY(cudaStreamUpdateCaptureDependencies(h->stream, &cn, 1, cudaStreamSetCaptureDependencies));
+        if (!h->body_stream) CUDA_TRY(cudaStreamCreateWithFlags(&h->body_stream, cudaStreamNonBlocking));
+        cudaStream_t main_stream = h->stream;
+        CUDA_TRY(cudaStreamBeginCaptureToGraph(h->body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        h->stream = h->body_stream;
+        try {
+            launch_restart<ST, CT>(h, false);
+            run_cycle(1);
+            launch_jacobi(h, 2);
+            k_restart_cond<<<1, 32, 0, h->stream>>>(ch, p0.st.done, p0.st.restarts, R);
+            CUDA_TRY(cudaGetLastError());
+            h->launches++;
+        } catch (...) {
+            h->stream = main_stream;
+            cudaGraph_t dummy;
+            cudaStreamEndCapture(h->body_stream, &dummy);
+            throw;
+        }
+        h->stream = main_stream;
+        cudaGraph_t body_out;
+        CUDA_TRY(cudaStreamEndCapture(h->body_stream, &body_out));
     }
     // a12-a13: Jacobi (redundant on every part, identical inputs)
     launch_jacobi(h, 0);
@@ -1127,6 +1185,7 @@ static void free_handle(topk_eig_s *h) {
     for (auto &q : h->prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
     clk.mark("destroy: events");
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->body_stream) cudaStreamDestroy(h->body_stream);
     clk.mark("destroy: stream");
     delete h;
     clk.mark("destroy: host state");
