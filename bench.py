@@ -304,6 +304,18 @@ def main():
         ms = float(t.item())
     ms_step = ms / args.steps
     value = m * args.steps / (ms / 1e3)
+    # per-solve device time for start vectors seeded 1..20 (median, p10, p90)
+    per = []
+    for sd in range(1, 21):
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        h.solve_async(sd, ev.data_ptr(), Y.data_ptr(), "f32")
+        q1.record(stream)
+        h.sync()
+        per.append(q0.elapsed_time(q1))
+    per_solve = {"seeds": "1..20", "median_ms": float(np.median(per)), "p10_ms": float(np.percentile(per, 10)),
+                 "p90_ms": float(np.percentile(per, 90))}
     h.close()
     # kernel breakdown pass: same workload, CUDA events around every kernel of part 0
     # recorded inside the graph on the solve stream
@@ -382,6 +394,7 @@ def main():
                              "algorithmic_bytes_per_launch": b_spmv, "avg_launch_ms": t_spmv,
                              "launches_timed": spmv_n,
                              "gather_bound": gather_bound(nnz_g, t_spmv)},
+                "per_solve": per_solve,
                 "kernels": kernels,
                 "kernel_breakdown_pass": {"steps": nprof, "ms_per_step_with_events": round(prof_ms_step, 4),
                                           "note": "per-kernel CUDA events inside the graph (part 0); "
