@@ -28,7 +28,10 @@ namespace topk {
 
 constexpr int kNT = 256;  // threads per block for the streaming kernels
 constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no shared memory)
-constexpr int kRitzKB = 8;  // Ritz outputs per thread
+#ifndef TOPK_RITZ_KB
+#define TOPK_RITZ_KB 8
+#endif
+constexpr int kRitzKB = TOPK_RITZ_KB;  // Ritz outputs per thread (dev knob, tools/build.py build_variant)
 constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
 constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
 
