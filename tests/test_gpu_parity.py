@@ -402,3 +402,15 @@ def test_periodic_reorth(T, c3s, storage, tol):
     a = T_all(T, c3s, K, storage, "f64", m, 6, reorth_period=1)
     b = T_all(T, c3s, K, storage, "f64", m, 6)
     assert np.array_equal(a, b)
+
+
+def test_bf16_vectors_report_only(T, c3s):
+    """bf16 vector storage (reading Q21: report-only, unstable as the paper says):
+    the bf16 kernels run end to end; the dominant, well separated eigenvalue is
+    still found to bf16 accuracy and the returned vectors are unit norm."""
+    ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=8, m=16, seed=2)
+    with T.TopkEig(c3s, 8, "bf16", "f64", values_storage="bf16", m=16) as h:
+        r = h.solve(seed=2, vectors=True, vec_dtype="f32")
+    assert r.info["k_found"] == 8 and np.all(np.isfinite(r.eigenvalues))
+    assert abs(r.eigenvalues[0] - ref.eigenvalues[0]) <= 1e-2 * abs(ref.eigenvalues[0])
+    assert np.allclose(np.linalg.norm(r.eigenvectors.astype(np.float64), axis=1), 1.0, atol=1e-3)
