@@ -1028,6 +1028,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
             CUDA_TRY(cudaFuncGetAttributes(&fa, k_jacobi<true>));
             h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
+            if (const char *ej = std::getenv("TOPK_JAC_THREADS"))  // dev knob (A/B)
+                h->jac_threads = std::max(32, std::min(h->jac_threads, std::atoi(ej) / 32 * 32));
         }
         // single CTA in shared memory for M <= 40; above that the cluster path is
         // faster (tools/jac_timing.py, profiles/r01_jacobi_timing.jsonl: m = 48 1.06 vs
