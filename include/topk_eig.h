@@ -77,7 +77,8 @@ typedef struct {
     uint32_t struct_size;
     int32_t krylov_dim;      /* m >= K Lanczos iterations; 0 -> K (the paper's "for i in 1, K", Alg.1 l.3) */
     int32_t reorth;          /* 1 full classical Gram-Schmidt (default; Alg.1 l.12-18 as full reorth,
-                                reading Q3), 2 CGS twice, -1 none (paper's optional mode) */
+                                reading Q3), 2 CGS twice, 3 partial (Simon's estimate decides per
+                                iteration, reading Q29), -1 none (paper's optional mode) */
     int32_t num_parts;       /* G row partitions. Single process: G virtual ranks on
                                 one device ("loopback"). Multi-process: must equal world. 0 -> 1     */
     int32_t device;          /* CUDA device ordinal of this process/handle                         */
@@ -135,7 +136,7 @@ typedef struct {
     int32_t converged_stop;   /* 1 if conv_tol stopped the iteration early                         */
     int32_t conv_checks;      /* convergence checks enqueued per solve                             */
     int32_t restarts;         /* thick restarts done (iterations then counts every Lanczos step)   */
-    int32_t reserved_;
+    int32_t reorth_passes;    /* reorth = 3: iterations that took the reorthogonalisation pass    */
 } topk_eig_info_t;
 
 /* Create a solver for M, K eigenpairs, storage/compute precision pair.

@@ -443,3 +443,67 @@ def solve_periodic(rowptr, col, val, K: int, m: int, period: int, seed: int = 1,
     Y = ritz(lz.V, S, idx) if want_vectors else None
     rest = np.abs(lz.beta[mf] * S[mf - 1, idx]) if mf > 0 else np.zeros(0)
     return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, rest, extra={"period": period})
+
+
+def solve_pro(rowptr, col, val, K: int, m: int, eps: float, seed: int = 1, v1vec=None,
+              tau: float = 1e-12, want_vectors: bool = True) -> SolveOut:
+    """Partial (selective) reorthogonalisation (SURVEY 8(f) NEXT-3, DESIGN.md reading Q29;
+    Simon, Math. Comp. 42 (1984); the paper makes reorthogonalisation optional,
+    PAPER.md:123). Every iteration is Alg.1's three-term step (O4 without reorth); the
+    level of orthogonality of the new vector is estimated by Simon's recurrence
+      beta_{j+1} w_{j+1,k} = beta_{k+1} w_{j,k+1} + (alpha_k - alpha_j) w_{j,k}
+                             + beta_k w_{j,k-1} - beta_j w_{j-1,k} + theta_{j,k},
+    theta_{j,k} = sign(.) eps (beta_{k+1} + beta_{j+1}) 0.3 (the deterministic worst case),
+    w_{j+1,j} = psi = eps sqrt(n), w_{j,j} = 1, with beta_{j+1} the norm before any
+    reorthogonalisation;
+    when max_k |w_{j+1,k}| > sqrt(eps) the new vector is fully reorthogonalised (MGS
+    against v_1..v_j, O5) and so is the next one, and the estimates of a
+    reorthogonalised vector are reset to psi. eps = unit roundoff of the vector storage.
+    extra["reorth_steps"] lists the reorthogonalised iterations."""
+    n = len(rowptr) - 1
+    if v1vec is None:
+        v1vec = v1(seed, n)
+    rp, c, v = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    u = _c(v1vec, np.float64)
+    V = np.zeros((m, n), np.float64)
+    V[0] = u / np.sqrt(np.add.accumulate(u * u)[-1])
+    vt, vn = np.zeros(n), np.zeros(n)
+    alpha, beta, ts = np.zeros(m), np.zeros(m + 1), np.zeros(1)
+    wp, wc = np.zeros(m + 2), np.zeros(m + 2)
+    wc[1] = 1.0                      # w_{1,1}
+    seps = np.sqrt(eps)
+    mf, bd, force, steps = m, False, False, []
+    for i in range(1, m + 1):
+        if _load().orc_lanczos_iter(n, _p(rp), _p(c), _p(v), i, 0, tau, _p(V), _p(vt), _p(vn),
+                                    _p(alpha), _p(beta), _p(ts)):
+            mf, bd = i - 1, True
+            break
+        b = float(np.sqrt(np.add.accumulate(vn * vn)[-1]))   # beta_{i+1} before reorth
+        ai, bi = alpha[i - 1], beta[i - 1]                    # alpha_i, beta_i
+        new = np.zeros(m + 2)
+        for k in range(1, i):
+            t = beta[k] * wc[k + 1] + (alpha[k - 1] - ai) * wc[k]
+            t = t + (beta[k - 1] * wc[k - 1] if k > 1 else 0.0)
+            t = t - bi * wp[k]
+            t = t + np.copysign(eps * (beta[k] + b) * 0.3, t)
+            new[k] = t / b
+        psi = eps * np.sqrt(n)
+        new[i] = psi
+        new[i + 1] = 1.0
+        thr = i > 1 and float(np.max(np.abs(new[1:i]))) > seps
+        if force or thr:
+            for j in range(1, i + 1):                          # O5: MGS against v_1..v_i
+                vj = V[j - 1]
+                vn -= float(np.add.accumulate(vj * vn)[-1]) * vj
+            new[1:i + 1] = psi
+            steps.append(i)
+        force = thr
+        wp, wc = wc, new
+    if not bd:
+        beta[m] = np.sqrt(np.add.accumulate(vn * vn)[-1])
+    lz = LanczosOut(alpha[:mf].copy(), beta[:mf + 1].copy(), V[:mf].copy(), mf, bd)
+    theta, S, sw, conv = jacobi(tridiag_dense(lz.alpha, lz.beta))
+    idx = select(theta, K)
+    Y = ritz(lz.V, S, idx) if want_vectors else None
+    rest = np.abs(lz.beta[mf] * S[mf - 1, idx]) if mf > 0 else np.zeros(0)
+    return SolveOut(theta[idx], Y, theta, S, idx, lz, sw, conv, rest, extra={"reorth_steps": steps})

@@ -393,6 +393,7 @@ struct StepArgs {
     Exch ex;
     int G, g, mode;
     int no_prev;        // first step after a thick restart: no beta_i v_{i-1} term (reading Q26)
+    const int *gate;    // partial reorthogonalisation (reading Q29): run only if *gate != 0
 };
 
 template <typename ST, typename CT, int JB>
@@ -534,6 +535,7 @@ __global__ void __launch_bounds__(kNT, 2) k_stepw(StepArgs a, int it, int j0) {
     __shared__ CT part[kNT / 32][NC];
     __shared__ int sflag;
     if (*(volatile int *)a.st.done) return;
+    if (a.gate && !*(volatile const int *)a.gate) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const ST *__restrict__ V = reinterpret_cast<const ST *>(a.V);
     const int64_t nvec = a.npad / VW;
@@ -626,6 +628,7 @@ struct CorrArgs {
     LzState st;
     Exch ex;
     int G, g, in_col;
+    const int *gate;    // partial reorthogonalisation (reading Q29): run only if *gate != 0
 };
 
 template <typename ST, typename CT>
@@ -636,6 +639,7 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     CT *red = reinterpret_cast<CT *>(red_storage);
     __shared__ int sflag;
     if (*(volatile int *)a.st.done) return;
+    if (a.gate && !*(volatile const int *)a.gate) return;
     const int tid = threadIdx.x;
     CT *coef = reinterpret_cast<CT *>(dsm);
     double *hd = dsm + a.ld;   // [it] raw dots H_j (fp64)
@@ -1806,6 +1810,72 @@ __global__ void __launch_bounds__(256) k_halo_pack(const EL *xg, int64_t nsend, 
 __global__ void k_restart_cond(cudaGraphConditionalHandle ch, const int *done, const int *restarts, int R) {
     if (threadIdx.x == 0)
         cudaGraphSetConditional(ch, (*(volatile const int *)done == 0 && *(volatile const int *)restarts < R) ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// Partial reorthogonalisation (reading Q29; Simon 1984):
+// after the three-term step of iteration `it`, Simon's recurrence estimates the
+// orthogonality w_{it+1,k} of the new vector against v_1..v_{it-1} (the oracle's order
+// of operations, no contraction); the pass (the CGS2 second-pass kernels on V[:, it])
+// runs when max |w| > sqrt(eps), and on the next vector too. Rows of w rotate in W[3].
+struct ProArgs {
+    LzState st;
+    Exch ex;
+    int G;
+    double eps, psi;   // storage unit roundoff; w_{j+1,j} = psi = eps sqrt(n)
+    double *W;         // [3][m + 2]
+    int *gate, *force, *count;
+};
+
+__global__ void __launch_bounds__(256) k_pro(ProArgs a, int it) {
+    __shared__ double s_b, s_max[8];
+    const int tid = threadIdx.x;
+    if (*(volatile int *)a.st.done) return;
+    const int ld = a.st.m + 2;
+    double *prev = a.W + (size_t)((it + 2) % 3) * ld, *cur = a.W + (size_t)(it % 3) * ld;
+    double *nw = a.W + (size_t)((it + 1) % 3) * ld;
+    if (it == 1) {
+        for (int k = tid; k < ld; k += blockDim.x) { prev[k] = 0.0; cur[k] = 0.0; }
+        __syncthreads();
+        if (tid == 0) { cur[1] = 1.0; *a.force = 0; *a.count = 0; }
+    }
+    if (tid == 0) {
+        double sq = 0.0;
+        for (int q = 0; q < a.G; ++q) sq += __ldcg(a.ex.norm_part + q);
+        s_b = sqrt(sq);  // beta_{it+1} before any reorthogonalisation
+    }
+    __syncthreads();
+    const double b = s_b, ai = a.st.alpha[it - 1], bi = a.st.beta[it - 1];
+    const double *al = a.st.alpha, *be = a.st.beta;
+    double mx = 0.0;
+    for (int k = 1 + tid; k < it; k += blockDim.x) {
+        double t = __dadd_rn(__dmul_rn(be[k], cur[k + 1]), __dmul_rn(__dsub_rn(al[k - 1], ai), cur[k]));
+        t = __dadd_rn(t, k > 1 ? __dmul_rn(be[k - 1], cur[k - 1]) : 0.0);
+        t = __dsub_rn(t, __dmul_rn(bi, prev[k]));
+        t = __dadd_rn(t, copysign(__dmul_rn(__dmul_rn(a.eps, __dadd_rn(be[k], b)), 0.3), t));
+        const double wv = __ddiv_rn(t, b);
+        nw[k] = wv;
+        mx = fmax(mx, fabs(wv));
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) s_max[tid >> 5] = mx;
+    __syncthreads();
+    __shared__ int s_do;
+    if (tid == 0) {
+        double m2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m2 = fmax(m2, s_max[w]);
+        nw[it] = a.psi;
+        nw[it + 1] = 1.0;
+        const int thr = (it > 1) && (m2 > sqrt(a.eps));
+        const int doit = *a.force || thr;
+        *a.gate = doit;
+        *a.force = thr;
+        if (doit) *a.count += 1;
+        s_do = doit;
+    }
+    __syncthreads();
+    if (s_do)
+        for (int k = 1 + tid; k <= it; k += blockDim.x) nw[k] = a.psi;
 }
 
 // ---------------------------------------------------------------------------

@@ -107,6 +107,8 @@ struct Part {
     int32_t *items = nullptr;
     void *yt = nullptr;            // Ritz output in position order, K values per row
     void *Vs = nullptr;            // thick restart scratch: keep columns (reading Q26)
+    int *pro_gate = nullptr, *pro_force = nullptr, *pro_count = nullptr;  // reading Q29 (state ints)
+    double *pro_w = nullptr;       // [3][m + 2] orthogonality estimates
     // halo exchange (reading Q27): compact SpMV input x_g = [own slot | remote entries]
     void *xg = nullptr;
     int64_t nhalo = 0;
@@ -385,9 +387,10 @@ static void stepw_grids(topk_eig_s *h) {
 }
 
 template <typename ST, typename CT>
-static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 0) {
+static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 0, const int *gate = nullptr) {
     StepArgs a;
     a.no_prev = no_prev;
+    a.gate = gate;
     a.y = p.y; a.w = p.w; a.V = p.V;
     a.vout = (char *)p.V + (size_t)it * p.npad * sizeof(ST);
     a.rep_slot = (mode == 1) ? rep_slot(h, p) : nullptr;
@@ -418,8 +421,9 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 
 }
 
 template <typename ST, typename CT>
-static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col) {
+static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int *gate = nullptr) {
     CorrArgs a;
+    a.gate = gate;
     a.w = p.w; a.V = p.V; a.rep_slot = rep_slot(h, p);
     a.npad = p.npad; a.ld = h->m + 1;
     a.slots = p.slots; a.counter = p.counters + 3;
@@ -475,6 +479,17 @@ static void launch_restart(topk_eig_s *h, bool decide = true) {
     }
 }
 
+static void launch_pro(topk_eig_s *h, Part &p, int it) {
+    ProArgs a;
+    a.st = p.st; a.ex = h->ex; a.G = h->G;
+    a.eps = h->vs == TOPK_F64 ? std::ldexp(1.0, -53) : h->vs == TOPK_F32 ? std::ldexp(1.0, -24) : std::ldexp(1.0, -8);
+    a.psi = a.eps * std::sqrt((double)h->n);
+    a.W = p.pro_w; a.gate = p.pro_gate; a.force = p.pro_force; a.count = p.pro_count;
+    k_pro<<<1, 256, 0, h->stream>>>(a, it);
+    CUDA_TRY(cudaGetLastError());
+    h->launches++;
+}
+
 template <typename VT, typename ST, typename CT>
 static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // a5: v1
@@ -500,6 +515,20 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     for (int it = it0; it <= h->m; ++it) {
         for (Part &p : h->parts) launch_spmv<VT, ST, CT>(h, p, it, nullptr);
         exch_alpha(h);
+        if (h->reorth == 3) {
+            // partial reorthogonalisation (reading Q29): three-term step, Simon's estimate,
+            // then the gated second pass (dots of u_{i+1} against V, correction in place)
+            for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 1);
+            exch_norm(h);
+            for (Part &p : h->parts) launch_pro(h, p, it);
+            for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 2, 0, p.pro_gate);
+            exch_h(h);
+            for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it, p.pro_gate);
+            exch_vec_norm(h);
+            if (h->keep == 0 && h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0)
+                launch_jacobi(h, 1);
+            continue;
+        }
         // reorth off (the paper's optional mode), or an iteration between two periodic
         // reorthogonalisations (reading Q28): the three-term step publishes u_{i+1}
         if (h->reorth < 0 || (h->period > 1 && it % h->period != 0 && (it == 1 || (it - 1) % h->period != 0))) {
@@ -649,7 +678,7 @@ static void set_kernels(topk_eig_s *h) {
         h->use_tma = !(e && e[0] == '1');
         // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed
         // restarts replace basis columns and periodic reorth skips the dots: explicit norm pass
-        h->use_gram = h->reorth != -1 && h->keep == 0 && h->period == 1;
+        h->use_gram = (h->reorth == 1 || h->reorth == 2) && h->keep == 0 && h->period == 1;
         const char *e2 = std::getenv("TOPK_TMA_CORRECT");
         h->tma_correct = e2 && e2[0] == '1';
         const char *e3 = std::getenv("TOPK_TMA_STEP");
@@ -683,7 +712,7 @@ static void carve_state(topk_eig_s *h, Part &p) {
     const int m = h->m, K = h->K;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
-    size_t o_int = take(8 * sizeof(int));
+    size_t o_int = take(12 * sizeof(int));
     size_t o_ts = take(sizeof(double));
     size_t o_alpha = take((size_t)m * 8), o_beta = take((size_t)(m + 2) * 8), o_scale = take((size_t)(m + 1) * 8);
     size_t o_theta = take((size_t)m * 8), o_evals = take((size_t)K * 8), o_resid = take((size_t)K * 8);
@@ -700,6 +729,10 @@ static void carve_state(topk_eig_s *h, Part &p) {
     p.st.jac_conv = ints + 4;
     p.st.arrow_k = ints + 5;
     p.st.restarts = ints + 6;
+    p.pro_gate = ints + 7;  // partial reorthogonalisation (reading Q29)
+    p.pro_force = ints + 8;
+    p.pro_count = ints + 9;
+    if (h->reorth == 3) p.pro_w = h->alloc<double>((size_t)3 * (m + 2));
     p.st.tscale = reinterpret_cast<double *>(b + o_ts);
     p.st.alpha = reinterpret_cast<double *>(b + o_alpha);
     p.st.beta = reinterpret_cast<double *>(b + o_beta);
@@ -902,7 +935,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     h->n = n; h->K = K; h->m = m; h->G = G; h->world = world; h->rank = world > 1 ? o.rank : 0;
     h->vs = storage; h->ms = ms; h->cs = compute;
     h->reorth = o.reorth == 0 ? 1 : o.reorth;
-    if (h->reorth != 1 && h->reorth != 2 && h->reorth != -1) return fail(TOPK_E_INVALID, "reorth must be 1, 2 or -1");
+    if (h->reorth != 1 && h->reorth != 2 && h->reorth != 3 && h->reorth != -1)
+        return fail(TOPK_E_INVALID, "reorth must be 1, 2, 3 or -1");
     h->tau = o.breakdown_tol > 0 ? o.breakdown_tol : (storage == TOPK_F64 ? 1e-12 : storage == TOPK_F32 ? 1e-6 : 1e-3);
     if (compute == TOPK_F32 && storage == TOPK_F64) return fail(TOPK_E_INVALID, "compute must be at least as precise as storage");
     if (!(o.conv_tol >= 0.0) || o.conv_check < 0) return fail(TOPK_E_INVALID, "conv_tol must be >= 0 and conv_check >= 0");
@@ -915,7 +949,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (o.restart_keep > 0) {
         if (o.restart_keep < K || o.restart_keep > m - 2 || o.restart_keep > 256)
             return fail(TOPK_E_INVALID, "restart_keep must be in [K, min(krylov_dim - 2, 256)]");
-        if (h->reorth < 0) return fail(TOPK_E_INVALID, "thick restart needs reorthogonalisation (reorth 1 or 2)");
+        if (h->reorth < 0 || h->reorth == 3) return fail(TOPK_E_INVALID, "thick restart needs full reorthogonalisation (reorth 1 or 2)");
         h->keep = o.restart_keep;
         h->max_restarts = o.max_restarts;
     }
@@ -1251,6 +1285,7 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     info->breakdown = done == 1;
     info->converged_stop = done == 2;
     info->conv_checks = h->conv_checks;
+    info->reorth_passes = (h->reorth == 3) ? hget<int>(p, p.pro_count) : 0;
     info->jacobi_sweeps = hget<int>(p, p.st.jac_sweeps);
     info->jacobi_converged = hget<int>(p, p.st.jac_conv);
     info->num_parts = h->G;

@@ -451,3 +451,22 @@ def test_row_length_boundaries(T, G):
     assert np.all(np.abs(y - yr) <= bound)
     ref = O.solve(A.rowptr, A.col, A.val, K=8, m=24, seed=2)
     check_solve(r, ref, 1e-8)
+
+
+@pytest.mark.parametrize("storage,tol", [("f64", 1e-8), ("f32", 1e-4)])
+def test_partial_reorth(T, c3s, storage, tol):
+    """Reading Q29: partial reorthogonalisation (reorth = 3) against oracle.solve_pro:
+    the same number of reorthogonalisation passes (the decisions come from Simon's
+    estimate in the same arithmetic order), Ritz values within the north-star
+    tolerances, and (fp64) far fewer passes than iterations."""
+    K, m, seed = 16, 64, 6
+    eps = 2.0 ** -53 if storage == "f64" else 2.0 ** -24
+    ref = O.solve_pro(c3s.rowptr, c3s.col, c3s.val, K, m, eps, seed=seed, tau=O.TAU[storage])
+    with T.TopkEig(c3s, K, storage, "f64", m=m, reorth=3) as h:
+        r = h.solve(seed=seed, vectors=False)
+        th = h.tridiag()[2]
+    assert r.info["reorth_passes"] == len(ref.extra["reorth_steps"]), (r.info["reorth_passes"], ref.extra["reorth_steps"])
+    # fp64 vectors: a fraction of the iterations; f32 vectors (eps = 2^-24) reach the
+    # sqrt(eps) level within a few steps, so most iterations take the pass
+    assert 0 < r.info["reorth_passes"] < (m // 2 if storage == "f64" else m)
+    assert normwise(th, ref.theta_all) <= tol

@@ -499,3 +499,24 @@ def test_p13_periodic_reorth_special_cases():
     assert orth(p4.lanczos.V) <= 1e-12 < orth(none.lanczos.V)
     nrm = np.abs(full.theta_all).max()
     assert np.abs(np.sort(p4.theta_all) - np.sort(full.theta_all)).max() <= 1e-12 * nrm
+
+
+# ---------------------------------------------------------------- P14 (partial reorth)
+def test_p14_partial_reorth_keeps_semi_orthogonality():
+    """solve_pro (reading Q29): Simon's estimate triggers reorthogonalisation of pairs
+    of consecutive vectors; the basis stays semi-orthogonal (<= 10 sqrt(eps), what the
+    scheme guarantees), the Ritz values equal the full-reorthogonalisation oracle to
+    1e-12 |theta_1|, and only a fraction of the iterations pay for the pass."""
+    A = S.rmat(12, 30_000, 3)
+    m, K, eps = 48, 8, 2.0 ** -53
+    full = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=4, reorth=1)
+    none = O.solve(A.rowptr, A.col, A.val, K, m=m, seed=4, reorth=0)
+    p = O.solve_pro(A.rowptr, A.col, A.val, K, m, eps, seed=4)
+    V = p.lanczos.V
+    assert np.abs(V @ V.T - np.eye(m)).max() <= 10 * np.sqrt(eps)
+    assert np.abs(none.lanczos.V @ none.lanczos.V.T - np.eye(m)).max() > 10 * np.sqrt(eps)
+    nrm = np.abs(full.theta_all).max()
+    assert np.abs(np.sort(p.theta_all) - np.sort(full.theta_all)).max() <= 1e-12 * nrm
+    st = p.extra["reorth_steps"]
+    assert 0 < len(st) < m // 2
+    assert all(b == a + 1 for a, b in zip(st[0::2], st[1::2]))
