@@ -631,15 +631,11 @@ struct CorrArgs {
     const int *gate;    // partial reorthogonalisation (reading Q29): run only if *gate != 0
 };
 
-template <typename ST, typename CT>
-__global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
-    constexpr int VW = Vw<ST>::N;
-    extern __shared__ double dsm[];  // coef[it]
-    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
-    CT *red = reinterpret_cast<CT *>(red_storage);
-    __shared__ int sflag;
-    if (*(volatile int *)a.st.done) return;
-    if (a.gate && !*(volatile const int *)a.gate) return;
+// a11 shared prologue: reorth coefficients c_j = H_j s_j^2 from the dots summed over
+// parts in rank order (shared memory: coef in CT, H and c in fp64), and block 0
+// extends the Gram matrix (reading Q24).
+template <typename CT>
+__device__ __forceinline__ void corr_prologue(const CorrArgs &a, int it, double *dsm) {
     const int tid = threadIdx.x;
     CT *coef = reinterpret_cast<CT *>(dsm);
     double *hd = dsm + a.ld;   // [it] raw dots H_j (fp64)
@@ -668,6 +664,20 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
         }
     }
     __syncthreads();
+}
+
+template <typename ST, typename CT>
+__global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
+    constexpr int VW = Vw<ST>::N;
+    extern __shared__ double dsm[];  // coef[it]
+    __shared__ double red_storage[kNT / 32];  // CT partials, or doubles for the final sums
+    CT *red = reinterpret_cast<CT *>(red_storage);
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    if (a.gate && !*(volatile const int *)a.gate) return;
+    const int tid = threadIdx.x;
+    CT *coef = reinterpret_cast<CT *>(dsm);
+    corr_prologue<CT>(a, it, dsm);
     ST *V = reinterpret_cast<ST *>(a.V);
     const ST *src = (a.in_col < 0) ? reinterpret_cast<const ST *>(a.w) : V + (size_t)a.in_col * a.npad;
     ST *dst = V + (size_t)it * a.npad;
@@ -700,6 +710,53 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
             const CT cj = coef[j];
 #pragma unroll
             for (int e = 0; e < VW; ++e) acc[e] -= cj * u[e];
+        }
+        vstore_back<ST, CT>(dst + v * VW, acc);
+        if (a.rep_slot) vstore<ST, CT>(reinterpret_cast<ST *>(a.rep_slot) + v * VW, acc);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) nrm += acc[e] * acc[e];
+    }
+    const CT tb = block_sum<CT, kNT>(nrm, red);
+    if (tid == 0) a.slots[blockIdx.x] = (double)tb;
+    if (arrive_last(a.counter, &sflag)) {
+        const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
+        if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
+    }
+}
+
+// a11 with a compile-time column count NC = it <= kStepMaxNC: every row-vector issues
+// all NC basis loads at once into raw registers (no 8-column batches), then the
+// subtractions in ascending j (the same order as k_correct).
+template <typename ST, typename CT, int NC>
+__global__ void __launch_bounds__(kNT) k_correctw(CorrArgs a, int it) {
+    constexpr int VW = Vw<ST>::N;
+    extern __shared__ double dsm[];
+    __shared__ double red_storage[kNT / 32];
+    CT *red = reinterpret_cast<CT *>(red_storage);
+    __shared__ int sflag;
+    if (*(volatile int *)a.st.done) return;
+    if (a.gate && !*(volatile const int *)a.gate) return;
+    const int tid = threadIdx.x;
+    const CT *coef = reinterpret_cast<const CT *>(dsm);
+    corr_prologue<CT>(a, it, dsm);
+    ST *V = reinterpret_cast<ST *>(a.V);
+    const ST *src = (a.in_col < 0) ? reinterpret_cast<const ST *>(a.w) : V + (size_t)a.in_col * a.npad;
+    ST *dst = V + (size_t)it * a.npad;
+    const int64_t nvec = a.npad / VW;
+    CT nrm = CT(0);
+    for (int64_t vv = (int64_t)blockIdx.x * kNT + tid; vv < nvec; vv += (int64_t)gridDim.x * kNT) {
+        const int64_t v = nvec - 1 - vv;  // descending: the columns k_stepw just read are in L2
+        uint4 u[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) u[q] = __ldg(reinterpret_cast<const uint4 *>(V + (size_t)q * a.npad + v * VW));
+        CT acc[VW];
+        vload<ST, CT>(src + v * VW, acc);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const ST *ue = reinterpret_cast<const ST *>(&u[q]);
+            const CT cj = coef[q];
+#pragma unroll
+            for (int e = 0; e < VW; ++e) acc[e] -= cj * cvt<CT>(ue[e]);
         }
         vstore_back<ST, CT>(dst + v * VW, acc);
         if (a.rep_slot) vstore<ST, CT>(reinterpret_cast<ST *>(a.rep_slot) + v * VW, acc);

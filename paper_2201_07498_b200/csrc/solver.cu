@@ -154,6 +154,8 @@ struct topk_eig_s {
     bool tma_correct = false;  // TOPK_TMA_CORRECT=1: TMA-ring k_correct_tma instead of k_correct
     bool tma_step = false;     // TOPK_TMA_STEP=1: TMA-ring k_step_tma instead of k_stepw
     int grid_stepw[kStepMaxNC + 1] = {0};
+    int grid_corrw[kStepMaxNC + 1] = {0};
+    bool corrw = true;                 // exact-width correction for it <= kStepMaxNC (TOPK_NO_CORRW=1: off)
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -420,6 +422,29 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 
     prof_end(h, p);
 }
 
+template <typename ST, typename CT, int NC>
+static void correctw_dispatch(topk_eig_s *h, const CorrArgs &a, int it, size_t smem) {
+    if constexpr (NC > kStepMaxNC) {
+        throw CudaFail("exact-width correction wider than kStepMaxNC");
+    } else {
+        if (it == NC) {
+            k_correctw<ST, CT, NC><<<h->grid_corrw[NC], kNT, smem, h->stream>>>(a, it);
+            CUDA_TRY(cudaGetLastError());
+        } else {
+            correctw_dispatch<ST, CT, NC + 1>(h, a, it, smem);
+        }
+    }
+}
+template <typename ST, typename CT, int NC>
+static void correctw_grids(topk_eig_s *h) {
+    if constexpr (NC <= kStepMaxNC) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_correctw<ST, CT, NC>, kNT, (size_t)3 * (h->m + 1) * 8);
+        h->grid_corrw[NC] = h->nsm * std::max(1, std::min(occ, 8));
+        correctw_grids<ST, CT, NC + 1>(h);
+    }
+}
+
 template <typename ST, typename CT>
 static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int *gate = nullptr) {
     CorrArgs a;
@@ -434,6 +459,8 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int
     // at it = 17, gpurun_out/r01n); k_correct_tma stays selectable for experiments
     if (it <= kTmaCols && h->use_tma && h->tma_correct)
         k_correct_tma<ST, CT><<<h->nsm, 256 * kCorrNG, kTmaSmem, h->stream>>>(a, it);
+    else if (it <= kStepMaxNC && h->corrw)
+        correctw_dispatch<ST, CT, 1>(h, a, it, smem);  // exact-width: all it basis loads in flight
     else
         k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
@@ -671,6 +698,7 @@ static void set_kernels(topk_eig_s *h) {
     h->grid_corr = h->nsm * std::max(1, std::min(occ4, 8));
     h->grid_stream = h->nsm * 4;
     stepw_grids<ST, CT, 1>(h);
+    correctw_grids<ST, CT, 1>(h);
     CUDA_TRY(cudaFuncSetAttribute(k_step_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_correct_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     {
@@ -958,6 +986,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
     if (o.exchange < 0 || o.exchange > 1) return fail(TOPK_E_INVALID, "exchange must be 0 (allgather) or 1 (halo)");
     h->halo = (G > 1 && o.exchange == 1);
+    if (const char *ec = std::getenv("TOPK_NO_CORRW")) h->corrw = !(ec[0] == '1');
     h->use_graph = o.use_graph >= 0;
     h->profile = o.profile > 0;
     h->device = o.device;
