@@ -34,6 +34,10 @@ constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no share
 constexpr int kRitzKB = TOPK_RITZ_KB;  // Ritz outputs per thread (dev knob, tools/build.py build_variant)
 constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
 constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
+#ifndef TOPK_CORR_MAXNC
+#define TOPK_CORR_MAXNC 17  // 24 measured the same on C3 (tools/lab/spmv_variants.py)
+#endif
+constexpr int kCorrMaxNC = TOPK_CORR_MAXNC;  // widest exact-width correction (k_correctw)
 
 struct LzState {
     double *alpha;      // [m]     alpha_1..alpha_m
@@ -724,7 +728,7 @@ __global__ void __launch_bounds__(kNT) k_correct(CorrArgs a, int it) {
     }
 }
 
-// a11 with a compile-time column count NC = it <= kStepMaxNC: every row-vector issues
+// a11 with a compile-time column count NC = it <= kCorrMaxNC: every row-vector issues
 // all NC basis loads at once into raw registers (no 8-column batches), then the
 // subtractions in ascending j (the same order as k_correct).
 template <typename ST, typename CT, int NC>

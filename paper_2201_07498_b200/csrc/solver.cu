@@ -154,8 +154,8 @@ struct topk_eig_s {
     bool tma_correct = false;  // TOPK_TMA_CORRECT=1: TMA-ring k_correct_tma instead of k_correct
     bool tma_step = false;     // TOPK_TMA_STEP=1: TMA-ring k_step_tma instead of k_stepw
     int grid_stepw[kStepMaxNC + 1] = {0};
-    int grid_corrw[kStepMaxNC + 1] = {0};
-    bool corrw = true;                 // exact-width correction for it <= kStepMaxNC (TOPK_NO_CORRW=1: off)
+    int grid_corrw[kCorrMaxNC + 1] = {0};
+    bool corrw = true;                 // exact-width correction for it <= kCorrMaxNC (TOPK_NO_CORRW=1: off)
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -424,8 +424,8 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 
 
 template <typename ST, typename CT, int NC>
 static void correctw_dispatch(topk_eig_s *h, const CorrArgs &a, int it, size_t smem) {
-    if constexpr (NC > kStepMaxNC) {
-        throw CudaFail("exact-width correction wider than kStepMaxNC");
+    if constexpr (NC > kCorrMaxNC) {
+        throw CudaFail("exact-width correction wider than kCorrMaxNC");
     } else {
         if (it == NC) {
             k_correctw<ST, CT, NC><<<h->grid_corrw[NC], kNT, smem, h->stream>>>(a, it);
@@ -437,7 +437,7 @@ static void correctw_dispatch(topk_eig_s *h, const CorrArgs &a, int it, size_t s
 }
 template <typename ST, typename CT, int NC>
 static void correctw_grids(topk_eig_s *h) {
-    if constexpr (NC <= kStepMaxNC) {
+    if constexpr (NC <= kCorrMaxNC) {
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_correctw<ST, CT, NC>, kNT, (size_t)3 * (h->m + 1) * 8);
         h->grid_corrw[NC] = h->nsm * std::max(1, std::min(occ, 8));
@@ -459,7 +459,7 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int
     // at it = 17, gpurun_out/r01n); k_correct_tma stays selectable for experiments
     if (it <= kTmaCols && h->use_tma && h->tma_correct)
         k_correct_tma<ST, CT><<<h->nsm, 256 * kCorrNG, kTmaSmem, h->stream>>>(a, it);
-    else if (it <= kStepMaxNC && h->corrw)
+    else if (it <= kCorrMaxNC && h->corrw)
         correctw_dispatch<ST, CT, 1>(h, a, it, smem);  // exact-width: all it basis loads in flight
     else
         k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
