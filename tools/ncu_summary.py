@@ -28,6 +28,7 @@ KEYS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
@@ -78,8 +79,10 @@ def full_metrics(tag_dir):
         hdr, units, vals = rows[0], rows[1], rows[2]
         d = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else m.group(1)}
         for key, label in KEYS:
-            if key in hdr:
-                d[label] = (vals[hdr.index(key)], units[hdr.index(key)])
+            # exact column, else a section-prefixed one (e.g. "FBSP.TriageCompute.<key>")
+            idx = hdr.index(key) if key in hdr else next((i for i, h in enumerate(hdr) if h.endswith("." + key)), None)
+            if idx is not None:
+                d[label] = (vals[idx], units[idx])
         res[m.group(1)] = d
     return res
 
