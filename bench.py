@@ -384,7 +384,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": N, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_of(wl, A, N),
+                "config": dict(config_of(wl, A, N), **({"exchange": args.exchange} if N > 1 else {})),
                 "time_to_topk_ms": ms_step,
                 "time_to_topk": ttk,
                 "spmv_hbm_gbs": spmv_gbs, "spmv_pct_of_8tbs": 100 * spmv_gbs / HBM_NOMINAL_GBS,
