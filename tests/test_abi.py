@@ -175,3 +175,35 @@ def test_physical_format_unpacks_to_logical(G):
         covered = np.concatenate([np.arange(a, b_) for a, b_ in it]) if len(it) else np.zeros(0, int)
         assert np.array_equal(covered, np.arange(nsl))
 
+
+
+@pytest.mark.skipif(has_gpu(), reason="uses the no-device status to see that the symmetry check passed")
+def test_symmetry_check_hash_multiset():
+    """Row a2 (reading Q17): the multiset-hash symmetry check accepts a symmetric
+    R-MAT and rejects one-bit, one-entry and swapped-value perturbations of it."""
+    import paper_2201_07498_b200 as T
+    A = S.rmat(13, 60_000, 7)
+    with pytest.raises(T.TopkError) as e:
+        T.TopkEig(A, 4, "f64", "f64")
+    assert e.value.status == 8  # symmetric: passes the check, then no device
+
+    def variant(kind):
+        rp, col, val = A.rowptr.copy(), A.col.copy(), A.val.copy()
+        r = int(np.argmax(np.diff(rp) > 3))
+        k = int(rp[r]) + 1
+        if kind == "bit":
+            val[k] = np.nextafter(val[k], np.inf)
+        elif kind == "swap":
+            j = k + 1
+            val[k], val[j] = val[j], val[k] + 1.0 / 128
+        else:  # drop one off-diagonal entry
+            col = np.delete(col, k)
+            val = np.delete(val, k)
+            rp = rp.copy()
+            rp[r + 1:] -= 1
+        return S.CSR(A.n, rp, col, val)
+
+    for kind in ("bit", "swap", "drop"):
+        with pytest.raises(T.TopkError) as e:
+            T.TopkEig(variant(kind), 4, "f64", "f64")
+        assert e.value.status == 3, kind
