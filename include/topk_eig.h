@@ -15,6 +15,9 @@
  * All steps run in hand-written sm_100a CUDA kernels owned by the handle.
  * Arithmetic is fp64 inside every kernel with vectors stored in the storage
  * dtype ("mixed precision": FDF = f32 storage, f64 compute).
+ * Options beyond the paper's fixed-m iteration (all off by default; DESIGN.md
+ * readings Q25-Q29): convergence-driven stop, thick restart, halo exchange,
+ * periodic and partial reorthogonalisation (see topk_eig_opts_t).
  *
  * Conventions for every entry point
  *   - Returns topk_status_t; no exception or signal crosses the ABI. On error a
