@@ -123,6 +123,16 @@ typedef struct {
      * kp and kp + 1 only (Grcar's periodic scheme); the others are the plain three-term step.
      * 0/1 -> every iteration. Not with thick restart. */
     int32_t reorth_period;
+    /* kernel-path selection (no environment variables are read by the library; these
+     * exist for A/B measurements and the tests that cover every path):
+     * jacobi_path 0 -> auto (one CTA in shared memory for m <= 40, else a thread-block
+     * cluster, else one CTA in global memory), 1 -> one CTA only, 2 -> cluster at any m;
+     * jacobi_cluster 0 -> auto (8 CTAs, 16 from m = 96), 8 or 16 -> that size first;
+     * restart_loop 0 -> thick-restart cycles in a CUDA-graph WHILE node when the solve is
+     * captured, 1 -> unrolled cycles. */
+    int32_t jacobi_path;
+    int32_t jacobi_cluster;
+    int32_t restart_loop;
 } topk_eig_opts_t;
 
 typedef struct {
@@ -255,6 +265,13 @@ topk_status_t topk_eig_export_tridiag(topk_eig_t h, double *alpha, double *beta,
  * s_j * u_j[r] for j < m'+1 (m'+1 columns when no breakdown), i.e. the
  * normalised v_{j+1} (host, (m'+1) * n_p doubles). */
 topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32_t *ncols);
+/* After a solve: the stored basis columns of part p WITHOUT the deferred scale s_j,
+ * converted exactly from the storage dtype to double: U[j * n_p + r] = u_j[r]. Column 0
+ * is the unnormalised start vector u_r = 2 U(h3(seed, 0x7631, row0 + r)) - 1 (reading
+ * Q8) rounded once to the storage dtype, the quantity the parity
+ * contract compares bit for bit with the oracle's orc_v1. Same sizes and
+ * NULL rules as topk_eig_export_basis. */
+topk_status_t topk_eig_export_basis_raw(topk_eig_t h, int32_t part, double *U, int32_t *ncols);
 /* One SpMV y = M x through the device kernel on part-local rows (x, y host, n
  * doubles, global indexing; x is rounded to the storage dtype first, y is the
  * fp64 row sums before storage rounding). */

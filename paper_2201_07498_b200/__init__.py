@@ -51,7 +51,8 @@ class _Opts(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("conv_tol", ctypes.c_double),
                 ("conv_check", ctypes.c_int32), ("restart_keep", ctypes.c_int32),
                 ("max_restarts", ctypes.c_int32), ("exchange", ctypes.c_int32),
-                ("reorth_period", ctypes.c_int32)]
+                ("reorth_period", ctypes.c_int32), ("jacobi_path", ctypes.c_int32),
+                ("jacobi_cluster", ctypes.c_int32), ("restart_loop", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -87,6 +88,7 @@ _SIGS = {
     "topk_eig_export_layout": (_S, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "topk_eig_export_tridiag": (_S, [_P, _P, _P, _P, _P]),
     "topk_eig_export_basis": (_S, [_P, _I32, _P, _P]),
+    "topk_eig_export_basis_raw": (_S, [_P, _I32, _P, _P]),
     "topk_eig_debug_spmv": (_S, [_P, _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -208,7 +210,8 @@ class TopkEig:
                  breakdown_tol: float = 0.0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, profile: bool = False,
                  conv_tol: float = 0.0, conv_check: int = 0, restart_keep: int = 0,
-                 max_restarts: int = 0, exchange: str = "allgather", reorth_period: int = 0):
+                 max_restarts: int = 0, exchange: str = "allgather", reorth_period: int = 0,
+                 jacobi_path: str = "auto", jacobi_cluster: int = 0, restart_loop: str = "auto"):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -232,6 +235,9 @@ class TopkEig:
         o.max_restarts = int(max_restarts)
         o.exchange = {"allgather": 0, "halo": 1}[exchange]
         o.reorth_period = int(reorth_period)
+        o.jacobi_path = {"auto": 0, "single": 1, "cluster": 2}[jacobi_path]
+        o.jacobi_cluster = int(jacobi_cluster)
+        o.restart_loop = {"auto": 0, "unrolled": 1}[restart_loop]
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -302,14 +308,17 @@ class TopkEig:
         _check(_lib.topk_eig_export_tridiag(self._h, _ptr(a), _ptr(b), _ptr(t), None))
         return a[:mm], b, t[:mm]
 
-    def basis(self, part: int = 0) -> np.ndarray:
+    def basis(self, part: int = 0, raw: bool = False) -> np.ndarray:
+        """Stored basis of `part` (part-local rows, original order): the normalised
+        v_j (topk_eig_export_basis), or with raw=True the unscaled stored u_j
+        (topk_eig_export_basis_raw; column 0 = the unnormalised start vector)."""
+        fn = _lib.topk_eig_export_basis_raw if raw else _lib.topk_eig_export_basis
         nc = ctypes.c_int32()
-        _check(_lib.topk_eig_export_basis(self._h, part, None, ctypes.byref(nc)))
-        _, _, _, _ = None, None, None, None
+        _check(fn(self._h, part, None, ctypes.byref(nc)))
         rp, _c, _v, _np = self.layout(part)
         nrows = len(rp) - 1
         V = np.zeros((nc.value, nrows), np.float64)
-        _check(_lib.topk_eig_export_basis(self._h, part, _ptr(V), None))
+        _check(fn(self._h, part, _ptr(V), None))
         return V
 
     def debug_spmv(self, x) -> np.ndarray:

@@ -55,7 +55,7 @@ struct LzState {
     double *resid;      // [K]
     double *gram;       // [m*m] G_jl = u_j . u_l of the stored (unnormalised) basis, summed over parts
     double *rnrm2;      // [K] ||y_k||^2 of the selected Ritz vectors from the Gram matrix
-    int use_gram;       // 1: Ritz norms from the Gram matrix (k_step_tma path), 0: Ritz pass 0
+    int use_gram;       // 1: Ritz norms from the Gram matrix (reading Q24), 0: Ritz pass 0
     int m;
     double tau;
     // thick restart (reading Q26): after a restart T is [[diag(theta), b], [b^T, tridiag]]
@@ -771,292 +771,6 @@ __global__ void __launch_bounds__(kNT) k_correctw(CorrArgs a, int it) {
     if (tid == 0) a.slots[blockIdx.x] = (double)tb;
     if (arrive_last(a.counter, &sflag)) {
         const double tot = block_sum_array<double, kNT>(a.slots, gridDim.x, 1, red_storage);
-        if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-pipelined a9 / a11 for it <= kTmaCols basis columns (the whole paper mode
-// at K <= 24). A persistent CTA per SM walks tiles of R = 4096 B / s rows; for
-// each tile one elected thread issues cp.async.bulk copies of the tile's slice
-// of every needed column (y or w, and V[0..it-1]) into a 2-stage shared-memory
-// ring completed by an mbarrier (tx bytes), so up to ~200 KB per SM are in
-// flight without register cost; the 256 threads then read one 16-byte vector
-// per column per tile from shared memory. Same arithmetic, rounding points and
-// reduction order as k_step / k_correct (deterministic).
-constexpr int kTmaCols = 24;
-constexpr int kTmaColBytes = 4096;
-// shared-memory stride of a staged column: 4 KB + 128/NG bytes, so within each
-// quarter-warp (8 lanes = 8 / NG row-vectors x NG columns, one 128-bit wavefront)
-// the NG column reads of a row-vector land in different 16-byte bank groups
-__host__ __device__ constexpr int tma_col_stride(int ng) { return kTmaColBytes + 128 / ng; }
-constexpr size_t kTmaSmem = (size_t)2 * (kTmaCols + 1) * (kTmaColBytes + 128);
-
-template <typename ST, typename CT>
-__device__ __forceinline__ void sload(const unsigned char *p, CT (&o)[Vw<ST>::N]) {
-    const uint4 raw = *reinterpret_cast<const uint4 *>(p);
-    const ST *e = reinterpret_cast<const ST *>(&raw);
-#pragma unroll
-    for (int q = 0; q < Vw<ST>::N; ++q) o[q] = cvt<CT>(e[q]);
-}
-
-// Issue one tile's column slices: column c of the stage <- src[c] + off (bytes each).
-// Called by all 32 lanes of one warp: lane 0 arms the barrier with the total tx
-// bytes (its single arrival), the lanes issue the column copies in parallel (the
-// mbarrier tx count may transiently go negative within the phase).
-__device__ __forceinline__ void tma_issue(unsigned char *stage, uint64_t *bar, const unsigned char *const *src,
-                                          int ncol, size_t off, unsigned bytes, int stride) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) mbar_expect_tx(bar, bytes * (unsigned)ncol);
-    for (int c = lane; c < ncol; c += 32) bulk_g2s(stage + (size_t)c * stride, src[c] + off, bytes, bar);
-}
-
-// Thread layout of the TMA kernels: NT = 256 * NG threads; thread t owns the
-// 16-byte row-vector v = t / NG of the tile and the basis columns j with
-// j % NG == t % NG (the NG partners of a row-vector are adjacent lanes of one
-// warp), so more warps share the per-tile work.
-constexpr int kStepNG = 2, kCorrNG = 4;
-
-template <typename ST, typename CT>
-__global__ void __launch_bounds__(256 * kStepNG, 1) k_step_tma(StepArgs a, int it) {
-    constexpr int NG = kStepNG, NT = 256 * NG, JPG = kTmaCols / NG;
-    constexpr int kTmaColStride = tma_col_stride(NG);
-    constexpr int VW = Vw<ST>::N;
-    constexpr int R = kTmaColBytes / (int)sizeof(ST);  // rows per tile = 256 * VW
-    extern __shared__ __align__(128) unsigned char tsm[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ const unsigned char *srcp[kTmaCols + 1];
-    __shared__ CT part[NT / 32][kTmaCols];
-    __shared__ int sflag;
-    if (*(volatile int *)a.st.done) return;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int grp = tid % NG, vt = tid / NG;
-    CT c1 = CT(0), c2 = CT(0);
-    if (a.mode != 2) {
-        double al = 0.0;
-        for (int q = 0; q < a.G; ++q) al += __ldcg(a.ex.alpha_part + q);  // l.10, rank order
-        const double bi = a.st.beta[it - 1];
-        if (blockIdx.x == 0 && tid == 0) {
-            a.st.alpha[it - 1] = al;
-            double ts = *a.st.tscale;
-            ts = fmax(ts, fabs(al));
-            ts = fmax(ts, bi);
-            *a.st.tscale = ts;
-        }
-        c1 = (CT)(al * a.st.scale[it - 1]);
-        c2 = (it > 1 && !a.no_prev) ? (CT)(bi * a.st.scale[it - 2]) : CT(0);
-    }
-    const ST *V = reinterpret_cast<const ST *>(a.V);
-    ST *wv = reinterpret_cast<ST *>(a.w);
-    const int ncol = it + 1;  // [base][V0 .. V(it-1)], base = y (mode 0) or V[:, it] (mode 2)
-    if (tid == 0) {
-        srcp[0] = reinterpret_cast<const unsigned char *>(a.mode == 2 ? V + (size_t)it * a.npad
-                                                                      : reinterpret_cast<const ST *>(a.y));
-        for (int j = 0; j < it; ++j) srcp[j + 1] = reinterpret_cast<const unsigned char *>(V + (size_t)j * a.npad);
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const int64_t ntiles = (a.npad + R - 1) / R;
-    auto issue = [&](int64_t t, int stg) {
-        const int64_t r0 = t * R;
-        const int64_t rows = (a.npad - r0 < (int64_t)R) ? a.npad - r0 : (int64_t)R;
-        tma_issue(tsm + (size_t)stg * (kTmaCols + 1) * kTmaColStride, &bar[stg], srcp, ncol,
-                  (size_t)r0 * sizeof(ST), (unsigned)(rows * (int64_t)sizeof(ST)), kTmaColStride);
-    };
-    if (tid < 32) {
-        if ((int64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-        if ((int64_t)blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
-    }
-    // reorth dots u_j . w and Gram dots u_j . u_it (j < it - 1) for this thread's columns
-    CT acc[JPG], gacc[JPG];
-#pragma unroll
-    for (int q = 0; q < JPG; ++q) acc[q] = gacc[q] = CT(0);
-    const bool gram = false;  // Gram entries come from the k_correct recursion (Q24)
-    int k = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int stg = k & 1;
-        mbar_wait(&bar[stg], (unsigned)((k >> 1) & 1));
-        const unsigned char *stage = tsm + (size_t)stg * (kTmaCols + 1) * kTmaColStride + (size_t)vt * 16;
-        const int64_t row = t * R + (int64_t)vt * VW;
-        if (row < a.npad) {
-            CT w[VW], u1[VW];
-            sload<ST, CT>(stage, w);
-            if (a.mode != 2) {
-                CT u0[VW];
-                sload<ST, CT>(stage + (size_t)it * kTmaColStride, u1);  // V[it-1] = u_i
-                if (it > 1) sload<ST, CT>(stage + (size_t)(it - 1) * kTmaColStride, u0);
-#pragma unroll
-                for (int q = 0; q < VW; ++q) w[q] = w[q] - c1 * u1[q] - (it > 1 ? c2 * u0[q] : CT(0));
-                // w rounded once (every group rounds identically); dots use what is stored
-                if (grp == 0) vstore_back<ST, CT>(wv + row, w);
-                else round_back<ST, CT>(w);
-            }
-#pragma unroll
-            for (int q = 0; q < JPG; ++q) {
-                const int j = grp + NG * q;
-                if (j < it) {
-                    CT u[VW];
-                    sload<ST, CT>(stage + (size_t)(j + 1) * kTmaColStride, u);
-                    CT d = CT(0), gd = CT(0);
-#pragma unroll
-                    for (int e = 0; e < VW; ++e) d += u[e] * w[e];
-                    acc[q] += d;
-                    if (gram && j < it - 1) {
-#pragma unroll
-                        for (int e = 0; e < VW; ++e) gd += u[e] * u1[e];
-                        gacc[q] += gd;
-                    }
-                }
-            }
-        }
-        __syncthreads();  // every thread is done with this stage
-        if (tid < 32 && t + 2 * (int64_t)gridDim.x < ntiles) issue(t + 2 * (int64_t)gridDim.x, stg);
-    }
-    // block partials: column j of group g = j % NG; reduce over the lanes of the
-    // same group (xor offsets >= NG), then over the warps
-    const int ng = gram ? it - 1 : 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int ncols = pass == 0 ? it : ng;
-#pragma unroll
-        for (int q = 0; q < JPG; ++q) {
-            CT v = pass == 0 ? acc[q] : gacc[q];
-#pragma unroll
-            for (int o = 16; o >= NG; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            const int j = grp + NG * q;
-            if (lane < NG && j < ncols) part[wid][j] = v;
-        }
-        __syncthreads();
-        for (int j = tid; j < ncols; j += NT) {
-            CT r = CT(0);
-#pragma unroll
-            for (int w8 = 0; w8 < NT / 32; ++w8) r += part[w8][j];
-            a.slots[(size_t)blockIdx.x * 2 * a.ld + (pass == 0 ? 0 : a.ld) + j] = (double)r;
-        }
-        __syncthreads();
-    }
-    if (arrive_last(a.counter, &sflag)) {
-        for (int j = wid; j < it + ng; j += NT / 32) {
-            const int col = j < it ? j : a.ld + (j - it);
-            double r = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) r += __ldcg(a.slots + (size_t)b * 2 * a.ld + col);
-            r = warp_sum(r);
-            if (lane == 0) a.ex.hpart[(size_t)a.g * 2 * a.ld + col] = r;
-        }
-        __syncthreads();
-        if (tid == 0) *a.counter = 0u;
-    }
-}
-
-template <typename ST, typename CT>
-__global__ void __launch_bounds__(256 * kCorrNG, 1) k_correct_tma(CorrArgs a, int it) {
-    constexpr int NG = kCorrNG, NT = 256 * NG, JPG = kTmaCols / NG;
-    constexpr int kTmaColStride = tma_col_stride(NG);
-    constexpr int VW = Vw<ST>::N;
-    constexpr int R = kTmaColBytes / (int)sizeof(ST);
-    extern __shared__ __align__(128) unsigned char tsm[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ const unsigned char *srcp[kTmaCols + 1];
-    __shared__ CT coef[kTmaCols];
-    __shared__ double red_storage[NT / 32];
-    CT *red = reinterpret_cast<CT *>(red_storage);
-    __shared__ int sflag;
-    if (*(volatile int *)a.st.done) return;
-    const int tid = threadIdx.x;
-    const int grp = tid % NG, vt = tid / NG;
-    __shared__ double hd[kTmaCols], cd[kTmaCols];
-    for (int j = tid; j < it; j += NT) {
-        double h = 0.0;
-        for (int q = 0; q < a.G; ++q) h += __ldcg(a.ex.hpart + (size_t)q * 2 * a.ld + j);
-        const double sj = a.st.scale[j];
-        coef[j] = (CT)(h * sj * sj);
-        hd[j] = h;
-        cd[j] = h * sj * sj;
-    }
-    __syncthreads();
-    if (blockIdx.x == 0 && a.st.use_gram && it < a.st.m) {  // Gram recursion, as in k_correct
-        const int m = a.st.m;
-        for (int j = tid; j < it; j += NT) {
-            double g = hd[j];
-            for (int l = 0; l < it; ++l) g -= cd[l] * a.st.gram[(size_t)j * m + l];
-            a.st.gram[(size_t)j * m + it] = g;
-            a.st.gram[(size_t)it * m + j] = g;
-        }
-    }
-    ST *V = reinterpret_cast<ST *>(a.V);
-    ST *dst = V + (size_t)it * a.npad;
-    const int ncol = it + 1;  // [w or V[:, in_col]][V0 .. V(it-1)]
-    if (tid == 0) {
-        srcp[0] = reinterpret_cast<const unsigned char *>(a.in_col < 0 ? reinterpret_cast<const ST *>(a.w)
-                                                                       : V + (size_t)a.in_col * a.npad);
-        for (int j = 0; j < it; ++j) srcp[j + 1] = reinterpret_cast<const unsigned char *>(V + (size_t)j * a.npad);
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const int64_t ntiles = (a.npad + R - 1) / R;
-    // tiles in DESCENDING order: k_step just streamed the same columns ascending,
-    // so the most recently read ones are still L2-resident
-    auto tile_of = [&](int64_t kk) { return ntiles - 1 - ((int64_t)blockIdx.x + kk * gridDim.x); };
-    auto issue = [&](int64_t t, int stg) {
-        const int64_t r0 = t * R;
-        const int64_t rows = (a.npad - r0 < (int64_t)R) ? a.npad - r0 : (int64_t)R;
-        tma_issue(tsm + (size_t)stg * (kTmaCols + 1) * kTmaColStride, &bar[stg], srcp, ncol,
-                  (size_t)r0 * sizeof(ST), (unsigned)(rows * (int64_t)sizeof(ST)), kTmaColStride);
-    };
-    const int64_t nmine = ((int64_t)blockIdx.x < ntiles) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    if (tid < 32) {
-        if (nmine > 0) issue(tile_of(0), 0);
-        if (nmine > 1) issue(tile_of(1), 1);
-    }
-    CT nrm = CT(0);
-    for (int64_t k = 0; k < nmine; ++k) {
-        const int stg = (int)(k & 1);
-        const int64_t t = tile_of(k);
-        mbar_wait(&bar[stg], (unsigned)((k >> 1) & 1));
-        const unsigned char *stage = tsm + (size_t)stg * (kTmaCols + 1) * kTmaColStride + (size_t)vt * 16;
-        const int64_t row = t * R + (int64_t)vt * VW;
-        const bool live = row < a.npad;  // warp-uniform per group of NG lanes
-        // group partial -sum_{j = grp mod NG} c_j u_j, then base + sum of the NG partials
-        CT acc[VW];
-#pragma unroll
-        for (int e = 0; e < VW; ++e) acc[e] = CT(0);
-        if (live) {
-#pragma unroll
-            for (int q = 0; q < JPG; ++q) {
-                const int j = grp + NG * q;
-                if (j < it) {
-                    CT u[VW];
-                    sload<ST, CT>(stage + (size_t)(j + 1) * kTmaColStride, u);
-                    const CT cj = coef[j];
-#pragma unroll
-                    for (int e = 0; e < VW; ++e) acc[e] -= cj * u[e];
-                }
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < VW; ++e)
-#pragma unroll
-            for (int o = 1; o < NG; o <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-        if (live && grp == 0) {
-            CT b[VW];
-            sload<ST, CT>(stage, b);
-#pragma unroll
-            for (int e = 0; e < VW; ++e) acc[e] = b[e] + acc[e];
-            vstore_back<ST, CT>(dst + row, acc);
-            if (a.rep_slot) vstore<ST, CT>(reinterpret_cast<ST *>(a.rep_slot) + row, acc);
-#pragma unroll
-            for (int e = 0; e < VW; ++e) nrm += acc[e] * acc[e];
-        }
-        __syncthreads();
-        if (tid < 32 && k + 2 < nmine) issue(tile_of(k + 2), stg);
-    }
-    const CT tb = block_sum<CT, NT>(nrm, red);
-    if (tid == 0) a.slots[blockIdx.x] = (double)tb;
-    if (arrive_last(a.counter, &sflag)) {
-        const double tot = block_sum_array<double, NT>(a.slots, gridDim.x, 1, red_storage);
         if (tid == 0) { a.ex.norm_part[a.g] = tot; *a.counter = 0u; }
     }
 }

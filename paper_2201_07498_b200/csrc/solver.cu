@@ -149,13 +149,15 @@ struct topk_eig_s {
     int use_graph = 1;
     int nsm = 148;
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
-    bool use_tma = true;  // TMA-pipelined k_step / k_correct for it <= kTmaCols (TOPK_NO_TMA=1: off)
-    bool use_gram = false;  // Ritz norms from the Gram matrix the TMA multi-dot computes (no Ritz pass 0)
-    bool tma_correct = false;  // TOPK_TMA_CORRECT=1: TMA-ring k_correct_tma instead of k_correct
-    bool tma_step = false;     // TOPK_TMA_STEP=1: TMA-ring k_step_tma instead of k_stepw
+    bool use_gram = false;  // Ritz norms from the Gram matrix (reading Q24; no Ritz pass 0)
     int grid_stepw[kStepMaxNC + 1] = {0};
     int grid_corrw[kCorrMaxNC + 1] = {0};
-    bool corrw = true;                 // exact-width correction for it <= kCorrMaxNC (TOPK_NO_CORRW=1: off)
+#ifdef TOPK_NO_CORRW
+    bool corrw = false;                // dev build variant: k_correct at every width
+#else
+    bool corrw = true;                 // exact-width correction for it <= kCorrMaxNC
+#endif
+    bool restart_unrolled = false;     // opts.restart_loop = 1: unrolled restart cycles, no WHILE node
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -188,6 +190,13 @@ struct topk_eig_s {
     void (*enqueue)(topk_eig_s *, bool) = nullptr;
     void (*spmv_only)(topk_eig_s *, Part &) = nullptr;
     std::vector<void *> allocs;
+
+    topk_eig_s() = default;
+    topk_eig_s(const topk_eig_s &) = delete;
+    topk_eig_s &operator=(const topk_eig_s &) = delete;
+    // Releases everything the handle owns, also after a failed create (any prefix of
+    // the set-up): graph, NCCL comm, pool blocks, events, streams.
+    ~topk_eig_s();
 
     template <typename T> T *alloc(size_t count) {
         size_t bytes = std::max<size_t>(count * sizeof(T), 256);
@@ -404,10 +413,6 @@ static void launch_step(topk_eig_s *h, Part &p, int it, int mode, int no_prev = 
         k_step<ST, CT, kStepJB><<<h->grid_step, kNT, 0, h->stream>>>(a, it);
         CUDA_TRY(cudaGetLastError());
         h->launches++;
-    } else if (h->use_tma && h->tma_step && it <= kTmaCols) {
-        k_step_tma<ST, CT><<<h->nsm, 256 * kStepNG, kTmaSmem, h->stream>>>(a, it);
-        CUDA_TRY(cudaGetLastError());
-        h->launches++;
     } else {
         // exact-width passes: one pass up to 17 columns, else balanced passes of <= 16
         const int npass = (it <= kStepMaxNC) ? 1 : (it + 15) / 16;
@@ -455,11 +460,9 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g; a.in_col = in_col;
     size_t smem = (size_t)3 * (h->m + 1) * sizeof(double);
     prof_begin(h, p, 3);
-    // the register-pipelined correction measured faster than the TMA ring here (57 vs 75 us
-    // at it = 17, gpurun_out/r01n); k_correct_tma stays selectable for experiments
-    if (it <= kTmaCols && h->use_tma && h->tma_correct)
-        k_correct_tma<ST, CT><<<h->nsm, 256 * kCorrNG, kTmaSmem, h->stream>>>(a, it);
-    else if (it <= kCorrMaxNC && h->corrw)
+    // the register-pipelined correction measured faster than a TMA (cp.async.bulk +
+    // mbarrier) ring (57 vs 75 us at it = 17, gpurun_out/r01n; that variant was removed)
+    if (it <= kCorrMaxNC && h->corrw)
         correctw_dispatch<ST, CT, 1>(h, a, it, smem);  // exact-width: all it basis loads in flight
     else
         k_correct<ST, CT><<<h->grid_corr, kNT, smem, h->stream>>>(a, it);
@@ -537,6 +540,11 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // cycles: the paper's fixed m iterations (cycle 0 only), or thick-restart cycles
     // (reading Q26): restart after cycles 0 .. R-1, then steps keep+1 .. m again
     const int R = h->keep > 0 ? h->max_restarts : 0;
+    // reading Q25: the convergence check follows iteration it whatever kind of step it was
+    auto maybe_check = [&](int it) {
+        if (h->keep == 0 && h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0)
+            launch_jacobi(h, 1);  // may set done = 2 (later launches return at once)
+    };
     auto run_cycle = [&](int cyc) {
     const int it0 = (cyc == 0) ? 1 : h->keep + 1;
     for (int it = it0; it <= h->m; ++it) {
@@ -552,8 +560,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             exch_h(h);
             for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it, p.pro_gate);
             exch_vec_norm(h);
-            if (h->keep == 0 && h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0)
-                launch_jacobi(h, 1);
+            maybe_check(it);
             continue;
         }
         // reorth off (the paper's optional mode), or an iteration between two periodic
@@ -561,6 +568,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
         if (h->reorth < 0 || (h->period > 1 && it % h->period != 0 && (it == 1 || (it - 1) % h->period != 0))) {
             for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 1);
             exch_vec_norm(h);
+            maybe_check(it);
             continue;
         }
         for (Part &p : h->parts) launch_step<ST, CT>(h, p, it, 0, (cyc > 0 && it == it0) ? 1 : 0);
@@ -573,18 +581,15 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             for (Part &p : h->parts) launch_correct<ST, CT>(h, p, it, it);
         }
         exch_vec_norm(h);
-        if (h->keep == 0 && h->conv_tol > 0.0 && it >= h->K && it < h->m && it % h->conv_check == 0) {
-            launch_jacobi(h, 1);  // reading Q25: may set done = 2 (later launches return at once)
-        }
+        maybe_check(it);
     }
     };
     // thick restart inside a captured graph: cycle 0, then a WHILE node whose body is one
     // restart + cycle, looping on the device (no unrolled cycles, no host round trip).
     // Unrolled cycles (finished ones return at once) when not capturing, when profiling
     // (event nodes are not allowed in conditional bodies), with several processes, or
-    // with TOPK_NO_COND=1.
-    const char *nc = std::getenv("TOPK_NO_COND");
-    const bool use_while = R > 0 && h->capturing && !h->profile && h->world == 1 && !(nc && nc[0] == '1');
+    // with opts.restart_loop = 1.
+    const bool use_while = R > 0 && h->capturing && !h->profile && h->world == 1 && !h->restart_unrolled;
     if (!use_while) {
         for (int cyc = 0; cyc <= R; ++cyc) {
             run_cycle(cyc);
@@ -699,19 +704,9 @@ static void set_kernels(topk_eig_s *h) {
     h->grid_stream = h->nsm * 4;
     stepw_grids<ST, CT, 1>(h);
     correctw_grids<ST, CT, 1>(h);
-    CUDA_TRY(cudaFuncSetAttribute(k_step_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    CUDA_TRY(cudaFuncSetAttribute(k_correct_tma<ST, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    {
-        const char *e = std::getenv("TOPK_NO_TMA");
-        h->use_tma = !(e && e[0] == '1');
-        // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed
-        // restarts replace basis columns and periodic reorth skips the dots: explicit norm pass
-        h->use_gram = (h->reorth == 1 || h->reorth == 2) && h->keep == 0 && h->period == 1;
-        const char *e2 = std::getenv("TOPK_TMA_CORRECT");
-        h->tma_correct = e2 && e2[0] == '1';
-        const char *e3 = std::getenv("TOPK_TMA_STEP");
-        h->tma_step = e3 && e3[0] == '1';
-    }
+    // Ritz norms from the Gram matrix (k_correct recursion) whenever dots are computed;
+    // restarts replace basis columns and periodic reorth skips the dots: explicit norm pass
+    h->use_gram = (h->reorth == 1 || h->reorth == 2) && h->keep == 0 && h->period == 1;
     int occ3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_ritz<ST, CT, kRitzKB, 1>, kNT, (size_t)h->m * kRitzKB * 8);
     h->grid_ritz = h->nsm * std::max(1, std::min(occ3, 2));
@@ -959,6 +954,13 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (storage < TOPK_F64 || storage > TOPK_BF16 || compute < TOPK_F64 || compute > TOPK_F32 || ms < TOPK_F64 || ms > TOPK_BF16)
         return fail(TOPK_E_INVALID, "bad dtype");
 
+    {  // the (values, vectors, compute) combinations select_kernels instantiates
+        const bool ok = (ms == TOPK_F64 && storage == TOPK_F64 && compute == TOPK_F64) ||
+                        (ms == TOPK_F32 && storage == TOPK_F32) ||
+                        (ms == TOPK_BF16 && storage == TOPK_F32 && compute == TOPK_F64) ||
+                        (ms == TOPK_BF16 && storage == TOPK_BF16 && compute == TOPK_F64);
+        if (!ok) return fail(TOPK_E_INVALID, "unsupported (values, storage, compute) dtype combination");
+    }
     std::unique_ptr<topk_eig_s> h(new topk_eig_s());
     h->n = n; h->K = K; h->m = m; h->G = G; h->world = world; h->rank = world > 1 ? o.rank : 0;
     h->vs = storage; h->ms = ms; h->cs = compute;
@@ -982,11 +984,16 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         h->max_restarts = o.max_restarts;
     }
     h->conv_check = o.conv_check > 0 ? o.conv_check : K;
-    if (h->conv_tol > 0.0)
+    if (h->conv_tol > 0.0 && h->period > 1)
+        return fail(TOPK_E_INVALID, "conv_tol > 0 is not supported with reorth_period > 1");
+    if (h->conv_tol > 0.0 && h->keep == 0)  // the checks enqueued per solve (thick restart tests per cycle)
         for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
     if (o.exchange < 0 || o.exchange > 1) return fail(TOPK_E_INVALID, "exchange must be 0 (allgather) or 1 (halo)");
     h->halo = (G > 1 && o.exchange == 1);
-    if (const char *ec = std::getenv("TOPK_NO_CORRW")) h->corrw = !(ec[0] == '1');
+    if (o.jacobi_path < 0 || o.jacobi_path > 2) return fail(TOPK_E_INVALID, "jacobi_path must be 0, 1 or 2");
+    if (o.jacobi_cluster != 0 && o.jacobi_cluster != 8 && o.jacobi_cluster != 16)
+        return fail(TOPK_E_INVALID, "jacobi_cluster must be 0, 8 or 16");
+    h->restart_unrolled = o.restart_loop == 1;
     h->use_graph = o.use_graph >= 0;
     h->profile = o.profile > 0;
     h->device = o.device;
@@ -1091,14 +1098,16 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
             CUDA_TRY(cudaFuncGetAttributes(&fa, k_jacobi<true>));
             h->jac_threads = std::min(h->jac_threads, fa.maxThreadsPerBlock / 32 * 32);
-            if (const char *ej = std::getenv("TOPK_JAC_THREADS"))  // dev knob (A/B)
-                h->jac_threads = std::max(32, std::min(h->jac_threads, std::atoi(ej) / 32 * 32));
+#ifdef TOPK_JAC_THREADS  // dev build variant (A/B of the CTA size)
+            h->jac_threads = std::max(32, std::min(h->jac_threads, TOPK_JAC_THREADS / 32 * 32));
+#endif
         }
         // single CTA in shared memory for M <= 40; above that the cluster path is
         // faster (tools/jac_timing.py, profiles/r01_jacobi_timing.jsonl: m = 48 1.06 vs
         // 1.27 ms, m = 96 2.7 vs 8.4 ms, m = 192 10.9 vs 106 ms)
-        const char *jf = std::getenv("TOPK_JAC_CLUSTER");  // 1: cluster path at any m (experiments)
-        if (jbytes <= 200 * 1024 && M <= 40 && !(jf && jf[0] == '1')) {
+        // opts.jacobi_path: 0 auto (as above), 1 single CTA only (shared memory up to
+        // M = 40, global memory above), 2 cluster at any m
+        if (jbytes <= 200 * 1024 && M <= 40 && o.jacobi_path != 2) {
             h->jac_smem = jbytes;
             CUDA_TRY(cudaFuncSetAttribute(k_jacobi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jbytes));
         } else {
@@ -1106,11 +1115,9 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             h->jac_bytes = (jbytes + 255) / 256 * 256;
             h->jac_work = h->alloc<double>((size_t)nlocal * h->jac_bytes / 8);
             // T, S distributed over a thread-block cluster when they fit its shared memory
-            const char *ev = std::getenv("TOPK_NO_JAC_CLUSTER");
-            const char *ec = std::getenv("TOPK_JAC_CL");  // force a cluster size (experiments)
-            const int first = ec ? (std::atoi(ec) == 16 ? 16 : 8) : (M >= 96 ? 16 : 8);
+            const int first = o.jacobi_cluster ? o.jacobi_cluster : (M >= 96 ? 16 : 8);
             for (int CL : {first, 24 - first}) {
-                if (ev && ev[0] == '1') break;
+                if (o.jacobi_path == 1) break;
                 const size_t R = (size_t)(M + CL - 1) / CL;
                 const size_t cb = 3 * R * M * 8 + (size_t)M * 8 + (size_t)(2 * M + M) * 4 + 64;
                 if (cb > 200 * 1024) continue;
@@ -1234,27 +1241,26 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     return TOPK_OK;
 }
 
-static void free_handle(topk_eig_s *h) {
-    if (!h) return;
+topk_eig_s::~topk_eig_s() {
     StageClock clk;
-    cudaSetDevice(h->device);
-    if (h->stream) cudaStreamSynchronize(h->stream);
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
     clk.mark("destroy: stream sync");
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (gexec) cudaGraphExecDestroy(gexec);
     clk.mark("destroy: graph");
-    if (h->comm) ncclCommDestroy(h->comm);
-    for (void *p : h->allocs) pool_dev_free(p);  // back to the cache (the stream is idle)
+    if (comm) ncclCommDestroy(comm);
+    for (void *p : allocs) pool_dev_free(p);  // back to the cache (the stream is idle)
     clk.mark("destroy: pool");
-    if (h->ev0) cudaEventDestroy(h->ev0);
-    if (h->ev1) cudaEventDestroy(h->ev1);
-    for (auto &q : h->prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (auto &q : prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
     clk.mark("destroy: events");
-    if (h->stream) cudaStreamDestroy(h->stream);
-    if (h->body_stream) cudaStreamDestroy(h->body_stream);
+    if (stream) cudaStreamDestroy(stream);
+    if (body_stream) cudaStreamDestroy(body_stream);
     clk.mark("destroy: stream");
-    delete h;
-    clk.mark("destroy: host state");
 }
+
+static void free_handle(topk_eig_s *h) { delete h; }
 
 // Enqueue one full solve on h->stream (graph replay or eager launches).
 static void enqueue(topk_eig_s *h, uint64_t seed, const double *v1_host, void *const *out_ptrs, int out_dtype) {
@@ -1304,7 +1310,9 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     if (!info) return;
     const Part &p = h->parts[0];
     std::memset(info, 0, sizeof(*info));
-    info->iterations = hget<int>(p, p.st.m_found);
+    const int m_cycle = hget<int>(p, p.st.m_found);  // steps of the last cycle (basis columns used)
+    info->iterations = m_cycle;
+    info->beta_next = hptr(p, p.st.beta)[m_cycle];   // beta has m + 2 entries; m_cycle <= m
     info->k_found = hget<int>(p, p.st.k_found);
     const int done = hget<int>(p, p.st.done);
     const int nrst = hget<int>(p, p.st.restarts);
@@ -1318,7 +1326,6 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     info->jacobi_sweeps = hget<int>(p, p.st.jac_sweeps);
     info->jacobi_converged = hget<int>(p, p.st.jac_conv);
     info->num_parts = h->G;
-    info->beta_next = hptr(p, p.st.beta)[info->iterations];
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev0, h->ev1);
     info->ms_solve = ms;
@@ -1635,7 +1642,7 @@ static double to_double_elem(const char *base, size_t idx, topk_dtype_t t) {
     return bf16_bits_to_double(reinterpret_cast<const uint16_t *>(base)[idx]);
 }
 
-topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32_t *ncols) {
+static topk_status_t export_basis_impl(topk_eig_t h, int32_t part, double *V, int32_t *ncols, bool scaled) {
     GUARD(h);
     if (part < 0 || part >= (int)h->parts.size()) return fail(TOPK_E_INVALID, "bad part");
     Part &p = h->parts[(size_t)part];
@@ -1651,13 +1658,21 @@ topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32
         const double *sc = hptr(p, p.st.scale);
         const double *bt = hptr(p, p.st.beta);
         for (int j = 0; j < nc; ++j) {
-            const double s = (j < mm) ? sc[j] : 1.0 / bt[mm];
+            const double s = !scaled ? 1.0 : (j < mm) ? sc[j] : 1.0 / bt[mm];
             for (int64_t r = 0; r < p.nrows; ++r)
                 V[(size_t)j * p.nrows + p.h_perm[(size_t)r]] = s * to_double_elem(t.data(), (size_t)j * p.npad + r, h->vs);
         }
     }
     CATCH(h)
     return TOPK_OK;
+}
+
+topk_status_t topk_eig_export_basis(topk_eig_t h, int32_t part, double *V, int32_t *ncols) {
+    return export_basis_impl(h, part, V, ncols, true);
+}
+
+topk_status_t topk_eig_export_basis_raw(topk_eig_t h, int32_t part, double *U, int32_t *ncols) {
+    return export_basis_impl(h, part, U, ncols, false);
 }
 
 topk_status_t topk_eig_debug_spmv(topk_eig_t h, const double *x, double *y) {

@@ -310,27 +310,27 @@ def test_c3_full_size_parity(T):
     check_solve(r, ref, 1e-4)
 
 
-# ------------------------------------------------------------------ kernel-path equivalence
-@pytest.mark.parametrize("storage", ["f64", "f32"])
-def test_tma_path_matches_register_path(T, c3s, storage, monkeypatch):
-    """The TMA multi-dot (k_step_tma, Gram-based Ritz norms) and the register
-    multi-dot + Ritz norm pass compute the same iteration: Ritz values agree to
-    rounding, eigenvectors to the vector tolerance."""
-    K, m = 16, 24
-    monkeypatch.setenv("TOPK_NO_TMA", "0")
-    with T.TopkEig(c3s, K, storage, "f64", m=m) as h:
-        r1 = h.solve(seed=9)
-        _, _, t1 = h.tridiag()
-    monkeypatch.setenv("TOPK_NO_TMA", "1")
-    with T.TopkEig(c3s, K, storage, "f64", m=m) as h:
-        r2 = h.solve(seed=9)
-        _, _, t2 = h.tridiag()
-    tol = 1e-12 if storage == "f64" else 1e-6
-    assert normwise(t1, t2) <= tol
-    for k in range(K):
-        y1, y2 = r1.eigenvectors[k], r2.eigenvectors[k]
-        assert abs(np.linalg.norm(y1) - 1) < 1e-6 and abs(np.linalg.norm(y2) - 1) < 1e-6
-        assert min(np.linalg.norm(y1 - y2), np.linalg.norm(y1 + y2)) <= (1e-10 if storage == "f64" else 1e-4)
+# ------------------------------------------------------------------ v1 bit-exact (SURVEY 8(c) parity contract)
+@pytest.mark.parametrize("storage,G", [("f64", 1), ("f32", 1), ("f64", 3), ("bf16", 1)])
+def test_v1_unnormalised_bit_exact(T, c3s, storage, G):
+    """The unnormalised start vector u_r = 2 U(h3(seed, 0x7631, r)) - 1 (reading Q8,
+    PAPER.md:75,205) stored as basis column 0 equals the oracle's orc_v1 bit for bit
+    after the one storage rounding (f64: identical; f32 / bf16: RNE straight from f64,
+    reading Q22), over every global row, for every part."""
+    seed = 12345
+    n = c3s.n
+    u = O.v1(seed, n)
+    # the oracle's storage rounding (O2 layout rule) of a diagonal matrix holding u:
+    # every row has degree 1, so the degree order is the original order
+    rp = np.arange(n + 1, dtype=np.int64)
+    _, _, want, _ = O.layout(rp, np.arange(n, dtype=np.int32), u, 1, np.array([0, n]), 0, storage)
+    with T.TopkEig(c3s, 8, storage, "f64", m=8, parts=G) as h:
+        h.solve(seed=seed, vectors=False)
+        b = h.partition()
+        got = np.empty(n)
+        for g in range(G):
+            got[b[g]:b[g + 1]] = h.basis(g, raw=True)[0]
+    assert np.array_equal(np.asarray(want, np.float64).view(np.uint64), got.view(np.uint64))
 
 
 # ------------------------------------------------------------------ closed form, random start (P5 via the ABI)
@@ -363,14 +363,12 @@ def test_c3_full_size_parity_ddd(T):
 
 @pytest.mark.parametrize("m", [64, 130, 192, 300])
 @pytest.mark.parametrize("cluster", [True, False])
-def test_large_m_jacobi_paths(T, c3s, m, cluster, monkeypatch):
+def test_large_m_jacobi_paths(T, c3s, m, cluster):
     """Krylov dimensions whose T, S do not fit one SM's shared memory: the
     cluster-distributed Jacobi (8 CTAs at m = 64; 16 at m = 130, 192, 300) and the
     single-CTA global-memory fallback both match the oracle (reading Q10)."""
-    if not cluster:
-        monkeypatch.setenv("TOPK_NO_JAC_CLUSTER", "1")
     ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=24, m=m, seed=8)
-    with T.TopkEig(c3s, 24, "f64", "f64", m=m) as h:
+    with T.TopkEig(c3s, 24, "f64", "f64", m=m, jacobi_path="auto" if cluster else "single") as h:
         r = h.solve(seed=8)
         _, _, th = h.tridiag()
     assert r.info["jacobi_converged"] == 1

@@ -55,6 +55,9 @@ def test_thick_restart_matches_oracle(T, c3s, storage, tol):
     err = np.abs(res.eigenvalues - ref.eigenvalues).max() / abs(ref.eigenvalues[0])
     assert err <= tol
     _vectors_close(res, ref, 1e-5 if storage == "f64" else 1e-3)
+    # beta_{m+1} of the last cycle (reading Q6), read at the cycle's own step count
+    bref = ref.lanczos.beta[ref.lanczos.m_found]
+    assert abs(res.info["beta_next"] - bref) <= tol * abs(ref.eigenvalues[0]), (res.info["beta_next"], bref)
 
 
 def test_thick_restart_converged_stop(T, c3s):

@@ -397,6 +397,47 @@ def test_p7_lanczos_invariants(m):
     assert np.all(np.abs(r.theta_all) <= nrmA * (1 + 1e-12))
 
 
+# ---------------------------------------------------------------- P15 (O8-O9 sign, reading Q12)
+
+
+@pytest.mark.parametrize("case", ["rmat_m24", "er_m64", "two_by_two"])
+def test_p15_ritz_sign_rule(case):
+    """Reading Q12: each returned eigenvector y_k is unit-norm with <y_k, v1/||v1||> > 0.
+    With an orthonormal basis, <y_k, v1> = |s_1k| where s_k is the unit eigenvector of T
+    for theta_k; |s_1k| is sign-invariant, so it is taken from numpy.linalg.eigh(T)
+    (LAPACK), not from the oracle's Jacobi. The inner products are formed here with
+    numpy from the returned vectors and the start vector, not by the oracle. Each case
+    also checks that the oracle's Jacobi hands back S[0,k] < 0 for at least one selected
+    k, so the flip branch is exercised (a sign rule that never flips, or flips the wrong
+    way, fails)."""
+    if case == "rmat_m24":
+        A = S.rmat(12, 40_000, 5)
+        rp, c, v, K, m, seed = A.rowptr, A.col, A.val, 8, 24, 3
+    elif case == "er_m64":
+        rp, c, v = er_csr(2000, 12_000, 4)
+        K, m, seed = 12, 64, 7
+    else:
+        rp, c, v = csr_of(np.array([[2.0, 1.0], [1.0, 2.0]]))
+        K, m, seed = 2, 2, 1
+    n = len(rp) - 1
+    u = O.v1(seed, n)
+    v1n = u / np.linalg.norm(u)
+    r = O.solve(rp, c, v, K=K, m=m, seed=seed)
+    T = O.tridiag_dense(r.lanczos.alpha, r.lanczos.beta)
+    w, Q = np.linalg.eigh(T)
+    flipped = 0
+    for k in range(len(r.eigenvalues)):
+        y = r.eigenvectors[k]
+        assert abs(np.linalg.norm(y) - 1.0) <= 1e-12
+        ip = float(np.dot(y, v1n))
+        assert ip > 0.0, (case, k, ip)
+        j = int(np.argmin(np.abs(w - r.eigenvalues[k])))
+        assert abs(ip - abs(Q[0, j])) <= 1e-9, (case, k, ip, Q[0, j])
+        flipped += r.S[0, r.idx[k]] < 0.0
+    if case != "two_by_two":
+        assert flipped >= 1, "no selected Jacobi column had S[0,k] < 0: the flip is untested"
+
+
 # ---------------------------------------------------------------- P8 (O4-O9)
 @pytest.mark.slow
 def test_p8_converged_pairs_match_arpack():

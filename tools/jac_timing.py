@@ -12,18 +12,15 @@ import synthgen as S  # noqa: E402
 
 def main():
     A = S.config_matrix("C3S")
-    paths = {"single": {"TOPK_NO_JAC_CLUSTER": "1"},
-             "cl8": {"TOPK_JAC_CLUSTER": "1", "TOPK_JAC_CL": "8"},
-             "cl16": {"TOPK_JAC_CLUSTER": "1", "TOPK_JAC_CL": "16"},
+    paths = {"single": dict(jacobi_path="single"),
+             "cl8": dict(jacobi_path="cluster", jacobi_cluster=8),
+             "cl16": dict(jacobi_path="cluster", jacobi_cluster=16),
              "default": {}}
     ms = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [24, 48, 64, 96, 130, 192, 256, 300]
     import paper_2201_07498_b200 as T
     for m in ms:
-        for path, env in paths.items():
-            for k in ("TOPK_NO_JAC_CLUSTER", "TOPK_JAC_CLUSTER", "TOPK_JAC_CL"):
-                os.environ.pop(k, None)
-            os.environ.update(env)
-            with T.TopkEig(A, 24, "f32", "f64", m=m, profile=True) as h:
+        for path, kw in paths.items():
+            with T.TopkEig(A, 24, "f32", "f64", m=m, profile=True, **kw) as h:
                 h.solve(seed=1, vectors=False)
                 r = h.solve(seed=1, vectors=False)
                 kt = h.kernel_times()

@@ -1,15 +1,14 @@
 """Thick restart on C3 (K = 24, m = 72, keep 36, tol 1e-5): device time per solve with
-the WHILE-node graph vs unrolled cycles (TOPK_NO_COND=1), for restart caps 10 and 40."""
+the WHILE-node graph vs unrolled cycles (restart_loop="unrolled"), for restart caps 10 and 40."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import synthgen as S, paper_2201_07498_b200 as T
 A = S.config_matrix("C3")
 for cond in (1, 0):
-    os.environ["TOPK_NO_COND"] = "0" if cond else "1"
     for cap in (10, 40):
         with T.TopkEig(A, 24, "f32", "f64", m=72, restart_keep=36, max_restarts=cap, conv_tol=1e-5,
-                       check_symmetry=False) as h:
+                       check_symmetry=False, restart_loop="auto" if cond else "unrolled") as h:
             ev = torch.zeros(24, dtype=torch.float64, device="cuda")
             h.solve_async(1, ev.data_ptr(), None); h.sync()
             st = torch.cuda.ExternalStream(h.stream)
