@@ -16,6 +16,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef struct {
     int64_t n;
@@ -48,45 +51,23 @@ void sg_free(sg_csr_t *m) {
     free(m);
 }
 
-/* ------------------------------------------------------------------ */
-/* LSD radix sort of 64-bit keys (16-bit digits), used to build CSR.   */
-static int radix_sort_u64(uint64_t *keys, int64_t n, int key_bits) {
-    uint64_t *tmp = (uint64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(uint64_t));
-    int64_t *cnt = (int64_t *)malloc(65536 * sizeof(int64_t));
-    if (!tmp || !cnt) { free(tmp); free(cnt); return -1; }
+/* LSD radix sort of n 64-bit keys on their low key_bits bits (11-bit digits), with a
+ * caller-provided scratch of n keys; the result is in keys. Used to build CSR. */
+static int radix_sort_u64_buf(uint64_t *keys, uint64_t *tmp, int64_t n, int key_bits) {
+    int64_t *cnt = (int64_t *)malloc(2048 * sizeof(int64_t));
+    if (!cnt) return -1;
     uint64_t *src = keys, *dst = tmp;
-    for (int shift = 0; shift < key_bits; shift += 16) {
-        memset(cnt, 0, 65536 * sizeof(int64_t));
-        for (int64_t i = 0; i < n; ++i) cnt[(src[i] >> shift) & 0xFFFF]++;
+    for (int shift = 0; shift < key_bits; shift += 11) {
+        memset(cnt, 0, 2048 * sizeof(int64_t));
+        for (int64_t i = 0; i < n; ++i) cnt[(src[i] >> shift) & 0x7FF]++;
         int64_t s = 0;
-        for (int d = 0; d < 65536; ++d) { int64_t c = cnt[d]; cnt[d] = s; s += c; }
-        for (int64_t i = 0; i < n; ++i) dst[cnt[(src[i] >> shift) & 0xFFFF]++] = src[i];
+        for (int d = 0; d < 2048; ++d) { int64_t c = cnt[d]; cnt[d] = s; s += c; }
+        for (int64_t i = 0; i < n; ++i) dst[cnt[(src[i] >> shift) & 0x7FF]++] = src[i];
         uint64_t *t = src; src = dst; dst = t;
     }
     if (src != keys) memcpy(keys, src, (size_t)n * sizeof(uint64_t));
-    free(tmp);
     free(cnt);
     return 0;
-}
-
-/* keys (row << sh) | col, sorted ascending and unique -> CSR skeleton. */
-static sg_csr_t *csr_from_sorted_keys(const uint64_t *keys, int64_t nk, int64_t n, int sh) {
-    sg_csr_t *m = (sg_csr_t *)calloc(1, sizeof(sg_csr_t));
-    if (!m) return NULL;
-    m->n = n;
-    m->nnz = nk;
-    m->rowptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
-    m->col = (int32_t *)malloc((size_t)(nk > 0 ? nk : 1) * sizeof(int32_t));
-    m->val = (double *)malloc((size_t)(nk > 0 ? nk : 1) * sizeof(double));
-    if (!m->rowptr || !m->col || !m->val) { sg_free(m); return NULL; }
-    uint64_t cmask = (sh >= 64) ? ~0ull : ((1ull << sh) - 1);
-    for (int64_t k = 0; k < nk; ++k) {
-        int64_t r = (int64_t)(keys[k] >> sh);
-        m->rowptr[r + 1]++;
-        m->col[k] = (int32_t)(keys[k] & cmask);
-    }
-    for (int64_t r = 0; r < n; ++r) m->rowptr[r + 1] += m->rowptr[r];
-    return m;
 }
 
 /* ------------------------------------------------------------------ */
@@ -146,16 +127,89 @@ sg_csr_t *sg_rmat(int scale, int64_t n, int64_t samples, double a, double b, dou
             keys[2 * e + 1] = (v << scale) | u;
         }
     }
-    int64_t nk = 0;
-    for (int64_t k = 0; k < 2 * samples; ++k)
-        if (keys[k] != SENT) keys[nk++] = keys[k];
-    if (radix_sort_u64(keys, nk, 2 * scale) != 0) { free(keys); return NULL; }
+    /* sort + dedupe in parallel (identical output to a serial sort of all keys):
+       scatter the non-sentinel keys into 2^B buckets by their top B bits (each bucket
+       = a disjoint row range), LSD-radix-sort every bucket, drop duplicates, build
+       the CSR rows of each bucket independently */
+    const int kb = 2 * scale;
+    const int B = scale < 12 ? scale : 12;
+    const int64_t NB = (int64_t)1 << B;
+    const int low = kb - B;  /* bits below the bucket id */
+    const int64_t ntot = 2 * samples;
+    uint64_t *tmp = (uint64_t *)malloc((size_t)(ntot + 1) * sizeof(uint64_t));
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    int64_t *hist = (int64_t *)calloc((size_t)nth * NB, sizeof(int64_t));
+    int64_t *boff = (int64_t *)calloc((size_t)NB + 1, sizeof(int64_t));
+    int64_t *ucnt = (int64_t *)calloc((size_t)NB + 1, sizeof(int64_t));
+    if (!tmp || !hist || !boff || !ucnt) { free(keys); free(tmp); free(hist); free(boff); free(ucnt); return NULL; }
+#pragma omp parallel num_threads(nth)
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        const int64_t k0 = ntot * t / nth, k1 = ntot * (t + 1) / nth;
+        int64_t *h = hist + (size_t)t * NB;
+        for (int64_t k = k0; k < k1; ++k)
+            if (keys[k] != SENT) h[keys[k] >> low]++;
+#pragma omp barrier
+#pragma omp single
+        {
+            int64_t acc = 0;
+            for (int64_t b = 0; b < NB; ++b) {
+                boff[b] = acc;
+                for (int tt = 0; tt < nth; ++tt) {
+                    int64_t c = hist[(size_t)tt * NB + b];
+                    hist[(size_t)tt * NB + b] = acc;
+                    acc += c;
+                }
+            }
+            boff[NB] = acc;
+        }
+        for (int64_t k = k0; k < k1; ++k)
+            if (keys[k] != SENT) tmp[h[keys[k] >> low]++] = keys[k];
+    }
+    int fail = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : fail)
+    for (int64_t b = 0; b < NB; ++b) {
+        const int64_t o = boff[b], c = boff[b + 1] - o;
+        if (c > 1 && low > 0 && radix_sort_u64_buf(tmp + o, keys + o, c, low) != 0) fail = 1;
+        int64_t nu = 0;
+        for (int64_t k = 0; k < c; ++k)
+            if (nu == 0 || tmp[o + k] != tmp[o + nu - 1]) tmp[o + nu++] = tmp[o + k];
+        ucnt[b] = nu;
+    }
+    if (fail) { free(keys); free(tmp); free(hist); free(boff); free(ucnt); return NULL; }
     int64_t nu = 0;
-    for (int64_t k = 0; k < nk; ++k)
-        if (nu == 0 || keys[k] != keys[nu - 1]) keys[nu++] = keys[k];
-    sg_csr_t *m = csr_from_sorted_keys(keys, nu, n, scale);
+    for (int64_t b = 0; b < NB; ++b) { int64_t c = ucnt[b]; ucnt[b] = nu; nu += c; }
+    ucnt[NB] = nu;
     free(keys);
-    if (!m) return NULL;
+    sg_csr_t *m = (sg_csr_t *)calloc(1, sizeof(sg_csr_t));
+    if (m) {
+        m->n = n;
+        m->nnz = nu;
+        m->rowptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+        m->col = (int32_t *)malloc((size_t)(nu > 0 ? nu : 1) * sizeof(int32_t));
+        m->val = (double *)malloc((size_t)(nu > 0 ? nu : 1) * sizeof(double));
+        if (!m->rowptr || !m->col || !m->val) { sg_free(m); m = NULL; }
+    }
+    if (!m) { free(tmp); free(hist); free(boff); free(ucnt); return NULL; }
+    const uint64_t cmask = ((uint64_t)1 << scale) - 1;
+    /* per-row counts (rows of different buckets are disjoint), then the prefix sum */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < NB; ++b) {
+        const int64_t o = boff[b], c = ucnt[b + 1] - ucnt[b], d = ucnt[b];
+        for (int64_t k = 0; k < c; ++k) {
+            const uint64_t key = tmp[o + k];
+            m->rowptr[(int64_t)(key >> scale) + 1]++;
+            m->col[d + k] = (int32_t)(key & cmask);
+        }
+    }
+    for (int64_t r = 0; r < n; ++r) m->rowptr[r + 1] += m->rowptr[r];
+    free(tmp); free(hist); free(boff); free(ucnt);
     const uint64_t W = 0x57454947ull; /* "WEIG" */
 #pragma omp parallel for schedule(dynamic, 4096)
     for (int64_t r = 0; r < n; ++r) {
