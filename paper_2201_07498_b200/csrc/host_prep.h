@@ -112,9 +112,18 @@ void build_halo(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t np
 //    value 0). One lane per row, coalesced 128-byte loads, no reductions.
 //  * work items: one per chunk, then groups of consecutive slices with
 //    sum(w_s) <= kSellItemWidth (about <= 2048 padded nonzeros per item).
-constexpr int kSellMaxLen = 128;
-constexpr int kChunkNnz = 2048;
-constexpr int kSellItemWidth = 64;
+#ifndef TOPK_SELL_MAXLEN
+#define TOPK_SELL_MAXLEN 128
+#endif
+#ifndef TOPK_CHUNK_NNZ
+#define TOPK_CHUNK_NNZ 8192
+#endif
+#ifndef TOPK_SELL_ITEM_WIDTH
+#define TOPK_SELL_ITEM_WIDTH 64
+#endif
+constexpr int kSellMaxLen = TOPK_SELL_MAXLEN;     // dev build variants (tools/lab/spmv_ab.py)
+constexpr int kChunkNnz = TOPK_CHUNK_NNZ;
+constexpr int kSellItemWidth = TOPK_SELL_ITEM_WIDTH;
 
 struct Chunk {       // big-row chunk (24 bytes; z0 is 64-bit: parts may hold >= 2^31 nonzeros)
     int64_t z0;      // first physical nonzero

@@ -146,6 +146,40 @@ def from_dense(a: np.ndarray) -> CSR:
     return CSR(n, rowptr, cols.astype(np.int32), a[rows, cols].copy())
 
 
+def stars(degrees, dense=(), gap: int = 7, seed: int = 3) -> CSR:
+    """Symmetric test matrix with rows of exactly the given degrees (SpMV layout
+    boundaries): for each d in `degrees` a star (a centre row joined to d leaf rows of
+    degree 1), for each s in `dense` a dense s x s block (rows of degree s); `gap`
+    empty rows before every component and a ragged empty tail. Values k/128,
+    k in [64, 191] (exact in bf16/f32/f64), drawn from a seeded numpy generator."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    r0 = 0
+    for d in degrees:
+        r0 += gap
+        c = r0
+        leaves = np.arange(c + 1, c + 1 + d)
+        w = rng.integers(64, 192, size=d).astype(np.float64) / 128.0
+        rows += [np.full(d, c), leaves]
+        cols += [leaves, np.full(d, c)]
+        vals += [w, w]
+        r0 = c + 1 + d
+    for sz in dense:
+        r0 += gap
+        w = rng.integers(64, 192, size=(sz, sz)).astype(np.float64) / 128.0
+        w = np.triu(w) + np.triu(w, 1).T
+        ii, jj = np.meshgrid(np.arange(sz), np.arange(sz), indexing="ij")
+        rows.append((r0 + ii).ravel()); cols.append((r0 + jj).ravel()); vals.append(w.ravel())
+        r0 += sz
+    n = r0 + gap + 5
+    row = np.concatenate(rows); col = np.concatenate(cols); val = np.concatenate(vals)
+    key = row.astype(np.int64) * n + col
+    o = np.argsort(key, kind="stable")
+    rowptr = np.zeros(n + 1, np.int64)
+    np.add.at(rowptr, row + 1, 1)
+    return CSR(n, np.cumsum(rowptr), col[o].astype(np.int32), val[o])
+
+
 def hash3(s: int, a: int, b: int) -> int:
     return int(_load().sg_hash3(s, a, b))
 

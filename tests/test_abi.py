@@ -140,19 +140,20 @@ def test_physical_format_unpacks_to_logical(G):
     holds exactly the logical CSR: every logical entry at its physical slot,
     padding = (column 0, 0.0), slices degree-sorted, items cover all slices."""
     A = S.rmat(13, 120_000, 5)
-    for g in range(G):
-        L = T.plan_layout(A, G, g, "f32")
+    st = S.stars([8191, 8192, 8193, 16385, 300], dense=[127, 128, 129, 3])
+    for M, g, G_ in [(A, g, G) for g in range(G)] + [(st, 0, 1)]:
+        L = T.plan_layout(M, G_, g, "f32")
         rp, col, val, nbig, nne = L["rowptr"], L["col"], L["val"], L["nbig"], L["nnonempty"]
         deg = np.diff(rp)
         assert np.all(deg[:-1] >= deg[1:]), "rows must be in degree order"
         assert nne == int((deg > 0).sum()) and np.all(deg[:nbig] > 128) and np.all(deg[nbig:] <= 128)
         pcol, pval, ch, sl, it = L["pcol"], L["pval"], L["chunks"], L["sell"], L["items"]
-        # big rows: CSR prefix, cut into <= 2048-nnz chunks in order
+        # big rows: CSR prefix, cut into <= 8192-nnz chunks (kChunkNnz) in order
         assert np.array_equal(pcol[:rp[nbig]], col[:rp[nbig]]) and np.array_equal(pval[:rp[nbig]], val[:rp[nbig]])
         cover = np.zeros(rp[nbig], np.int32)
         for row, z0, cnt, lid in ch:
-            assert rp[row] <= z0 and z0 + cnt <= rp[row + 1] and 1 <= cnt <= 2048
-            assert (lid >= 0) == (deg[row] > 2048)
+            assert rp[row] <= z0 and z0 + cnt <= rp[row + 1] and 1 <= cnt <= 8192
+            assert (lid >= 0) == (deg[row] > 8192)
             cover[z0:z0 + cnt] += 1
         assert np.all(cover == 1)
         # SELL-32: slice s rows nbig + 32 s + i, width = degree of its first row, column-major

@@ -414,32 +414,13 @@ def test_bf16_vectors_report_only(T, c3s):
     assert np.allclose(np.linalg.norm(r.eigenvectors.astype(np.float64), axis=1), 1.0, atol=1e-3)
 
 
-def _block_matrix(sizes, empty_every=7, seed=3):
-    """Block-diagonal symmetric matrix: dense blocks of the given sizes (rows of exactly
-    that degree), separated by empty rows; values k/128 (exact in every storage dtype)."""
-    rng = np.random.default_rng(seed)
-    rows, cols, vals = [], [], []
-    r0 = 0
-    for s in sizes:
-        r0 += empty_every  # empty rows between the blocks
-        w = rng.integers(64, 192, size=(s, s)).astype(np.float64) / 128.0
-        w = np.triu(w) + np.triu(w, 1).T
-        ii, jj = np.meshgrid(np.arange(s), np.arange(s), indexing="ij")
-        rows.append((r0 + ii).ravel()); cols.append((r0 + jj).ravel()); vals.append(w.ravel())
-        r0 += s
-    n = r0 + empty_every + 5  # ragged empty tail
-    row = np.concatenate(rows); col = np.concatenate(cols).astype(np.int32); val = np.concatenate(vals)
-    rp, c, v = O.coo_to_csr(n, row, col, val)
-    return S.CSR(n, rp, c, v)
-
-
 @pytest.mark.parametrize("G", [1, 3])
 def test_row_length_boundaries(T, G):
     """Rows of degree exactly at the layout boundaries -- 127/128 (SELL) vs 129 (big
-    row), 2047/2048 (one chunk) vs 2049 and 4097 (several chunks, finished by the last
+    row), 8191/8192 (one chunk) vs 8193 and 16385 (several chunks, finished by the last
     arriving one) -- plus empty rows and a ragged tail: every SpMV row within the
     rigorous fp64 bound of the oracle, and the solve at the DDD tolerance."""
-    A = _block_matrix([127, 128, 129, 2047, 2048, 2049, 4097, 3])
+    A = S.stars([8191, 8192, 8193, 16385], dense=[127, 128, 129, 3])
     x = np.random.default_rng(1).standard_normal(A.n)
     with T.TopkEig(A, 8, "f64", "f64", m=24, parts=G) as h:
         y = h.debug_spmv(x)
