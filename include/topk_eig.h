@@ -150,6 +150,12 @@ typedef struct {
     int32_t conv_checks;      /* convergence checks enqueued per solve                             */
     int32_t restarts;         /* thick restarts done (iterations then counts every Lanczos step)   */
     int32_t reorth_passes;    /* reorth = 3: iterations that took the reorthogonalisation pass    */
+    double ms_lanczos;        /* device time of v1 + the Lanczos iterations (phase 1)  */
+    double ms_jacobi;         /* device time of the final Jacobi solve + top-K selection (a12-a13)  */
+    double ms_ritz;           /* device time of the Ritz projection + output reordering (a14)      */
+    int64_t bytes_nvlink;     /* one process per GPU: modelled bytes this rank receives over the
+                                 interconnect per solve at the fixed m (the vector exchange, v1 +
+                                 one per step, and the scalar allgathers); 0 in one process      */
 } topk_eig_info_t;
 
 /* Create a solver for M, K eigenpairs, storage/compute precision pair.

@@ -62,7 +62,9 @@ class Info(ctypes.Structure):
                 ("beta_next", ctypes.c_double), ("ms_solve", ctypes.c_double),
                 ("bytes_model", ctypes.c_int64), ("gpu_launches", ctypes.c_int64),
                 ("converged_stop", ctypes.c_int32), ("conv_checks", ctypes.c_int32),
-                ("restarts", ctypes.c_int32), ("reorth_passes", ctypes.c_int32)]
+                ("restarts", ctypes.c_int32), ("reorth_passes", ctypes.c_int32),
+                ("ms_lanczos", ctypes.c_double), ("ms_jacobi", ctypes.c_double),
+                ("ms_ritz", ctypes.c_double), ("bytes_nvlink", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -168,15 +168,24 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
 // a2 (reading Q17): M = M^T structurally and bitwise in values. The canonical CSR has
 // no duplicates, so this holds iff the multiset of off-diagonal entries (r, c, bits)
 // with c > r equals the multiset of (c, r, bits) with c < r. Both multisets are
-// compared through two independent 64-bit hash sums (splitmix64 finaliser, wrapping
-// addition): a symmetric matrix always passes; an asymmetric one passes only on a
-// simultaneous collision of both sums (probability ~2^-128). One parallel pass over
-// the nonzeros instead of a binary search per nonzero (1.8 s -> tens of ms at C3).
+// compared through two independent 64-bit hash sums (wrapping addition) of the entry
+// key (min(r,c) << 32 | max(r,c), unique because n < 2^31) and the value bits: a
+// symmetric matrix always passes; an asymmetric one passes only on a simultaneous
+// collision of both sums (probability ~2^-128 for random-function hashes). One
+// parallel pass over the nonzeros (a binary search per nonzero took 1.8 s at C3).
+// Two finalisers per entry: splitmix64's and murmur3's fmix64 (different constants).
 static inline uint64_t sym_mix(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
     x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
     return x ^ (x >> 31);
+}
+static inline uint64_t sym_fmix(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    return x ^ (x >> 33);
 }
 bool is_symmetric(const Csr &m) {
     uint64_t u1 = 0, u2 = 0, l1 = 0, l2 = 0;
@@ -188,9 +197,9 @@ bool is_symmetric(const Csr &m) {
             uint64_t vb;
             const double v = m.val[(size_t)k];
             std::memcpy(&vb, &v, 8);
-            const uint64_t a = (uint64_t)std::min(r, c), b = (uint64_t)std::max(r, c);
-            const uint64_t h1 = sym_mix(sym_mix(sym_mix(a ^ 0x5f3759dfull) ^ b) ^ vb);
-            const uint64_t h2 = sym_mix(sym_mix(sym_mix(b ^ 0x2545f4914f6cdd1dull) ^ vb) ^ a);
+            const uint64_t key = ((uint64_t)std::min(r, c) << 32) | (uint64_t)std::max(r, c);
+            const uint64_t h1 = sym_mix(key ^ (vb * 0x9E3779B97F4A7C15ull));
+            const uint64_t h2 = sym_fmix((key * 0xD6E8FEB86659FD93ull) ^ (vb + 0x2545F4914F6CDD1Dull));
             if (c > r) { u1 += h1; u2 += h2; } else { l1 += h1; l2 += h2; }
         }
     }

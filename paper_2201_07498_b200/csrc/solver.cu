@@ -178,6 +178,8 @@ struct topk_eig_s {
     size_t jac_cl_smem = 0;
     cudaGraphExec_t gexec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t evL = nullptr, evJ = nullptr;  // end of the Lanczos phase / of the final Jacobi (info ms_*)
+    int64_t bytes_nvlink = 0;                  // modelled bytes received over the interconnect per solve
     ncclComm_t comm = nullptr;
     bool sticky = false;
     int64_t bytes_model = 0;
@@ -520,6 +522,13 @@ static void launch_pro(topk_eig_s *h, Part &p, int it) {
     h->launches++;
 }
 
+// phase boundary events (topk_eig_info_t ms_lanczos / ms_jacobi / ms_ritz): event-record
+// nodes when the solve is being captured
+static void record_event(topk_eig_s *h, cudaEvent_t e) {
+    if (h->capturing) CUDA_TRY(cudaEventRecordWithFlags(e, h->stream, cudaEventRecordExternal));
+    else CUDA_TRY(cudaEventRecord(e, h->stream));
+}
+
 template <typename VT, typename ST, typename CT>
 static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // a5: v1
@@ -641,7 +650,9 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
         CUDA_TRY(cudaStreamEndCapture(h->body_stream, &body_out));
     }
     // a12-a13: Jacobi (redundant on every part, identical inputs)
+    record_event(h, h->evL);
     launch_jacobi(h, 0);
+    record_event(h, h->evJ);
     if (!want_vectors) return;
     // a14: Ritz projection + normalisation, two streaming passes (norms, output)
     for (int pass = h->use_gram ? 1 : 0; pass < 2; ++pass) {
@@ -1029,6 +1040,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreate(&h->ev0));
         CUDA_TRY(cudaEventCreate(&h->ev1));
+        CUDA_TRY(cudaEventCreate(&h->evL));
+        CUDA_TRY(cudaEventCreate(&h->evJ));
         clk.mark("device init");
         // a4, first half, in the background: the local parts' CSR slices go up on a
         // helper thread (own stream) while this thread builds the degree order and tables
@@ -1223,6 +1236,12 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             h->bytes_model += model_bytes(h.get(), p);
             clk.mark("allocations");
         }
+        if (h->comm) {  // interconnect bytes received per solve (model, fixed m: v1 + one exchange per step)
+            const int64_t es = (int64_t)dsize(storage);
+            const int64_t vec = h->halo ? h->parts[0].nhalo * es : (int64_t)(G - 1) * npad * es;
+            const int64_t scal = (int64_t)(G - 1) * 8 * (3 + 2 * (m + 1));  // alpha, norm, [h, Gram] per step
+            h->bytes_nvlink = (int64_t)(m + 1) * vec + (int64_t)m * scal + (int64_t)(G - 1) * 8 * K;
+        }
         if (h->halo && !h->comm) {  // parts on one device pull from each other's x_g
             std::vector<const void *> src;
             for (Part &p : h->parts) src.push_back(p.xg);
@@ -1253,6 +1272,8 @@ topk_eig_s::~topk_eig_s() {
     clk.mark("destroy: pool");
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (evL) cudaEventDestroy(evL);
+    if (evJ) cudaEventDestroy(evJ);
     for (auto &q : prof) { cudaEventDestroy(q.a); cudaEventDestroy(q.b); }
     clk.mark("destroy: events");
     if (stream) cudaStreamDestroy(stream);
@@ -1326,9 +1347,16 @@ static void fill_info(topk_eig_s *h, topk_eig_info_t *info) {
     info->jacobi_sweeps = hget<int>(p, p.st.jac_sweeps);
     info->jacobi_converged = hget<int>(p, p.st.jac_conv);
     info->num_parts = h->G;
-    float ms = 0.f;
+    float ms = 0.f, ml = 0.f, mj = 0.f, mr = 0.f;
     cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    cudaEventElapsedTime(&ml, h->ev0, h->evL);
+    cudaEventElapsedTime(&mj, h->evL, h->evJ);
+    cudaEventElapsedTime(&mr, h->evJ, h->ev1);
     info->ms_solve = ms;
+    info->ms_lanczos = ml;
+    info->ms_jacobi = mj;
+    info->ms_ritz = mr;
+    info->bytes_nvlink = h->bytes_nvlink;
     info->bytes_model = h->bytes_model;
     info->gpu_launches = h->launches;
 }

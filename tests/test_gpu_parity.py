@@ -449,3 +449,16 @@ def test_partial_reorth(T, c3s, storage, tol):
     # sqrt(eps) level within a few steps, so most iterations take the pass
     assert 0 < r.info["reorth_passes"] < (m // 2 if storage == "f64" else m)
     assert normwise(th, ref.theta_all) <= tol
+
+
+# ------------------------------------------------------------------ info: phase times
+def test_info_phase_times(T, c3s):
+    """topk_eig_info_t ms_lanczos + ms_jacobi + ms_ritz partition ms_solve (events at the
+    phase boundaries inside the graph); one process: no interconnect bytes."""
+    with T.TopkEig(c3s, 8, "f32", "f64", m=24) as h:
+        for _ in range(2):
+            r = h.solve(seed=3)
+    i = r.info
+    assert i["ms_lanczos"] > 0 and i["ms_jacobi"] > 0 and i["ms_ritz"] > 0
+    assert abs(i["ms_lanczos"] + i["ms_jacobi"] + i["ms_ritz"] - i["ms_solve"]) <= 0.02 * i["ms_solve"] + 0.01
+    assert i["bytes_nvlink"] == 0
