@@ -124,6 +124,30 @@ def make_matrix(name: str):
     return S.config_matrix(name)
 
 
+def shared_matrix(name: str, rank: int, N: int, dist):
+    """One process per GPU: rank 0 generates the matrix once and writes it to a file
+    (synthgen.save_csr, /dev/shm when it has room, else /tmp); every rank maps it
+    read-only, so the pages are shared and each rank's create reads only the row
+    pointers and its own rows (plus its share of the symmetry hash). Returns
+    (matrix, path or None); rank 0 removes the file at the end."""
+    import shutil
+    import synthgen as S
+    if N == 1:
+        return make_matrix(name), None
+    tag = os.environ.get("TORCHELASTIC_RUN_ID", os.environ.get("MASTER_PORT", "0"))
+    path = None
+    if rank == 0:
+        A = make_matrix(name)
+        need = 8 * (A.n + 1) + 12 * A.nnz + 64
+        d = "/dev/shm" if shutil.disk_usage("/dev/shm").free > 1.2 * need else "/tmp"
+        path = os.path.join(d, f"topk_{name}_{tag}.csr")
+        S.save_csr(path, A)
+        del A
+    obj = [path]
+    dist.broadcast_object_list(obj, src=0)
+    return S.load_csr_mmap(obj[0]), obj[0]
+
+
 def gather_bound(nnz_g, t_ms):
     """The SpMV's other ceiling: one random 4/8-byte x gather
     per nonzero. profiles/gather_ceiling.json holds the measured B200 rate of
@@ -247,9 +271,13 @@ def main():
     if args.impl == "reference":
         return run_reference(args, wl)
 
-    import torch
     ws, rank, local = dist_env()
     N = max(ws, 1)
+    if N > 1 and rank > 0 and "OMP_NUM_THREADS" not in os.environ:
+        # the host cores are shared by the ranks (rank 0 keeps all of them: it generates
+        # the matrix while the others wait); set before libgomp loads
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or N) // N))
+    import torch
     if N != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
     torch.cuda.set_device(local)
@@ -259,7 +287,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2201_07498_b200 as T
 
-    A = make_matrix(wl["name"])
+    A, shared_path = shared_matrix(wl["name"], rank, N, dist)
     nid = None
     if N > 1:
         obj = [T.nccl_id() if rank == 0 else None]
@@ -411,6 +439,8 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
+        if rank == 0 and shared_path:
+            os.remove(shared_path)
         dist.destroy_process_group()
     return 0
 

@@ -237,6 +237,15 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
  * driver; returns the bytes released. Thread-safe; live handles are unaffected. */
 size_t topk_eig_trim_pool(void);
 
+/* Host-only: the symmetry check's four wrapping 64-bit hash sums over rows [r0, r1) of
+ * the canonical matrix (row a2, reading Q17): sums[0], sums[1] over the entries (r, c, v)
+ * with c > r, sums[2], sums[3] over the transposed entries with c < r (key (min, max),
+ * value bits). The sums are additive over row ranges: one process per GPU hashes its
+ * own rows and the ranks add their sums (create does this with an NCCL all-reduce);
+ * M = M^T passes always, an asymmetric M only on a double 64-bit collision. sums: host,
+ * 4 uint64 out. Errors as in create. */
+topk_status_t topk_eig_plan_symmetry(const topk_matrix_t *A, int64_t r0, int64_t r1, uint64_t *sums);
+
 /* Host-only halo plan of part g of G (reading Q27): the
  * remote entries part g's SpMV reads, grouped by owner q in ascending owner position,
  * exactly as topk_eig_create with opts.exchange = 1 lays them out after the own slot.

@@ -82,6 +82,7 @@ _SIGS = {
     "topk_eig_destroy": (None, [_P]),
     "topk_eig_trim_pool": (ctypes.c_size_t, []),
     "topk_eig_plan_halo": (_S, [_P, _I32, _I32, _P, _P, _P]),
+    "topk_eig_plan_symmetry": (_S, [_P, _I64, _I64, _P]),
     "topk_eig_last_error": (ctypes.c_char_p, []),
     "topk_eig_nccl_id": (_S, [_P]),
     "topk_eig_plan_partition": (_S, [_P, _I64, _I32, _P]),
@@ -130,6 +131,15 @@ def plan_halo(A, G: int, g: int) -> dict:
     pos = np.zeros(max(nh.value, 1), np.int32)
     _check(_lib.topk_eig_plan_halo(ctypes.byref(mat), G, g, ctypes.byref(nh), _ptr(off), _ptr(pos)))
     return {"n_halo": nh.value, "off": off, "pos": pos[:nh.value]}
+
+
+def plan_symmetry(A, r0: int, r1: int) -> np.ndarray:
+    """The four symmetry-check hash sums of rows [r0, r1) (topk_eig_plan_symmetry)."""
+    keep = []
+    mat = _matrix(A, keep)
+    out = np.zeros(4, np.uint64)
+    _check(_lib.topk_eig_plan_symmetry(ctypes.byref(mat), int(r0), int(r1), _ptr(out)))
+    return out
 
 
 def plan_partition(rowptr, G: int) -> np.ndarray:

@@ -188,9 +188,15 @@ static inline uint64_t sym_fmix(uint64_t x) {
     return x ^ (x >> 33);
 }
 bool is_symmetric(const Csr &m) {
+    uint64_t h[4];
+    symmetry_sums(m, 0, m.n, h);
+    return h[0] == h[2] && h[1] == h[3];
+}
+
+void symmetry_sums(const Csr &m, int64_t r0, int64_t r1, uint64_t out[4]) {
     uint64_t u1 = 0, u2 = 0, l1 = 0, l2 = 0;
 #pragma omp parallel for schedule(dynamic, 4096) reduction(+ : u1, u2, l1, l2)
-    for (int64_t r = 0; r < m.n; ++r) {
+    for (int64_t r = r0; r < r1; ++r) {
         for (int64_t k = m.rowptr[(size_t)r]; k < m.rowptr[(size_t)r + 1]; ++k) {
             const int64_t c = m.col[(size_t)k];
             if (c == r) continue;
@@ -203,7 +209,7 @@ bool is_symmetric(const Csr &m) {
             if (c > r) { u1 += h1; u2 += h2; } else { l1 += h1; l2 += h2; }
         }
     }
-    return u1 == l1 && u2 == l2;
+    out[0] = u1; out[1] = u2; out[2] = l1; out[3] = l2;
 }
 
 // Number of parts a left-to-right greedy packing with bottleneck B needs,

@@ -57,8 +57,12 @@ struct Csr {
 // a1: COO/CSR -> canonical CSR. Duplicates summed in input order.
 topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err);
 
-// a2: structural + bitwise value symmetry.
+// a2: structural + bitwise value symmetry (multiset hash, host_prep.cpp).
 bool is_symmetric(const Csr &m);
+// The four wrapping hash sums of rows [r0, r1) (upper h1, h2; transposed lower h1, h2).
+// The sums are additive over row ranges, so one process per GPU checks its own rows
+// and the ranks add their sums (the matrix is symmetric iff upper == lower for both).
+void symmetry_sums(const Csr &m, int64_t r0, int64_t r1, uint64_t out[4]);
 
 // a3: rule P (reading Q15). b has G+1 entries.
 topk_status_t partition_rule_p(const int64_t *rowptr, int64_t n, int32_t G, int64_t *b);

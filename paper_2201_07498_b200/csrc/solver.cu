@@ -1016,7 +1016,10 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     topk_status_t s = canonicalize(*A, csr, err);
     if (s != TOPK_OK) return fail(s, err);
     clk.mark("canonicalize");
-    if (o.check_symmetry >= 0 && !is_symmetric(csr)) return fail(TOPK_E_NOT_SYMMETRIC, "matrix is not symmetric");
+    // one process: the whole matrix here; one process per GPU: each rank hashes its own
+    // rows and the sums are added over the ranks once the communicator exists (below)
+    if (world == 1 && o.check_symmetry >= 0 && !is_symmetric(csr))
+        return fail(TOPK_E_NOT_SYMMETRIC, "matrix is not symmetric");
     clk.mark("symmetry check");
     h->bounds.resize((size_t)G + 1);
     s = partition_rule_p(csr.rowptr.data(), n, G, h->bounds.data());
@@ -1162,6 +1165,15 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             ncclUniqueId id;
             std::memcpy(&id, o.nccl_id, sizeof(id));
             NCCL_TRY(ncclCommInitRank(&h->comm, world, id, h->rank));
+            if (o.check_symmetry >= 0) {  // a2, distributed: the multiset hash sums are additive
+                uint64_t hs[4];
+                symmetry_sums(csr, h->bounds[(size_t)h->rank], h->bounds[(size_t)h->rank + 1], hs);
+                uint64_t *d_hs = h->alloc<uint64_t>(4);
+                CUDA_TRY(scopy(h->stream, d_hs, hs, sizeof(hs), cudaMemcpyHostToDevice));
+                NCCL_TRY(ncclAllReduce(d_hs, d_hs, 4, ncclUint64, ncclSum, h->comm, h->stream));
+                CUDA_TRY(scopy(h->stream, hs, d_hs, sizeof(hs), cudaMemcpyDeviceToHost));
+                if (!(hs[0] == hs[2] && hs[1] == hs[3])) return fail(TOPK_E_NOT_SYMMETRIC, "matrix is not symmetric");
+            }
         }
         // column map (global column -> device column entry), shared by the local parts
         // (with the halo exchange each part uploads its own compact map instead)
@@ -1548,6 +1560,21 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
             }
         if (sell) std::memcpy(sell, L.sell.data(), L.sell.size() * 8);
         if (items) std::memcpy(items, L.items.data(), L.items.size() * 4);
+    } catch (std::bad_alloc &) {
+        return fail(TOPK_E_NOMEM, "host allocation failed");
+    }
+    return TOPK_OK;
+}
+
+topk_status_t topk_eig_plan_symmetry(const topk_matrix_t *A, int64_t r0, int64_t r1, uint64_t *sums) {
+    if (!A || !sums) return fail(TOPK_E_INVALID, "A and sums must be non-NULL");
+    try {
+        Csr csr;
+        std::string err;
+        topk_status_t s = canonicalize(*A, csr, err);
+        if (s != TOPK_OK) return fail(s, err);
+        if (r0 < 0 || r1 < r0 || r1 > csr.n) return fail(TOPK_E_INVALID, "need 0 <= r0 <= r1 <= n");
+        symmetry_sums(csr, r0, r1, sums);
     } catch (std::bad_alloc &) {
         return fail(TOPK_E_NOMEM, "host allocation failed");
     }

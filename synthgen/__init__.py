@@ -180,6 +180,42 @@ def stars(degrees, dense=(), gap: int = 7, seed: int = 3) -> CSR:
     return CSR(n, np.cumsum(rowptr), col[o].astype(np.int32), val[o])
 
 
+_MAGIC = b"TKEVCSR1"
+
+
+def save_csr(path: str, A: CSR) -> None:
+    """Write A as one flat binary file (magic, n, nnz, int64 rowptr[n+1], int32
+    col[nnz] padded to 8 bytes, float64 val[nnz]) through a temporary name, so
+    readers never see a partial file (one process per GPU: rank 0 writes, the
+    others map it; SURVEY L0 "TKEV cache")."""
+    tmp = path + f".tmp{os.getpid()}"
+    with open(tmp, "wb") as f:
+        f.write(_MAGIC)
+        f.write(np.array([A.n, A.nnz], np.int64).tobytes())
+        np.ascontiguousarray(A.rowptr, np.int64).tofile(f)
+        np.ascontiguousarray(A.col, np.int32).tofile(f)
+        if A.nnz % 2:
+            f.write(b"\0" * 4)
+        np.ascontiguousarray(A.val, np.float64).tofile(f)
+    os.replace(tmp, path)
+
+
+def load_csr_mmap(path: str) -> CSR:
+    """Map a save_csr file read-only: the arrays are views of the page cache, shared
+    by every process that maps the same file (no per-process copy)."""
+    head = np.fromfile(path, dtype=np.int64, count=3)
+    if head[:1].tobytes() != _MAGIC:
+        raise ValueError(f"{path}: not a save_csr file")
+    n, nnz = int(head[1]), int(head[2])
+    o = 24
+    rowptr = np.memmap(path, np.int64, "r", offset=o, shape=(n + 1,))
+    o += 8 * (n + 1)
+    col = np.memmap(path, np.int32, "r", offset=o, shape=(max(nnz, 1),))[:nnz]
+    o += 4 * nnz + (4 if nnz % 2 else 0)
+    val = np.memmap(path, np.float64, "r", offset=o, shape=(max(nnz, 1),))[:nnz]
+    return CSR(n, rowptr, col, val)
+
+
 def hash3(s: int, a: int, b: int) -> int:
     return int(_load().sg_hash3(s, a, b))
 

@@ -161,3 +161,66 @@ def test_two_rank_halo_exchange_protocol():
         assert err <= 1e-13, (rank, err)
         assert exact_set, f"rank {rank}: halo is not exactly the touched remote columns"
         assert 0 < nhalo < nremote  # the halo is smaller than the peer's whole slot
+
+
+def _ingest_worker(rank, port, path, q):
+    """Rank-local ingest (one process per GPU at C4 scale): rank 0 writes the matrix
+    once (synthgen.save_csr), every rank maps it read-only, plans its own part from
+    the mapped arrays, and the distributed symmetry check adds the ranks' hash sums
+    over their own rows (topk_eig_plan_symmetry; create does this with NCCL)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import paper_2201_07498_b200 as T
+        if rank == 0:
+            S.save_csr(path, S.rmat(12, 40_000, 14))
+        dist.barrier()
+        A = S.load_csr_mmap(path)
+        ref = S.rmat(12, 40_000, 14)
+        same = (A.n == ref.n and np.array_equal(A.rowptr, ref.rowptr) and np.array_equal(A.col, ref.col)
+                and np.array_equal(A.val, ref.val))
+        G = WORLD
+        b = T.plan_partition(np.asarray(A.rowptr), G)
+        L = T.plan_layout(A, G, rank, "f64")
+        Lr = T.plan_layout(ref, G, rank, "f64")
+        layout_same = all(np.array_equal(L[k], Lr[k]) for k in ("rowptr", "col", "val", "perm"))
+
+        def global_ok(M):
+            mine = T.plan_symmetry(M, int(b[rank]), int(b[rank + 1]))
+            allh = [torch.zeros(4, dtype=torch.int64) for _ in range(G)]
+            dist.all_gather(allh, torch.from_numpy(mine.view(np.int64).copy()))
+            tot = np.zeros(4, np.uint64)
+            for t in allh:  # wrapping uint64 sums, rank order
+                tot = tot + t.numpy().view(np.uint64)
+            return bool(tot[0] == tot[2] and tot[1] == tot[3]), tot
+
+        sym, tot = global_ok(A)
+        whole = T.plan_symmetry(ref, 0, ref.n)
+        # one asymmetric value (an entry in rank 1's rows): the summed check must fail
+        bad = S.CSR(ref.n, ref.rowptr.copy(), ref.col.copy(), ref.val.copy())
+        k = int(ref.rowptr[int(b[1])])
+        bad.val[k] += 1.0 / 128
+        asym, _ = global_ok(bad)
+        q.put((rank, same, layout_same, sym, np.array_equal(tot, whole), asym))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_shared_ingest_and_distributed_symmetry(tmp_path):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = str(tmp_path / "m.csr")
+    procs = [ctx.Process(target=_ingest_worker, args=(r, port, path, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, layout_same, sym, whole_eq, asym in out:
+        assert same, f"rank {rank}: mapped matrix differs"
+        assert layout_same, f"rank {rank}: layout from the mapped arrays differs"
+        assert sym and whole_eq, f"rank {rank}: distributed symmetry sums"
+        assert not asym, f"rank {rank}: asymmetric value not detected"
