@@ -129,10 +129,13 @@ typedef struct {
      * cluster, else one CTA in global memory), 1 -> one CTA only, 2 -> cluster at any m;
      * jacobi_cluster 0 -> auto (8 CTAs, 16 from m = 96), 8 or 16 -> that size first;
      * restart_loop 0 -> thick-restart cycles in a CUDA-graph WHILE node when the solve is
-     * captured, 1 -> unrolled cycles. */
+     * captured, 1 -> unrolled cycles; ritz_path below. */
     int32_t jacobi_path;
     int32_t jacobi_cluster;
     int32_t restart_loop;
+    /* Ritz output pass (a14) with compute dtype f64: 0 -> fp64 tensor cores (mma.sync
+     * m8n8k4 f64) when the coefficients fit shared memory, 1 -> fp64 FMA on CUDA cores */
+    int32_t ritz_path;
 } topk_eig_opts_t;
 
 typedef struct {

@@ -1377,6 +1377,103 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz(RitzArgs a) {
     }
 }
 
+// a14 output pass on the fp64 tensor-core path (mma.sync m8n8k4 f64, DMMA): the same
+// projection Y = V_stored C (C = coefS: S_K diag(s), sign-fixed) and scaling by
+// 1/||y_k|| as k_ritz pass 1, for compute dtype f64. A warp owns 32 positions x 8 TN
+// outputs: per step of 4 basis columns it loads one f32/f64 basis element per position
+// tile (A fragments, converted to f64) and one coefficient per output tile from shared
+// memory (B fragments), and issues TM x TN DMMAs; accumulators stay in registers. The
+// coefficients of the block's output group are staged once in shared memory
+// [mm rounded up to 4][8 TN]. Writes yt[group][position][8] like k_ritz pass 1.
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+#ifndef TOPK_RITZ_TM
+#define TOPK_RITZ_TM 8
+#endif
+constexpr int kRitzTM = TOPK_RITZ_TM;  // position tiles of 8 per warp (dev build variant)
+template <typename ST, int TN>
+__global__ void __launch_bounds__(kNT, 2) k_ritz_mma(RitzArgs a) {
+    static_assert(kRitzKB == 8, "yt groups of 8 outputs");
+    extern __shared__ double csm[];  // coef [mm4][8 TN], then inv [8 TN]
+    constexpr int NO = 8 * TN;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int mm = *a.st.m_found, kf = *a.st.k_found, K = a.K;
+    const int nog = (K + NO - 1) / NO;
+    const int og = (int)(blockIdx.x % (unsigned)nog);
+    const int rblk = (int)(blockIdx.x / (unsigned)nog), nrblk = (int)(gridDim.x / (unsigned)nog);
+    const int k0 = og * NO;
+    if (k0 >= kf) return;
+    void *out = *a.out_ptr;
+    if (!out) return;
+    const int dt = *a.out_dtype;
+    const int mm4 = (mm + 3) & ~3;
+    double *coef = csm;
+    double *inv = csm + (size_t)mm4 * NO;
+    for (int i = tid; i < mm4 * NO; i += kNT) {
+        const int j = i / NO, q = i - j * NO;
+        coef[i] = (j < mm && k0 + q < kf) ? a.st.coefS[(size_t)j * K + k0 + q] : 0.0;
+    }
+    if (tid < NO) {
+        double sq = 0.0;
+        if (a.st.use_gram) sq = (k0 + tid < kf) ? a.st.rnrm2[k0 + tid] : 1.0;
+        else
+            for (int q = 0; q < a.G; ++q) sq += __ldcg(a.ex.ritz_part + (size_t)q * K + k0 + tid);
+        inv[tid] = (k0 + tid < kf) ? 1.0 / sqrt(sq) : 0.0;
+    }
+    __syncthreads();
+    const ST *V = reinterpret_cast<const ST *>(a.V);
+    const int r = lane >> 2, c = lane & 3;  // fragment row / column of this lane
+    const int64_t ntile = a.npad / (8 * kRitzTM);
+    const int warp = (int)(rblk * (kNT / 32) + (tid >> 5)), nwarp = nrblk * (kNT / 32);
+    for (int64_t t = warp; t < ntile; t += nwarp) {
+        const int64_t p0 = t * 8 * kRitzTM;
+        double acc[kRitzTM][TN][2];
+#pragma unroll
+        for (int i = 0; i < kRitzTM; ++i)
+#pragma unroll
+            for (int n = 0; n < TN; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
+        // A fragments one step ahead: the next 4 basis columns' loads are in flight
+        // while this step's DMMAs run
+        ST araw[kRitzTM];
+#pragma unroll
+        for (int i = 0; i < kRitzTM; ++i)
+            araw[i] = (c < mm) ? V[(size_t)c * a.npad + p0 + 8 * i + r] : ST(0);
+        for (int j0 = 0; j0 < mm4; j0 += 4) {
+            double af[kRitzTM];
+#pragma unroll
+            for (int i = 0; i < kRitzTM; ++i) af[i] = cvt<double>(araw[i]);
+            const int jn = j0 + 4 + c;
+#pragma unroll
+            for (int i = 0; i < kRitzTM; ++i)
+                araw[i] = (jn < mm) ? V[(size_t)jn * a.npad + p0 + 8 * i + r] : ST(0);
+            double bf[TN];
+#pragma unroll
+            for (int n = 0; n < TN; ++n) bf[n] = coef[(j0 + c) * NO + 8 * n + r];
+#pragma unroll
+            for (int i = 0; i < kRitzTM; ++i)
+#pragma unroll
+                for (int n = 0; n < TN; ++n) dmma_8x8x4(acc[i][n][0], acc[i][n][1], af[i], bf[n]);
+        }
+        // D fragment: lane holds rows r, columns 2c, 2c + 1 of each 8 x 8 tile
+#pragma unroll
+        for (int i = 0; i < kRitzTM; ++i) {
+            const int64_t p = p0 + 8 * i + r;
+#pragma unroll
+            for (int n = 0; n < TN; ++n) {
+                if ((og * TN + n) * 8 >= K) break;  // groups past ceil(K / 8): not in yt
+                const int kk = 8 * n + 2 * c;
+                const double y0 = acc[i][n][0] * inv[kk], y1 = acc[i][n][1] * inv[kk + 1];
+                const size_t o = ((size_t)(og * TN + n) * a.npad + (size_t)p) * kRitzKB + 2 * c;
+                if (dt == 0) __stcs(reinterpret_cast<double2 *>(reinterpret_cast<double *>(a.yt) + o), make_double2(y0, y1));
+                else __stcs(reinterpret_cast<float2 *>(reinterpret_cast<float *>(a.yt) + o), make_float2((float)y0, (float)y1));
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Thick restart (reading Q26; not in the paper):
 // Y_j = sum_l coefR[l][j] u_l (coefR = S_J diag(s), the kept Ritz vectors of the

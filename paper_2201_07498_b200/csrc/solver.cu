@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <thread>
+#include <type_traits>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -149,6 +150,7 @@ struct topk_eig_s {
     int use_graph = 1;
     int nsm = 148;
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
+    int ritz_tn = 0;           // > 0: Ritz output pass on the fp64 tensor cores, 8 * ritz_tn outputs per warp
     bool use_gram = false;  // Ritz norms from the Gram matrix (reading Q24; no Ritz pass 0)
     int grid_stepw[kStepMaxNC + 1] = {0};
     int grid_corrw[kCorrMaxNC + 1] = {0};
@@ -158,6 +160,7 @@ struct topk_eig_s {
     bool corrw = true;                 // exact-width correction for it <= kCorrMaxNC
 #endif
     bool restart_unrolled = false;     // opts.restart_loop = 1: unrolled restart cycles, no WHILE node
+    int ritz_mode = 0;                 // opts.ritz_path: 0 auto, 1 fp64 CUDA cores only
     std::vector<int64_t> bounds;
     std::vector<Part> parts;
     Exch ex{};
@@ -529,6 +532,27 @@ static void record_event(topk_eig_s *h, cudaEvent_t e) {
     else CUDA_TRY(cudaEventRecord(e, h->stream));
 }
 
+// a14 output pass on the fp64 tensor cores (k_ritz_mma; compute dtype f64 only)
+template <typename ST, int TN>
+static void ritz_mma_tn(topk_eig_s *h, const RitzArgs &a) {
+    const int nog = (h->K + 8 * TN - 1) / (8 * TN);
+    const size_t smem = ((size_t)((h->m + 3) & ~3) * 8 * TN + 8 * TN) * sizeof(double);
+    k_ritz_mma<ST, TN><<<(unsigned)(h->nsm * 2 * nog), kNT, smem, h->stream>>>(a);
+}
+template <typename ST, typename CT>
+static void launch_ritz_mma(topk_eig_s *h, const RitzArgs &a) {
+    if constexpr (std::is_same<CT, double>::value) {
+        switch (h->ritz_tn) {
+            case 1: ritz_mma_tn<ST, 1>(h, a); break;
+            case 2: ritz_mma_tn<ST, 2>(h, a); break;
+            case 3: ritz_mma_tn<ST, 3>(h, a); break;
+            default: ritz_mma_tn<ST, 4>(h, a); break;
+        }
+    } else {
+        throw CudaFail("k_ritz_mma needs compute dtype f64");
+    }
+}
+
 template <typename VT, typename ST, typename CT>
 static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
     // a5: v1
@@ -669,7 +693,8 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
             const unsigned ngroups = (unsigned)((h->K + kRitzKB - 1) / kRitzKB);
             const dim3 grid((unsigned)h->grid_ritz * ngroups);
             prof_begin(h, p, 5 + pass);
-            if (pass == 0) k_ritz<ST, CT, kRitzKB, 0><<<grid, kNT, smem, h->stream>>>(a);
+            if (pass == 1 && h->ritz_tn > 0) launch_ritz_mma<ST, CT>(h, a);
+            else if (pass == 0) k_ritz<ST, CT, kRitzKB, 0><<<grid, kNT, smem, h->stream>>>(a);
             else k_ritz<ST, CT, kRitzKB, 1><<<grid, kNT, smem, h->stream>>>(a);
             CUDA_TRY(cudaGetLastError());
             prof_end(h, p);
@@ -728,6 +753,14 @@ static void set_kernels(topk_eig_s *h) {
                                   (int)(1024 * kRitzKB * sizeof(double))));
     CUDA_TRY(cudaFuncSetAttribute(k_ritz<ST, CT, kRitzKB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(1024 * kRitzKB * sizeof(double))));
+    if constexpr (std::is_same<CT, double>::value) {
+        // fp64 tensor-core output pass when the coefficients fit 96 KB of shared memory
+        const int tn = h->K <= 8 ? 1 : h->K <= 16 ? 2 : h->K <= 24 ? 3 : 4;
+        const size_t smem = ((size_t)((h->m + 3) & ~3) * 8 * tn + 8 * tn) * sizeof(double);
+        h->ritz_tn = (smem <= 96 * 1024 && h->ritz_mode != 1) ? tn : 0;
+        for (auto f : {&k_ritz_mma<ST, 1>, &k_ritz_mma<ST, 2>, &k_ritz_mma<ST, 3>, &k_ritz_mma<ST, 4>})
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    }
 }
 
 static bool select_kernels(topk_eig_s *h) {
@@ -1005,6 +1038,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (o.jacobi_cluster != 0 && o.jacobi_cluster != 8 && o.jacobi_cluster != 16)
         return fail(TOPK_E_INVALID, "jacobi_cluster must be 0, 8 or 16");
     h->restart_unrolled = o.restart_loop == 1;
+    if (o.ritz_path < 0 || o.ritz_path > 1) return fail(TOPK_E_INVALID, "ritz_path must be 0 or 1");
+    h->ritz_mode = o.ritz_path;
     h->use_graph = o.use_graph >= 0;
     h->profile = o.profile > 0;
     h->device = o.device;
