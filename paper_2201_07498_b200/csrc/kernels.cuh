@@ -1397,6 +1397,7 @@ constexpr int kRitzTM = TOPK_RITZ_TM;  // position tiles of 8 per warp (dev buil
 template <typename ST, int TN>
 __global__ void __launch_bounds__(kNT, 2) k_ritz_mma(RitzArgs a) {
     static_assert(kRitzKB == 8, "yt groups of 8 outputs");
+    constexpr int TM = TN >= 4 ? 4 : kRitzTM;  // 8 x 4 position tiles spill at 4 output tiles
     extern __shared__ double csm[];  // coef [mm4][8 TN], then inv [8 TN]
     constexpr int NO = 8 * TN;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -1426,40 +1427,40 @@ __global__ void __launch_bounds__(kNT, 2) k_ritz_mma(RitzArgs a) {
     __syncthreads();
     const ST *V = reinterpret_cast<const ST *>(a.V);
     const int r = lane >> 2, c = lane & 3;  // fragment row / column of this lane
-    const int64_t ntile = a.npad / (8 * kRitzTM);
+    const int64_t ntile = a.npad / (8 * TM);
     const int warp = (int)(rblk * (kNT / 32) + (tid >> 5)), nwarp = nrblk * (kNT / 32);
     for (int64_t t = warp; t < ntile; t += nwarp) {
-        const int64_t p0 = t * 8 * kRitzTM;
-        double acc[kRitzTM][TN][2];
+        const int64_t p0 = t * 8 * TM;
+        double acc[TM][TN][2];
 #pragma unroll
-        for (int i = 0; i < kRitzTM; ++i)
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int n = 0; n < TN; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
         // A fragments one step ahead: the next 4 basis columns' loads are in flight
         // while this step's DMMAs run
-        ST araw[kRitzTM];
+        ST araw[TM];
 #pragma unroll
-        for (int i = 0; i < kRitzTM; ++i)
+        for (int i = 0; i < TM; ++i)
             araw[i] = (c < mm) ? V[(size_t)c * a.npad + p0 + 8 * i + r] : ST(0);
         for (int j0 = 0; j0 < mm4; j0 += 4) {
-            double af[kRitzTM];
+            double af[TM];
 #pragma unroll
-            for (int i = 0; i < kRitzTM; ++i) af[i] = cvt<double>(araw[i]);
+            for (int i = 0; i < TM; ++i) af[i] = cvt<double>(araw[i]);
             const int jn = j0 + 4 + c;
 #pragma unroll
-            for (int i = 0; i < kRitzTM; ++i)
+            for (int i = 0; i < TM; ++i)
                 araw[i] = (jn < mm) ? V[(size_t)jn * a.npad + p0 + 8 * i + r] : ST(0);
             double bf[TN];
 #pragma unroll
             for (int n = 0; n < TN; ++n) bf[n] = coef[(j0 + c) * NO + 8 * n + r];
 #pragma unroll
-            for (int i = 0; i < kRitzTM; ++i)
+            for (int i = 0; i < TM; ++i)
 #pragma unroll
                 for (int n = 0; n < TN; ++n) dmma_8x8x4(acc[i][n][0], acc[i][n][1], af[i], bf[n]);
         }
         // D fragment: lane holds rows r, columns 2c, 2c + 1 of each 8 x 8 tile
 #pragma unroll
-        for (int i = 0; i < kRitzTM; ++i) {
+        for (int i = 0; i < TM; ++i) {
             const int64_t p = p0 + 8 * i + r;
 #pragma unroll
             for (int n = 0; n < TN; ++n) {
