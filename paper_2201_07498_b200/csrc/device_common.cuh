@@ -7,6 +7,23 @@
 
 namespace topk {
 
+// Device-side checks of a dev build variant (tools/build.py build_variant with
+// TOPK_CHECKS; tools/check_run.sh): bounds of every gather / scatter index and the
+// ticket counters of the last-block reductions. A failed check prints and traps.
+// compute-sanitizer is not available on this GPU pool, so these replace it.
+#ifdef TOPK_CHECKS
+#define TOPK_DCHECK(cond, what)                                                              \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("TOPK_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__,    \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define TOPK_DCHECK(cond, what) do { } while (0)
+#endif
+
 using bf16 = __nv_bfloat16;
 
 // ---- storage dtype traits: vector width for 16-byte loads -------------------
@@ -184,7 +201,11 @@ __device__ __forceinline__ T block_sum_array(const T *a, int n, int stride, T *s
 __device__ __forceinline__ bool arrive_last_n(unsigned *counter, unsigned nblocks, int *sflag) {
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *sflag = (atomicAdd(counter, 1u) == nblocks - 1);
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(counter, 1u);
+        TOPK_DCHECK(prev < nblocks, "last-block ticket past the grid (counter not reset)");
+        *sflag = (prev == nblocks - 1);
+    }
     __syncthreads();
     const bool last = *sflag;
     if (last) __threadfence();

@@ -200,6 +200,7 @@ struct SpmvArgs {
     unsigned *long_cnt;   // [nlong]
     double *alpha_long;   // [nlong]
     const void *x;        // gather source: V column it-1 (G = 1) or the replica
+    int64_t xlen;         // elements of x (TOPK_CHECKS bounds)
     const void *ui;       // local u_it (V column it-1)
     void *y;              // v_tmp (Q2), storage dtype
     double *y_dbg;        // optional fp64 unscaled row sums (debug export)
@@ -272,7 +273,10 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             for (int t0 = 0; t0 < nt; t0 += GQ) {
                 ST xg[GQ];  // raw storage values, converted at use
 #pragma unroll
-                for (int q = 0; q < GQ; ++q) xg[q] = (t0 + q < nt) ? __ldg(x + cc[q]) : ST(0);
+                for (int q = 0; q < GQ; ++q) {
+                    TOPK_DCHECK(t0 + q >= nt || (cc[q] >= 0 && cc[q] < a.xlen), "SpMV chunk gather out of x");
+                    xg[q] = (t0 + q < nt) ? __ldg(x + cc[q]) : ST(0);
+                }
                 VT vc[GQ];
 #pragma unroll
                 for (int q = 0; q < GQ; ++q) {
@@ -291,6 +295,7 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             CT part = warp_sum(acc0 + acc1);
             if (lane == 0) {
                 if (clid < 0) {
+                    TOPK_DCHECK(crow >= 0 && crow < a.nbig, "big-row position");
                     const CT yv = s * part;
                     y[crow] = rnd_ct<ST, CT>(yv);
                     alpha_acc += yv * (s * cvt<CT>(ui[crow]));
@@ -300,6 +305,7 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
                     a.long_parts[wi] = (double)part;
                     __threadfence();
                     const unsigned prev = atomicAdd(a.long_cnt + clid, 1u);
+                    TOPK_DCHECK(prev < (unsigned)L.z && crow == L.x, "long-row ticket");
                     if (prev == (unsigned)L.z - 1) {
                         __threadfence();
                         CT sum = CT(0);
@@ -334,7 +340,10 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             for (int t0 = 0; t0 < ntot; t0 += GQ) {
                 ST xg[GQ];  // raw storage values, converted at use
 #pragma unroll
-                for (int q = 0; q < GQ; ++q) xg[q] = (t0 + q < ntot) ? __ldg(x + cc[q]) : ST(0);
+                for (int q = 0; q < GQ; ++q) {
+                    TOPK_DCHECK(t0 + q >= ntot || (cc[q] >= 0 && cc[q] < a.xlen), "SpMV SELL gather out of x");
+                    xg[q] = (t0 + q < ntot) ? __ldg(x + cc[q]) : ST(0);
+                }
                 VT vc[GQ];
 #pragma unroll
                 for (int q = 0; q < GQ; ++q) {
@@ -1620,7 +1629,8 @@ __global__ void __launch_bounds__(kNT) k_restart_copy(RestartArgs a) {
 template <typename VT>
 __global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const int32_t *scol, const VT *sval,
                                                     const int32_t *perm, const int64_t *drp, const int32_t *colmap,
-                                                    int nbig, int32_t *pcol, VT *pval) {
+                                                    int nbig, int64_t nphys, int32_t *pcol, VT *pval) {
+    (void)nphys;
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1628,6 +1638,7 @@ __global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const in
         const int r = perm[p];
         const int64_t k0 = srp[r], len = srp[r + 1] - k0, d0 = drp[p];
         for (int64_t e = lane; e < len; e += 32) {
+            TOPK_DCHECK(d0 + e < nphys && d0 + e < drp[nbig], "big-row scatter destination");
             pcol[d0 + e] = colmap[scol[k0 + e]];
             pval[d0 + e] = sval[k0 + e];
         }
@@ -1638,7 +1649,8 @@ template <typename VT>
 __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const int32_t *scol, const VT *sval,
                                                      const int32_t *perm, const int64_t *drp, const int32_t *colmap,
                                                      const longlong2 *sell, int64_t nbig, int64_t nne, int64_t nsl,
-                                                     int32_t *pcol, VT *pval) {
+                                                     int64_t nphys, int32_t *pcol, VT *pval) {
+    (void)nphys;
     const int64_t tot = 32 * nsl;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sl = i >> 5, lane = i & 31, p = nbig + i;
@@ -1648,6 +1660,7 @@ __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const i
             len = drp[p + 1] - drp[p];
             k0 = srp[perm[p]];
         }
+        TOPK_DCHECK(len <= S.y && S.x + 32 * S.y <= nphys, "SELL slice bounds");
         for (int64_t e = 0; e < S.y; ++e) {
             const int64_t d = S.x + 32 * e + lane;
             if (e < len) {

@@ -363,6 +363,7 @@ static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     a.alpha_long = p.alpha_long; a.nlong = p.nlong;
     const void *ucol = (const char *)p.V + (size_t)(it - 1) * p.npad * sizeof(ST);
     a.x = (h->G == 1) ? ucol : (h->halo ? p.xg : h->replica);
+    a.xlen = (h->G == 1) ? p.npad : (h->halo ? p.npad + p.nhalo : (int64_t)h->G * p.npad);
     a.ui = ucol;
     a.y = p.y; a.y_dbg = y_dbg;
     a.slots = p.slots; a.counter = p.counters + 1;
@@ -893,14 +894,14 @@ static void device_layout_t(topk_eig_s *h, Part &p, const PartLayout &L, const D
     const VT *sval = static_cast<const VT *>(d.sval);
     if (L.nbig > 0) {
         k_layout_big<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap, L.nbig,
-                                                           p.col, reinterpret_cast<VT *>(p.val));
+                                                           L.nphys, p.col, reinterpret_cast<VT *>(p.val));
         CUDA_TRY(cudaGetLastError());
     }
     const int64_t nsl = (int64_t)L.sell.size() / 2;
     if (nsl > 0) {
         k_layout_sell<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap,
                                                             reinterpret_cast<const longlong2 *>(p.sell), (int64_t)L.nbig,
-                                                            L.nnonempty, nsl, p.col, reinterpret_cast<VT *>(p.val));
+                                                            L.nnonempty, nsl, L.nphys, p.col, reinterpret_cast<VT *>(p.val));
         CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
