@@ -136,6 +136,13 @@ typedef struct {
     /* Ritz output pass (a14) with compute dtype f64: 0 -> fp64 tensor cores (mma.sync
      * m8n8k4 f64) when the coefficients fit shared memory, 1 -> fp64 FMA on CUDA cores */
     int32_t ritz_path;
+    /* overlapped vector exchange: with G > 1 and
+     * exchange = 0 the SpMV runs as two passes, the own-slot columns first (they need nothing
+     * from the peers), then the other columns and the epilogue; one process per GPU runs the
+     * allgather of v_i on a second stream during the first pass. 0 -> on with one process per
+     * GPU, off in one process; 1 -> on (also in one process: same kernels and sums as the
+     * multi-process run); -1 -> off (one pass after the exchange). */
+    int32_t overlap;
 } topk_eig_opts_t;
 
 typedef struct {

@@ -53,7 +53,7 @@ class _Opts(ctypes.Structure):
                 ("max_restarts", ctypes.c_int32), ("exchange", ctypes.c_int32),
                 ("reorth_period", ctypes.c_int32), ("jacobi_path", ctypes.c_int32),
                 ("jacobi_cluster", ctypes.c_int32), ("restart_loop", ctypes.c_int32),
-                ("ritz_path", ctypes.c_int32)]
+                ("ritz_path", ctypes.c_int32), ("overlap", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -225,7 +225,7 @@ class TopkEig:
                  conv_tol: float = 0.0, conv_check: int = 0, restart_keep: int = 0,
                  max_restarts: int = 0, exchange: str = "allgather", reorth_period: int = 0,
                  jacobi_path: str = "auto", jacobi_cluster: int = 0, restart_loop: str = "auto",
-                 ritz_path: str = "auto"):
+                 ritz_path: str = "auto", overlap: int = 0):
         self._h = ctypes.c_void_p()
         self.n = int(A.n)
         self.K = int(K)
@@ -253,6 +253,7 @@ class TopkEig:
         o.jacobi_cluster = int(jacobi_cluster)
         o.restart_loop = {"auto": 0, "unrolled": 1}[restart_loop]
         o.ritz_path = {"auto": 0, "cuda_cores": 1}[ritz_path]
+        o.overlap = int(overlap)
         idbuf = None
         if nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

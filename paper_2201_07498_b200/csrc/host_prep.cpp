@@ -437,6 +437,52 @@ topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32
     return TOPK_OK;
 }
 
+void build_pass_tables(const int32_t *deg, int64_t nbig, int64_t nne, bool min_one, PassTables &out) {
+    out.bigptr.assign((size_t)nbig + 1, 0);
+    for (int64_t p = 0; p < nbig; ++p) out.bigptr[(size_t)p + 1] = out.bigptr[(size_t)p] + deg[(size_t)p];
+    out.chunks.clear();
+    out.longrows.clear();
+    for (int64_t p = 0; p < nbig; ++p) {
+        const int64_t rb = out.bigptr[(size_t)p], len = out.bigptr[(size_t)p + 1] - rb;
+        int32_t nch = (int32_t)((len + kChunkNnz - 1) / kChunkNnz);
+        if (nch == 0 && min_one) nch = 1;
+        const int32_t lid = nch > 1 ? (int32_t)out.longrows.size() : -1;
+        if (nch > 1) out.longrows.push_back(LongRow{(int32_t)p, (int32_t)out.chunks.size(), nch, 0});
+        for (int32_t c = 0; c < nch; ++c)
+            out.chunks.push_back(Chunk{rb + (int64_t)c * kChunkNnz, (int32_t)p,
+                                       (int32_t)std::max<int64_t>(0, std::min<int64_t>(kChunkNnz, len - (int64_t)c * kChunkNnz)),
+                                       lid, 0});
+    }
+    const int64_t nsl = (nne - nbig + 31) / 32;
+    out.sell.assign((size_t)(2 * nsl), 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        const int64_t p0 = nbig + 32 * sl, p1 = std::min(nne, p0 + 32);
+        int64_t w = min_one ? 1 : 0;
+        for (int64_t p = p0; p < p1; ++p) w = std::max<int64_t>(w, deg[(size_t)p]);
+        out.sell[(size_t)(2 * sl + 1)] = w;
+    }
+    int64_t phys = out.bigptr[(size_t)nbig];
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        out.sell[(size_t)(2 * sl)] = phys;
+        phys += 32 * out.sell[(size_t)(2 * sl + 1)];
+    }
+    out.items.clear();
+    for (int64_t sl = 0; sl < nsl;) {
+        if (out.sell[(size_t)(2 * sl + 1)] == 0) { ++sl; continue; }  // nothing of this pass in the slice
+        int64_t e = sl, width = 0;
+        while (e < nsl && out.sell[(size_t)(2 * e + 1)] > 0 &&
+               (e == sl || width + out.sell[(size_t)(2 * e + 1)] <= kSellItemWidth)) {
+            width += out.sell[(size_t)(2 * e + 1)];
+            ++e;
+        }
+        out.items.push_back((int32_t)sl);
+        out.items.push_back((int32_t)e);
+        sl = e;
+    }
+    out.nphys = phys;
+}
+
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err) {
     topk_status_t s = build_part_tables(m, b, G, g, npad, pos, out, err);

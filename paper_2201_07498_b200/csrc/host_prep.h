@@ -158,6 +158,25 @@ struct PartLayout {
     std::vector<int32_t> items;     // 2 per SELL work item: first slice, end slice
 };
 
+// Tables of one SpMV pass over a SUBSET of every row's entries (DESIGN.md section 8,
+// the overlapped exchange: own-slot columns first, then the others), from the pass
+// degree deg[p] of each position: big rows = positions [0, nbig) of the full layout,
+// their pass entries contiguous at bigptr[p] and cut into ceil(d / kChunkNnz) chunks;
+// SELL slices over [nbig, nne) with width = the largest pass degree of the slice's
+// rows, padded with (col 0, value 0); slices of width 0 and big rows without pass
+// entries get no work (their partial sums stay 0). With min_one = true every big row
+// gets a chunk and every slice width >= 1 (the final pass finishes every non-empty
+// row). With every entry in the pass this is the single-pass format above.
+struct PassTables {
+    std::vector<int64_t> bigptr;    // nbig+1
+    std::vector<Chunk> chunks;
+    std::vector<LongRow> longrows;
+    std::vector<int64_t> sell;      // 2 per slice: base, width
+    std::vector<int32_t> items;     // 2 per SELL work item: first slice, end slice
+    int64_t nphys = 0;
+};
+void build_pass_tables(const int32_t *deg, int64_t nbig, int64_t nne, bool min_one, PassTables &out);
+
 topk_status_t build_part(const Csr &m, const int64_t *b, int32_t G, int32_t g, int64_t npad,
                          const int32_t *pos, const int32_t *colmap, PartLayout &out, std::string &err);
 // The same layout without the physical arrays (perm, rowptr, chunks, long rows,

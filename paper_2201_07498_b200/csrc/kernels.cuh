@@ -201,6 +201,8 @@ struct SpmvArgs {
     double *alpha_long;   // [nlong]
     const void *x;        // gather source: V column it-1 (G = 1) or the replica
     int64_t xlen;         // elements of x (TOPK_CHECKS bounds)
+    double *ypart;        // two-pass SpMV (overlapped exchange): own-slot row sums, written by the
+                          // first pass, added by the final one; nullptr: one pass
     const void *ui;       // local u_it (V column it-1)
     void *y;              // v_tmp (Q2), storage dtype
     double *y_dbg;        // optional fp64 unscaled row sums (debug export)
@@ -221,7 +223,11 @@ __device__ __forceinline__ int ld_col_stream(const int32_t *p) {
     return v;
 }
 
-template <typename VT, typename ST, typename CT>
+template <typename VT, typename ST, typename CT, bool LOCAL>
+// LOCAL: the first pass of the two-pass SpMV: only the own-slot
+// columns, which do not wait for the vector exchange; unscaled fp64 row sums to
+// ypart, no alpha, no state writes. Otherwise the final (or only) pass, which adds
+// ypart (when set) before the epilogue.
 // dev knobs (tools/build.py build_variant): prefetch depth and an optional
 // min-blocks bound. Measured on C3 (tools/lab/spmv_variants.py): GQ 8 with the plain
 // bound (80 registers, 3 CTAs/SM) 229 us; GQ 4 / 6 at 4 CTAs/SM 229 / 232 us; an
@@ -239,9 +245,14 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
     __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
 
-    double sd;
-    if (!lz_prologue(it, a.st, a.ex, a.G, sd)) return;
+    double sd = 1.0;
+    if constexpr (LOCAL) {
+        if (*(volatile int *)a.st.done) return;  // no state writes: the final pass does them
+    } else {
+        if (!lz_prologue(it, a.st, a.ex, a.G, sd)) return;
+    }
     const CT s = (CT)sd;
+    const double *__restrict__ yp = a.ypart;
     const int lane = threadIdx.x & 31;
     const int gwarp = (int)((blockIdx.x * kSpmvNT + threadIdx.x) >> 5);
     const int nwarps = (int)(gridDim.x * (kSpmvNT / 32));
@@ -296,10 +307,15 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             if (lane == 0) {
                 if (clid < 0) {
                     TOPK_DCHECK(crow >= 0 && crow < a.nbig, "big-row position");
-                    const CT yv = s * part;
-                    y[crow] = rnd_ct<ST, CT>(yv);
-                    alpha_acc += yv * (s * cvt<CT>(ui[crow]));
-                    if (a.y_dbg) a.y_dbg[crow] = (double)part;
+                    if constexpr (LOCAL) {
+                        a.ypart[crow] = (double)part;
+                    } else {
+                        if (yp) part += (CT)__ldcg(yp + crow);
+                        const CT yv = s * part;
+                        y[crow] = rnd_ct<ST, CT>(yv);
+                        alpha_acc += yv * (s * cvt<CT>(ui[crow]));
+                        if (a.y_dbg) a.y_dbg[crow] = (double)part;
+                    }
                 } else {
                     const int4 L = __ldg(a.longrows + clid);
                     a.long_parts[wi] = (double)part;
@@ -310,10 +326,15 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
                         __threadfence();
                         CT sum = CT(0);
                         for (int q = 0; q < L.z; ++q) sum += (CT)__ldcg(a.long_parts + L.y + q);
-                        const CT yv = s * sum;
-                        y[L.x] = rnd_ct<ST, CT>(yv);
-                        a.alpha_long[clid] = (double)(yv * (s * cvt<CT>(ui[L.x])));
-                        if (a.y_dbg) a.y_dbg[L.x] = (double)sum;
+                        if constexpr (LOCAL) {
+                            a.ypart[L.x] = (double)sum;
+                        } else {
+                            if (yp) sum += (CT)__ldcg(yp + L.x);
+                            const CT yv = s * sum;
+                            y[L.x] = rnd_ct<ST, CT>(yv);
+                            a.alpha_long[clid] = (double)(yv * (s * cvt<CT>(ui[L.x])));
+                            if (a.y_dbg) a.y_dbg[L.x] = (double)sum;
+                        }
                         a.long_cnt[clid] = 0u;
                     }
                 }
@@ -361,10 +382,15 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
                         if (t + 1 == bound) {  // warp-uniform: slice sl complete
                             const int row = a.nbig + 32 * sl + lane;
                             if (row < a.nnonempty) {
-                                const CT yv = s * acc;
-                                y[row] = rnd_ct<ST, CT>(yv);
-                                alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
-                                if (a.y_dbg) a.y_dbg[row] = (double)acc;
+                                if constexpr (LOCAL) {
+                                    a.ypart[row] = (double)acc;
+                                } else {
+                                    if (yp) acc += (CT)__ldcg(yp + row);
+                                    const CT yv = s * acc;
+                                    y[row] = rnd_ct<ST, CT>(yv);
+                                    alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
+                                    if (a.y_dbg) a.y_dbg[row] = (double)acc;
+                                }
                             }
                             acc = CT(0);
                             ++sl;
@@ -375,6 +401,7 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             }
         }
     }
+    if constexpr (LOCAL) return;
     const CT tot = block_sum<CT, kSpmvNT>(alpha_acc, red);
     if (threadIdx.x == 0) a.slots[blockIdx.x] = (double)tot;
     if (arrive_last(a.counter, &sflag)) {
@@ -1626,30 +1653,54 @@ __global__ void __launch_bounds__(kNT) k_restart_copy(RestartArgs a) {
 // host rule of build_part (host_prep.cpp): position p holds original part row
 // perm[p]; entry e of a big row goes to rowptr_deg[p] + e, entry e of SELL slice
 // row i to base + 32 e + i, padding (column 0, value 0); columns through colmap.
-template <typename VT>
+// MODE 0: every entry; MODE 1: the own-slot entries (device column / n_pad == g, the
+// first pass of the two-pass SpMV); MODE 2: the others (the final pass).
+template <int MODE> __device__ __forceinline__ bool pass_keeps(int32_t c, int64_t npad, int g) {
+    if constexpr (MODE == 0) return true;
+    const bool own = (int64_t)c / npad == (int64_t)g;
+    return MODE == 1 ? own : !own;
+}
+
+// big rows: warp per row; the j-th kept entry (input order) goes to dbig[p] + j
+template <typename VT, int MODE>
 __global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const int32_t *scol, const VT *sval,
-                                                    const int32_t *perm, const int64_t *drp, const int32_t *colmap,
-                                                    int nbig, int64_t nphys, int32_t *pcol, VT *pval) {
+                                                    const int32_t *perm, const int64_t *dbig, const int32_t *colmap,
+                                                    int nbig, int64_t nphys, int64_t npad, int g, int32_t *pcol,
+                                                    VT *pval) {
     (void)nphys;
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t p = w; p < nbig; p += nw) {
         const int r = perm[p];
-        const int64_t k0 = srp[r], len = srp[r + 1] - k0, d0 = drp[p];
-        for (int64_t e = lane; e < len; e += 32) {
-            TOPK_DCHECK(d0 + e < nphys && d0 + e < drp[nbig], "big-row scatter destination");
-            pcol[d0 + e] = colmap[scol[k0 + e]];
-            pval[d0 + e] = sval[k0 + e];
+        const int64_t k0 = srp[r], len = srp[r + 1] - k0, d0 = dbig[p];
+        int64_t written = 0;
+        for (int64_t e0 = 0; e0 < len; e0 += 32) {
+            const int64_t e = e0 + lane;
+            int32_t c = 0;
+            bool keep = false;
+            if (e < len) {
+                c = colmap[scol[k0 + e]];
+                keep = pass_keeps<MODE>(c, npad, g);
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int64_t d = d0 + written + __popc(msk & ((1u << lane) - 1u));
+                TOPK_DCHECK(d < nphys && d < dbig[p + 1], "big-row scatter destination");
+                pcol[d] = c;
+                pval[d] = sval[k0 + e];
+            }
+            written += __popc(msk);
         }
     }
 }
 
-template <typename VT>
+// SELL slices: thread per slice row; the j-th kept entry to base + 32 j + i, then padding
+template <typename VT, int MODE>
 __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const int32_t *scol, const VT *sval,
                                                      const int32_t *perm, const int64_t *drp, const int32_t *colmap,
                                                      const longlong2 *sell, int64_t nbig, int64_t nne, int64_t nsl,
-                                                     int64_t nphys, int32_t *pcol, VT *pval) {
+                                                     int64_t nphys, int64_t npad, int g, int32_t *pcol, VT *pval) {
     (void)nphys;
     const int64_t tot = 32 * nsl;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1660,17 +1711,39 @@ __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const i
             len = drp[p + 1] - drp[p];
             k0 = srp[perm[p]];
         }
-        TOPK_DCHECK(len <= S.y && S.x + 32 * S.y <= nphys, "SELL slice bounds");
-        for (int64_t e = 0; e < S.y; ++e) {
-            const int64_t d = S.x + 32 * e + lane;
-            if (e < len) {
-                pcol[d] = colmap[scol[k0 + e]];
-                pval[d] = sval[k0 + e];
-            } else {
-                pcol[d] = 0;
-                pval[d] = VT(0);
-            }
+        TOPK_DCHECK(S.x + 32 * S.y <= nphys, "SELL slice bounds");
+        int64_t j = 0;
+        for (int64_t e = 0; e < len; ++e) {
+            const int32_t c = colmap[scol[k0 + e]];
+            if (!pass_keeps<MODE>(c, npad, g)) continue;
+            TOPK_DCHECK(j < S.y, "SELL row longer than its slice");
+            const int64_t d = S.x + 32 * j + lane;
+            pcol[d] = c;
+            pval[d] = sval[k0 + e];
+            ++j;
         }
+        for (; j < S.y; ++j) {
+            const int64_t d = S.x + 32 * j + lane;
+            pcol[d] = 0;
+            pval[d] = VT(0);
+        }
+    }
+}
+
+// own-slot entries per position (the first pass's degrees), warp per row
+__global__ void __launch_bounds__(256) k_own_count(const int64_t *srp, const int32_t *scol, const int32_t *perm,
+                                                   const int32_t *colmap, int64_t nne, int64_t npad, int g,
+                                                   int32_t *cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = w; p < nne; p += nw) {
+        const int r = perm[p];
+        const int64_t k0 = srp[r], len = srp[r + 1] - k0;
+        int c = 0;
+        for (int64_t e = lane; e < len; e += 32) c += pass_keeps<1>(colmap[scol[k0 + e]], npad, g);
+        c = warp_sum(c);
+        if (lane == 0) cnt[p] = c;
     }
 }
 

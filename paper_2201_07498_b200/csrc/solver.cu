@@ -91,21 +91,34 @@ struct SolveParams {
     void *out_ptr;
 };
 
-struct Part {
-    int g = 0;
-    int64_t row0 = 0, nrows = 0, npad = 0, nnz = 0;
-    int nchunks = 0, nlong = 0, nitems = 0, nbig = 0;
-    int64_t nnonempty = 0, nphys = 0;
-    int32_t *col = nullptr, *perm = nullptr;
-    std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
-    int32_t *inv = nullptr;         // original part-local row -> position
-    std::vector<int64_t> h_sell;    // host copy of the SELL table (export_layout)
-    std::vector<int64_t> h_rowptr;  // host copy (export_layout)
+// One SpMV pass on the device: physical arrays + work tables (host_prep.h).
+struct SpmvDev {
+    int nchunks = 0, nlong = 0, nitems = 0;
+    int64_t nphys = 0;
+    int32_t *col = nullptr;
     void *val = nullptr;
     Chunk *chunks = nullptr;
     LongRow *longrows = nullptr;
     int64_t *sell = nullptr;
     int32_t *items = nullptr;
+    double *long_parts = nullptr, *alpha_long = nullptr;
+    unsigned *long_cnt = nullptr;
+    std::vector<int64_t> h_sell, h_bigptr;  // host copies (export_layout)
+};
+
+struct Part {
+    int g = 0;
+    int64_t row0 = 0, nrows = 0, npad = 0, nnz = 0;
+    int nbig = 0;
+    int64_t nnonempty = 0;
+    int32_t *perm = nullptr;
+    std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
+    int32_t *inv = nullptr;         // original part-local row -> position
+    std::vector<int64_t> h_rowptr;  // host copy (export_layout)
+    SpmvDev sp;                     // the SpMV (final pass when split)
+    SpmvDev own;                    // two-pass SpMV: own-slot columns first
+    double *ypart = nullptr;        // own-slot row sums of the first pass (nullptr: one pass)
+    int32_t *owndeg = nullptr;      // own-slot entries per position (device; export_layout)
     void *yt = nullptr;            // Ritz output in position order, K values per row
     void *Vs = nullptr;            // thick restart scratch: keep columns (reading Q26)
     int *pro_gate = nullptr, *pro_force = nullptr, *pro_count = nullptr;  // reading Q29 (state ints)
@@ -119,8 +132,6 @@ struct Part {
     std::vector<int64_t> send_off;     // G+1 (multi-process)
     int32_t *send_pos = nullptr;       // device: own positions requested by each peer
     void *sendbuf = nullptr;
-    double *long_parts = nullptr, *alpha_long = nullptr;
-    unsigned *long_cnt = nullptr;
     void *V = nullptr, *y = nullptr, *w = nullptr;
     void *out = nullptr;       // internal eigenvector output (K * nrows f64)
     double *v1buf = nullptr;
@@ -168,6 +179,10 @@ struct topk_eig_s {
     void *replica = nullptr;
     bool halo = false;                 // opts.exchange == 1 (reading Q27)
     cudaStream_t body_stream = nullptr; // captures the thick-restart WHILE body (reading Q26)
+    bool split = false;                // two-pass SpMV: own-slot columns first
+    cudaStream_t comm_stream = nullptr; // one process per GPU + split: the vector exchange overlaps
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool join_pending = false;
     const void **d_xsrc = nullptr;     // device: every local part's x_g (halo pull)
     SolveParams *dparams = nullptr, *hparams = nullptr;  // hparams: pageable (a pinned block's free
                                                           // measured up to 380 ms on destroy)
@@ -238,7 +253,9 @@ static void prof_end(topk_eig_s *h, const Part &p) {
 
 // ---------------------------------------------------------------------------
 // exchanges (no-ops in loopback: shared buffers on one stream)
+static void exch_join(topk_eig_s *h);
 static void launch_jacobi(topk_eig_s *h, int check) {
+    exch_join(h);  // beta_{i+1} comes from the exchanged norm partials
     for (Part &p : h->parts) {
         JacArgs a;
         a.st = p.st; a.ex = h->ex; a.G = h->G; a.m = h->m; a.K = h->K; a.max_sweeps = 50;
@@ -314,6 +331,7 @@ static void exch_halo(topk_eig_s *h) {
 }
 
 static void exch_vec_norm(topk_eig_s *h) {
+    exch_join(h);
     if (h->halo) {
         exch_halo(h);
         if (h->comm) NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
@@ -322,25 +340,47 @@ static void exch_vec_norm(topk_eig_s *h) {
     if (!h->comm) return;
     Part &p = h->parts[0];
     size_t vb = (size_t)p.npad * dsize(h->vs);
+    // two-pass SpMV: the vector (and the norm partials) move on the comm stream while the
+    // next SpMV's own-slot pass runs; launch_spmv joins before its final pass
+    cudaStream_t cs = h->stream;
+    if (h->split && h->comm_stream) {
+        CUDA_TRY(cudaEventRecord(h->ev_fork, h->stream));
+        CUDA_TRY(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
+        cs = h->comm_stream;
+    }
     NCCL_TRY(ncclGroupStart());
-    NCCL_TRY(ncclAllGather((char *)h->replica + (size_t)h->rank * vb, h->replica, vb, ncclUint8, h->comm, h->stream));
-    NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
+    NCCL_TRY(ncclAllGather((char *)h->replica + (size_t)h->rank * vb, h->replica, vb, ncclUint8, h->comm, cs));
+    NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, cs));
     NCCL_TRY(ncclGroupEnd());
+    if (cs != h->stream) {
+        CUDA_TRY(cudaEventRecord(h->ev_join, cs));
+        h->join_pending = true;
+    }
+}
+// the main stream waits for an exchange still running on the comm stream
+static void exch_join(topk_eig_s *h) {
+    if (!h->join_pending) return;
+    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+    h->join_pending = false;
 }
 static void exch_norm(topk_eig_s *h) {
+    exch_join(h);  // one NCCL operation of the communicator at a time
     if (!h->comm) return;
     NCCL_TRY(ncclAllGather(h->ex.norm_part + h->rank, h->ex.norm_part, 1, ncclFloat64, h->comm, h->stream));
 }
 static void exch_alpha(topk_eig_s *h) {
+    exch_join(h);  // one NCCL operation of the communicator at a time
     if (!h->comm) return;
     NCCL_TRY(ncclAllGather(h->ex.alpha_part + h->rank, h->ex.alpha_part, 1, ncclFloat64, h->comm, h->stream));
 }
 static void exch_h(topk_eig_s *h) {
+    exch_join(h);  // one NCCL operation of the communicator at a time
     if (!h->comm) return;
     size_t ld = (size_t)h->m + 1;
     NCCL_TRY(ncclAllGather(h->ex.hpart + h->rank * 2 * ld, h->ex.hpart, 2 * ld, ncclFloat64, h->comm, h->stream));
 }
 static void exch_ritz(topk_eig_s *h) {
+    exch_join(h);  // one NCCL operation of the communicator at a time
     if (!h->comm) return;
     NCCL_TRY(ncclAllGather(h->ex.ritz_part + (size_t)h->rank * h->K, h->ex.ritz_part, h->K, ncclFloat64, h->comm, h->stream));
 }
@@ -352,24 +392,40 @@ static void *rep_slot(topk_eig_s *h, Part &p) {
 }
 
 // ---------------------------------------------------------------------------
+static void pass_args(SpmvArgs &a, const SpmvDev &d) {
+    a.col = d.col; a.val = d.val;
+    a.chunks = d.chunks; a.longrows = reinterpret_cast<const int4 *>(d.longrows);
+    a.sell = reinterpret_cast<const longlong2 *>(d.sell); a.items = reinterpret_cast<const int2 *>(d.items);
+    a.nchunks = d.nchunks; a.nitems = d.nitems;
+    a.long_parts = d.long_parts; a.long_cnt = d.long_cnt;
+    a.alpha_long = d.alpha_long; a.nlong = d.nlong;
+}
+
+// a7. Two-pass SpMV (h->split): the own-slot columns first (they do
+// not need the vector exchange), then -- after the exchange, which one process per GPU
+// runs on the comm stream meanwhile -- the other columns plus the epilogue.
 template <typename VT, typename ST, typename CT>
 static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     SpmvArgs a;
-    a.col = p.col; a.val = p.val;
-    a.chunks = p.chunks; a.longrows = reinterpret_cast<const int4 *>(p.longrows);
-    a.sell = reinterpret_cast<const longlong2 *>(p.sell); a.items = reinterpret_cast<const int2 *>(p.items);
-    a.nchunks = p.nchunks; a.nitems = p.nitems; a.nbig = p.nbig; a.nnonempty = (int)p.nnonempty;
-    a.long_parts = p.long_parts; a.long_cnt = p.long_cnt;
-    a.alpha_long = p.alpha_long; a.nlong = p.nlong;
+    a.nbig = p.nbig; a.nnonempty = (int)p.nnonempty;
     const void *ucol = (const char *)p.V + (size_t)(it - 1) * p.npad * sizeof(ST);
     a.x = (h->G == 1) ? ucol : (h->halo ? p.xg : h->replica);
     a.xlen = (h->G == 1) ? p.npad : (h->halo ? p.npad + p.nhalo : (int64_t)h->G * p.npad);
     a.ui = ucol;
     a.y = p.y; a.y_dbg = y_dbg;
+    a.ypart = p.ypart;
     a.slots = p.slots; a.counter = p.counters + 1;
     a.st = p.st; a.ex = h->ex; a.G = h->G; a.g = p.g;
     prof_begin(h, p, 1);
-    k_spmv<VT, ST, CT><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
+    if (p.ypart) {
+        pass_args(a, p.own);
+        k_spmv<VT, ST, CT, true><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
+        CUDA_TRY(cudaGetLastError());
+        h->launches++;
+        exch_join(h);  // the remote columns need the exchanged vector
+    }
+    pass_args(a, p.sp);
+    k_spmv<VT, ST, CT, false><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
     CUDA_TRY(cudaGetLastError());
     prof_end(h, p);
     h->launches++;
@@ -480,6 +536,7 @@ static void launch_correct(topk_eig_s *h, Part &p, int it, int in_col, const int
 // thick restart (reading Q26): Jacobi on the cycle's T (convergence test + the
 // kept pairs), projection of the kept Ritz vectors, norm exchange, basis rewrite
 static void exch_rst(topk_eig_s *h) {
+    exch_join(h);  // one NCCL operation of the communicator at a time
     if (!h->comm) return;
     NCCL_TRY(ncclAllGather(h->ex.rst_part + (size_t)h->rank * h->keep, h->ex.rst_part, h->keep, ncclFloat64,
                            h->comm, h->stream));
@@ -675,6 +732,7 @@ static void enqueue_solve(topk_eig_s *h, bool want_vectors) {
         CUDA_TRY(cudaStreamEndCapture(h->body_stream, &body_out));
     }
     // a12-a13: Jacobi (redundant on every part, identical inputs)
+    exch_join(h);
     record_event(h, h->evL);
     launch_jacobi(h, 0);
     record_event(h, h->evJ);
@@ -729,8 +787,9 @@ static void set_kernels(topk_eig_s *h) {
     h->spmv_only = &spmv_only<VT, ST, CT>;
     int occ = 0;
     // the SpMV uses no dynamic shared memory: the whole unified L1 caches x
-    CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT>, kSpmvNT, 0);
+    CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT, false>, kSpmvNT, 0);
     h->grid_spmv = h->nsm * std::max(1, occ);
     int occ2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
@@ -884,6 +943,59 @@ static void free_dev_csr(DevCsr &d) {
     pool_dev_free(d.sval);
     d = DevCsr{};
 }
+// Device arrays and work tables of one SpMV pass (tables uploaded here).
+static void alloc_pass(topk_eig_s *h, SpmvDev &d, const std::vector<Chunk> &chunks, const std::vector<LongRow> &longrows,
+                       const std::vector<int64_t> &sell, const std::vector<int32_t> &items, const std::vector<int64_t> &bigptr,
+                       int64_t nphys, size_t val_es) {
+    d.nchunks = (int)chunks.size();
+    d.nlong = (int)longrows.size();
+    d.nitems = (int)items.size() / 2;
+    d.nphys = nphys;
+    d.col = h->alloc<int32_t>((size_t)nphys + 128);  // physical col/val padded by 128 entries
+    d.val = h->alloc<char>(((size_t)nphys + 128) * val_es);
+    d.chunks = h->alloc<Chunk>(chunks.size());
+    d.longrows = h->alloc<LongRow>(longrows.size());
+    d.sell = h->alloc<int64_t>(sell.size());
+    d.items = h->alloc<int32_t>(items.size());
+    d.long_parts = h->alloc<double>(chunks.size());
+    d.long_cnt = h->alloc<unsigned>(longrows.size());
+    d.alpha_long = h->alloc<double>(longrows.size());
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (!chunks.empty()) CUDA_TRY(scopy(h->stream, d.chunks, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+    if (!longrows.empty()) CUDA_TRY(scopy(h->stream, d.longrows, longrows.data(), longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
+    if (!sell.empty()) CUDA_TRY(scopy(h->stream, d.sell, sell.data(), sell.size() * 8, cudaMemcpyHostToDevice));
+    if (!items.empty()) CUDA_TRY(scopy(h->stream, d.items, items.data(), items.size() * 4, cudaMemcpyHostToDevice));
+    d.h_sell = sell;
+    d.h_bigptr = bigptr;
+}
+
+template <typename VT, int MODE>
+static void scatter_pass(topk_eig_s *h, Part &p, const PartLayout &L, const DevCsr &d, const int32_t *d_colmap,
+                         const int64_t *d_drp, SpmvDev &dp) {
+    const VT *sval = static_cast<const VT *>(d.sval);
+    if (L.nbig > 0) {
+        int64_t *d_big = static_cast<int64_t *>(dalloc_or_throw(dp.h_bigptr.size() * 8));
+        CUDA_TRY(scopy(h->stream, d_big, dp.h_bigptr.data(), dp.h_bigptr.size() * 8, cudaMemcpyHostToDevice));
+        k_layout_big<VT, MODE><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_big, d_colmap, L.nbig,
+                                                                 dp.nphys, p.npad, p.g, dp.col, reinterpret_cast<VT *>(dp.val));
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        pool_dev_free(d_big);
+    }
+    const int64_t nsl = (int64_t)dp.h_sell.size() / 2;
+    if (nsl > 0) {
+        k_layout_sell<VT, MODE><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap,
+                                                                  reinterpret_cast<const longlong2 *>(dp.sell), (int64_t)L.nbig,
+                                                                  L.nnonempty, nsl, dp.nphys, p.npad, p.g, dp.col,
+                                                                  reinterpret_cast<VT *>(dp.val));
+        CUDA_TRY(cudaGetLastError());
+    }
+}
+
+// a4, second half: the SpMV passes of part p from its uploaded CSR slice with the rule of
+// build_part. Two-pass SpMV (h->split): the own-slot entries per position are counted on
+// the device, both passes' tables built on the host (build_pass_tables), and the entries
+// scattered into the own-slot pass and the final pass.
 template <typename VT>
 static void device_layout_t(topk_eig_s *h, Part &p, const PartLayout &L, const DevCsr &d, const int32_t *d_colmap) {
     const int64_t ng = L.nrows;
@@ -891,18 +1003,28 @@ static void device_layout_t(topk_eig_s *h, Part &p, const PartLayout &L, const D
     const char *drp = reinterpret_cast<const char *>(L.rowptr.data());
     CUDA_TRY(staged_h2d(d_drp, (size_t)(ng + 1) * 8, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, drp + off, nb); },
                         h->stream));
-    const VT *sval = static_cast<const VT *>(d.sval);
-    if (L.nbig > 0) {
-        k_layout_big<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap, L.nbig,
-                                                           L.nphys, p.col, reinterpret_cast<VT *>(p.val));
-        CUDA_TRY(cudaGetLastError());
-    }
-    const int64_t nsl = (int64_t)L.sell.size() / 2;
-    if (nsl > 0) {
-        k_layout_sell<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, d_colmap,
-                                                            reinterpret_cast<const longlong2 *>(p.sell), (int64_t)L.nbig,
-                                                            L.nnonempty, nsl, L.nphys, p.col, reinterpret_cast<VT *>(p.val));
-        CUDA_TRY(cudaGetLastError());
+    if (!h->split) {
+        const std::vector<int64_t> bigptr(L.rowptr.begin(), L.rowptr.begin() + L.nbig + 1);
+        alloc_pass(h, p.sp, L.chunks, L.longrows, L.sell, L.items, bigptr, L.nphys, sizeof(VT));
+        scatter_pass<VT, 0>(h, p, L, d, d_colmap, d_drp, p.sp);
+    } else {
+        const int64_t nne = L.nnonempty;
+        p.owndeg = h->alloc<int32_t>((size_t)std::max<int64_t>(nne, 1));
+        if (nne > 0) {
+            k_own_count<<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, p.perm, d_colmap, nne, p.npad, p.g, p.owndeg);
+            CUDA_TRY(cudaGetLastError());
+        }
+        std::vector<int32_t> od((size_t)std::max<int64_t>(ng, 1), 0), rd((size_t)std::max<int64_t>(ng, 1), 0);
+        if (nne > 0) CUDA_TRY(scopy(h->stream, od.data(), p.owndeg, (size_t)nne * 4, cudaMemcpyDeviceToHost));
+        for (int64_t q = 0; q < ng; ++q) rd[(size_t)q] = (int32_t)(L.rowptr[(size_t)q + 1] - L.rowptr[(size_t)q]) - od[(size_t)q];
+        PassTables To, Tr;
+        build_pass_tables(od.data(), L.nbig, nne, false, To);
+        build_pass_tables(rd.data(), L.nbig, nne, true, Tr);
+        alloc_pass(h, p.own, To.chunks, To.longrows, To.sell, To.items, To.bigptr, To.nphys, sizeof(VT));
+        alloc_pass(h, p.sp, Tr.chunks, Tr.longrows, Tr.sell, Tr.items, Tr.bigptr, Tr.nphys, sizeof(VT));
+        p.ypart = h->alloc<double>((size_t)std::max<int64_t>(p.npad, 1));  // rows without own entries stay 0
+        scatter_pass<VT, 1>(h, p, L, d, d_colmap, d_drp, p.own);
+        scatter_pass<VT, 2>(h, p, L, d, d_colmap, d_drp, p.sp);
     }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     pool_dev_free(d_drp);
@@ -1035,6 +1157,10 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         for (int i = K; i < m; ++i) h->conv_checks += (i % h->conv_check == 0);
     if (o.exchange < 0 || o.exchange > 1) return fail(TOPK_E_INVALID, "exchange must be 0 (allgather) or 1 (halo)");
     h->halo = (G > 1 && o.exchange == 1);
+    if (o.overlap < -1 || o.overlap > 1) return fail(TOPK_E_INVALID, "overlap must be -1, 0 or 1");
+    // two-pass SpMV, own-slot columns first: by default with one process
+    // per GPU (the vector exchange then overlaps the first pass); overlap = 1 also in one process
+    h->split = G > 1 && !h->halo && (o.overlap == 1 || (o.overlap == 0 && world > 1));
     if (o.jacobi_path < 0 || o.jacobi_path > 2) return fail(TOPK_E_INVALID, "jacobi_path must be 0, 1 or 2");
     if (o.jacobi_cluster != 0 && o.jacobi_cluster != 8 && o.jacobi_cluster != 16)
         return fail(TOPK_E_INVALID, "jacobi_cluster must be 0, 8 or 16");
@@ -1080,6 +1206,11 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         CUDA_TRY(cudaEventCreate(&h->ev0));
         CUDA_TRY(cudaEventCreate(&h->ev1));
         CUDA_TRY(cudaEventCreate(&h->evL));
+        if (h->split && world > 1) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        }
         CUDA_TRY(cudaEventCreate(&h->evJ));
         clk.mark("device init");
         // a4, first half, in the background: the local parts' CSR slices go up on a
@@ -1230,24 +1361,11 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             if (s != TOPK_OK) return fail(s, err);
             clk.mark("layout tables");
             p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.rowptr.back();
-            p.nchunks = (int)L.chunks.size(); p.nlong = (int)L.longrows.size();
-            p.nitems = (int)L.items.size() / 2; p.nbig = L.nbig; p.nnonempty = L.nnonempty;
-            p.nphys = L.nphys;
-            // physical col/val padded by 128 entries
-            p.col = h->alloc<int32_t>((size_t)L.nphys + 128);
-            p.val = h->alloc<char>(((size_t)L.nphys + 128) * dsize(ms));
+            p.nbig = L.nbig; p.nnonempty = L.nnonempty;
             p.h_rowptr = L.rowptr;
             p.h_perm = L.perm;
-            p.h_sell = L.sell;
             p.perm = h->alloc<int32_t>(L.perm.size());
             p.inv = h->alloc<int32_t>(L.perm.size());
-            p.chunks = h->alloc<Chunk>(L.chunks.size());
-            p.longrows = h->alloc<LongRow>(L.longrows.size());
-            p.sell = h->alloc<int64_t>(L.sell.size());
-            p.items = h->alloc<int32_t>(L.items.size());
-            p.long_parts = h->alloc<double>(L.chunks.size());
-            p.long_cnt = h->alloc<unsigned>(L.longrows.size());
-            p.alpha_long = h->alloc<double>(L.longrows.size());
             CUDA_TRY(cudaStreamSynchronize(h->stream));
             if (!L.perm.empty()) {
                 hvec<int32_t> inv(L.perm.size());
@@ -1256,10 +1374,6 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 CUDA_TRY(scopy(h->stream, p.perm, L.perm.data(), L.perm.size() * 4, cudaMemcpyHostToDevice));
                 CUDA_TRY(scopy(h->stream, p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
             }
-            if (!L.chunks.empty()) CUDA_TRY(scopy(h->stream, p.chunks, L.chunks.data(), L.chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
-            if (!L.longrows.empty()) CUDA_TRY(scopy(h->stream, p.longrows, L.longrows.data(), L.longrows.size() * sizeof(LongRow), cudaMemcpyHostToDevice));
-            if (!L.sell.empty()) CUDA_TRY(scopy(h->stream, p.sell, L.sell.data(), L.sell.size() * 8, cudaMemcpyHostToDevice));
-            if (!L.items.empty()) CUDA_TRY(scopy(h->stream, p.items, L.items.data(), L.items.size() * 4, cudaMemcpyHostToDevice));
             if (h->halo) setup_halo(h.get(), p, csr, npad, pos.data(), d_colmap);
             if (uploader.joinable()) {
                 uploader.join();
@@ -1326,6 +1440,9 @@ topk_eig_s::~topk_eig_s() {
     clk.mark("destroy: events");
     if (stream) cudaStreamDestroy(stream);
     if (body_stream) cudaStreamDestroy(body_stream);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     clk.mark("destroy: stream");
 }
 
@@ -1650,6 +1767,26 @@ topk_status_t topk_eig_export_partition(topk_eig_t h, int64_t *boundaries) {
     return TOPK_OK;
 }
 
+// one pass's physical arrays back on the host (device column entries, values as double)
+static void download_pass(topk_eig_s *h, const SpmvDev &d, std::vector<int32_t> &c, std::vector<double> &v) {
+    const size_t zp = (size_t)d.nphys;
+    c.assign(zp, 0);
+    v.assign(zp, 0.0);
+    if (!zp) return;
+    CUDA_TRY(scopy(h->stream, c.data(), d.col, zp * 4, cudaMemcpyDeviceToHost));
+    if (h->ms == TOPK_F64) {
+        CUDA_TRY(scopy(h->stream, v.data(), d.val, zp * 8, cudaMemcpyDeviceToHost));
+    } else if (h->ms == TOPK_F32) {
+        std::vector<float> f(zp);
+        CUDA_TRY(scopy(h->stream, f.data(), d.val, zp * 4, cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < zp; ++k) v[k] = f[k];
+    } else {
+        std::vector<uint16_t> f(zp);
+        CUDA_TRY(scopy(h->stream, f.data(), d.val, zp * 2, cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < zp; ++k) v[k] = bf16_bits_to_double(f[k]);
+    }
+}
+
 topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr, int32_t *col, double *val,
                                      int64_t *n_pad, int64_t *n_rows, int64_t *nnz) {
     GUARD(h);
@@ -1661,53 +1798,56 @@ topk_status_t topk_eig_export_layout(topk_eig_t h, int32_t part, int64_t *rowptr
     try {
         if (rowptr)
             for (size_t i = 0; i < p.h_rowptr.size(); ++i) rowptr[i] = p.h_rowptr[i];
-        if (col || val) {
-            // logical entry k of position row q -> physical index (big-row CSR prefix or SELL slot)
-            std::vector<int64_t> phys((size_t)p.nnz);
-            for (int64_t q = 0; q < p.nrows; ++q) {
-                const int64_t rb = p.h_rowptr[(size_t)q], re = p.h_rowptr[(size_t)q + 1];
-                for (int64_t k = rb; k < re; ++k) {
-                    if (q < p.nbig) { phys[(size_t)k] = k; continue; }
-                    const int64_t sl = (q - p.nbig) / 32, i = (q - p.nbig) % 32;
-                    phys[(size_t)k] = p.h_sell[(size_t)(2 * sl)] + 32 * (k - rb) + i;
-                }
+        if (!col && !val) return TOPK_OK;
+        const bool split = p.ypart != nullptr;
+        std::vector<int32_t> mc, oc;
+        std::vector<double> mv, ov;
+        download_pass(h, p.sp, mc, mv);
+        std::vector<int32_t> odeg((size_t)std::max<int64_t>(p.nrows, 1), 0);
+        if (split) {
+            download_pass(h, p.own, oc, ov);
+            if (p.nnonempty) CUDA_TRY(scopy(h->stream, odeg.data(), p.owndeg, (size_t)p.nnonempty * 4, cudaMemcpyDeviceToHost));
+        }
+        std::vector<int32_t> hq;
+        if (h->halo) {  // compact entries back to the logical q * n_pad + position (reading Q27)
+            hq.resize((size_t)p.nhalo);
+            for (int q2 = 0; q2 < h->G; ++q2)
+                for (int64_t t2 = p.halo_off[(size_t)q2]; t2 < p.halo_off[(size_t)q2 + 1]; ++t2) hq[(size_t)t2] = q2;
+        }
+        auto logical_col = [&](int32_t c) -> int32_t {
+            if (!h->halo) return c;
+            if (c < p.npad) return (int32_t)(p.g * p.npad + c);
+            const int64_t e = c - p.npad;
+            return (int32_t)(hq[(size_t)e] * p.npad + p.halo_pos_h[(size_t)e]);
+        };
+        auto slot_of = [&](const SpmvDev &d, int64_t q, int64_t e) -> size_t {
+            if (q < p.nbig) return (size_t)(d.h_bigptr[(size_t)q] + e);
+            const int64_t sl = (q - p.nbig) / 32, i = (q - p.nbig) % 32;
+            return (size_t)(d.h_sell[(size_t)(2 * sl)] + 32 * e + i);
+        };
+        // a row's entries are in canonical (ascending original column) order; with the
+        // split, original columns owned by parts q < g precede the own part's, which precede
+        // q > g, so the row is [final-pass entries with owner < g | own-slot pass | the rest]
+        for (int64_t q = 0; q < p.nrows; ++q) {
+            const int64_t rb = p.h_rowptr[(size_t)q], d = p.h_rowptr[(size_t)q + 1] - rb;
+            const int64_t no = split ? odeg[(size_t)q] : 0, nm = d - no;
+            int64_t im = 0, k = rb;
+            auto put = [&](int32_t c, double v) {
+                if (col) col[k] = c;
+                if (val) val[k] = v;
+                ++k;
+            };
+            while (split && im < nm && mc[slot_of(p.sp, q, im)] / p.npad < p.g) {
+                const size_t sidx = slot_of(p.sp, q, im++);
+                put(mc[sidx], mv[sidx]);
             }
-            const size_t zp = (size_t)p.nphys;
-            if (col) {
-                std::vector<int32_t> t(zp);
-                if (zp) CUDA_TRY(scopy(h->stream, t.data(), p.col, zp * 4, cudaMemcpyDeviceToHost));
-                std::vector<int32_t> hq;
-                if (h->halo) {  // compact entries back to the logical q * n_pad + position (reading Q27)
-                    hq.resize((size_t)p.nhalo);
-                    for (int q2 = 0; q2 < h->G; ++q2)
-                        for (int64_t t2 = p.halo_off[(size_t)q2]; t2 < p.halo_off[(size_t)q2 + 1]; ++t2) hq[(size_t)t2] = q2;
-                }
-                for (size_t k = 0; k < phys.size(); ++k) {
-                    int32_t c = t[(size_t)phys[k]];
-                    if (h->halo) {
-                        if (c < p.npad) c = (int32_t)(p.g * p.npad + c);
-                        else {
-                            const int64_t e = c - p.npad;
-                            c = (int32_t)(hq[(size_t)e] * p.npad + p.halo_pos_h[(size_t)e]);
-                        }
-                    }
-                    col[k] = c;
-                }
+            for (int64_t io = 0; io < no; ++io) {
+                const size_t sidx = slot_of(p.own, q, io);
+                put(oc[sidx], ov[sidx]);
             }
-            if (val) {
-                std::vector<double> t(zp);
-                if (h->ms == TOPK_F64) {
-                    if (zp) CUDA_TRY(scopy(h->stream, t.data(), p.val, zp * 8, cudaMemcpyDeviceToHost));
-                } else if (h->ms == TOPK_F32) {
-                    std::vector<float> f(zp);
-                    if (zp) CUDA_TRY(scopy(h->stream, f.data(), p.val, zp * 4, cudaMemcpyDeviceToHost));
-                    for (size_t k = 0; k < zp; ++k) t[k] = f[k];
-                } else {
-                    std::vector<uint16_t> f(zp);
-                    if (zp) CUDA_TRY(scopy(h->stream, f.data(), p.val, zp * 2, cudaMemcpyDeviceToHost));
-                    for (size_t k = 0; k < zp; ++k) t[k] = bf16_bits_to_double(f[k]);
-                }
-                for (size_t k = 0; k < phys.size(); ++k) val[k] = t[(size_t)phys[k]];
+            while (im < nm) {
+                const size_t sidx = slot_of(p.sp, q, im++);
+                put(logical_col(mc[sidx]), mv[sidx]);
             }
         }
     }

@@ -462,3 +462,51 @@ def test_info_phase_times(T, c3s):
     assert i["ms_lanczos"] > 0 and i["ms_jacobi"] > 0 and i["ms_ritz"] > 0
     assert abs(i["ms_lanczos"] + i["ms_jacobi"] + i["ms_ritz"] - i["ms_solve"]) <= 0.02 * i["ms_solve"] + 0.01
     assert i["bytes_nvlink"] == 0
+
+
+# ------------------------------------------------------------------ two-pass SpMV (overlapped exchange)
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_two_pass_spmv_overlap(T, c3s, G):
+    """The SpMV as two passes, own-slot columns first (what one
+    process per GPU runs so the vector allgather overlaps the first pass), on G loopback
+    parts (overlap = 1: the same kernels and sums as the multi-process run): every SpMV row
+    within the rigorous fp64 bound, the layout export (both passes merged back into
+    canonical order) bit-exact against the oracle, the DDD solve within 1e-12 of the one-pass
+    solve and within the parity tolerance of the oracle, bitwise repeatable."""
+    x = np.random.default_rng(13).standard_normal(c3s.n)
+    with T.TopkEig(c3s, 8, "f64", "f64", m=24, parts=G, overlap=1) as h:
+        y = h.debug_spmv(x)
+        r = h.solve(seed=5)
+        r2 = h.solve(seed=5)
+        b = h.partition()
+        for g in range(G):
+            rp, col, val, npad = h.layout(g)
+            orp, ocol, oval, onpad = O.layout(c3s.rowptr, c3s.col, c3s.val, G, b, g, "f64")
+            assert npad == onpad and np.array_equal(rp, orp)
+            assert np.array_equal(col, ocol) and np.array_equal(val.view(np.uint64), oval.view(np.uint64))
+    yr = O.spmv(c3s.rowptr, c3s.col, c3s.val, x)
+    bound = (np.diff(c3s.rowptr) + 2) * 2.0 ** -53 * O.spmv(c3s.rowptr, c3s.col, np.abs(c3s.val), np.abs(x))
+    assert np.all(np.abs(y - yr) <= bound + 1e-300)
+    assert np.array_equal(r.eigenvalues, r2.eigenvalues) and np.array_equal(r.eigenvectors, r2.eigenvectors)
+    with T.TopkEig(c3s, 8, "f64", "f64", m=24, parts=G, overlap=-1) as h:
+        r0 = h.solve(seed=5)
+    assert np.abs(r.eigenvalues - r0.eigenvalues).max() <= 1e-12 * abs(r0.eigenvalues[0])
+    ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=8, m=24, seed=5)
+    check_solve(r, ref, 1e-8)
+
+
+def test_two_pass_spmv_fdf_row_boundaries(T):
+    """Two-pass SpMV on rows at the chunk / SELL boundaries (stars), FDF, G = 3 loopback:
+    rows whose entries are all own-slot or all remote, empty rows, ragged tail."""
+    A = S.stars([8191, 8192, 8193, 16385], dense=[127, 128, 129, 3])
+    x = np.random.default_rng(2).standard_normal(A.n)
+    with T.TopkEig(A, 8, "f32", "f64", m=24, parts=3, overlap=1) as h:
+        y = h.debug_spmv(x)
+        r = h.solve(seed=2)
+    xr = x.astype(np.float32).astype(np.float64)
+    av = A.val.astype(np.float32).astype(np.float64)
+    yr = O.spmv(A.rowptr, A.col, av, xr)
+    bound = (np.diff(A.rowptr) + 2) * 2.0 ** -53 * O.spmv(A.rowptr, A.col, np.abs(av), np.abs(xr))
+    assert np.all(np.abs(y - yr) <= bound + 1e-300)
+    ref = O.solve(A.rowptr, A.col, A.val, K=8, m=24, seed=2)
+    check_solve(r, ref, 1e-4)
