@@ -432,6 +432,14 @@ def main():
                 "gpu_launches": int(info["gpu_launches"]) * args.steps,
                 "gpu_launches_per_step": int(info["gpu_launches"]),
                 "clocks": clocks,
+                "interconnect": None if N == 1 else {
+                    "exchange": args.exchange, "overlap": "allgather on a second stream during the own-slot SpMV pass"
+                    if args.exchange == "allgather" else "none (halo send/recv before the SpMV)",
+                    "bytes_received_per_rank_per_solve": int(info["bytes_nvlink"]),
+                    "bytes_per_iteration": int(info["bytes_nvlink"]) // max(1, m),
+                    "gbs_if_spread_over_lanczos_phase": round(info["bytes_nvlink"] / max(info["ms_lanczos"], 1e-9) / 1e6, 1),
+                    "nvlink5_gbs_per_direction": 900,
+                    "note": "modelled bytes (topk_eig_info_t.bytes_nvlink); the exchange is not timed separately"},
                 "solve_info": {k: info[k] for k in ("k_found", "iterations", "breakdown", "jacobi_sweeps",
                                                     "jacobi_converged")},
                 "paper_context": "paper (V100, fp32): 67x vs 104-thread ARPACK, 1.9x vs Alveo U280 FPGA "
