@@ -85,7 +85,13 @@ typedef struct {
     int32_t num_parts;       /* G row partitions. Single process: G virtual ranks on
                                 one device ("loopback"). Multi-process: must equal world. 0 -> 1     */
     int32_t device;          /* CUDA device ordinal of this process/handle                         */
-    int32_t check_symmetry;  /* 0 default -> check; -1 skip (caller guarantees M = M^T)            */
+    int32_t check_symmetry;  /* 0 default -> check; -1 skip (caller guarantees M = M^T). The check
+                                compares the multiset of upper-triangle entries (position, value
+                                bits) with the transposed lower ones through two 64-bit hash sums:
+                                M = M^T always passes; an asymmetric M is rejected unless both sums
+                                collide (~2^-128 for random-function hashes), i.e. the check is
+                                probabilistic. One process per GPU: each rank hashes its own rows
+                                and the sums are all-reduced (every rank returns the same status) */
     int32_t values_storage;  /* device dtype of matrix values; -1/0 default -> same as storage      */
     int32_t use_graph;       /* 0 default -> capture the solve as one CUDA graph; -1 -> eager launches */
     double breakdown_tol;    /* tau of reading Q7; 0 -> 1e-12 (f64), 1e-6 (f32), 1e-3 (bf16) storage */
