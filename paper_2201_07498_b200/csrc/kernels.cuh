@@ -33,7 +33,10 @@ constexpr int kSpmvNT = 256;  // SpMV CTA size (occupancy-limited grid, no share
 #endif
 constexpr int kRitzKB = TOPK_RITZ_KB;  // Ritz outputs per thread (dev knob, tools/build.py build_variant)
 constexpr int kStepJB = 16;  // basis columns per multi-dot pass of k_step (reorth-off path)
-constexpr int kStepMaxNC = 17;  // widest exact-width multi-dot pass (k_stepw)
+#ifndef TOPK_STEP_MAXNC
+#define TOPK_STEP_MAXNC 17
+#endif
+constexpr int kStepMaxNC = TOPK_STEP_MAXNC;  // widest exact-width multi-dot pass (k_stepw; dev build variant)
 #ifndef TOPK_CORR_MAXNC
 #define TOPK_CORR_MAXNC 17  // 24 measured the same on C3 (tools/lab/spmv_variants.py)
 #endif

@@ -7,7 +7,7 @@ import synthgen as S, paper_2201_07498_b200 as T
 A = S.config_matrix("C3")
 for rep in range(5):
     t0 = time.perf_counter()
-    h = T.TopkEig(A, 24, "f32", "f64", check_symmetry=False)
+    h = T.TopkEig(A, 24, "f32", "f64")  # default options (symmetry check on)
     t1 = time.perf_counter()
     r = h.solve(seed=1, vectors=True, vec_dtype="f32")
     t2 = time.perf_counter()
