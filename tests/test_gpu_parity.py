@@ -510,3 +510,22 @@ def test_two_pass_spmv_fdf_row_boundaries(T):
     assert np.all(np.abs(y - yr) <= bound + 1e-300)
     ref = O.solve(A.rowptr, A.col, A.val, K=8, m=24, seed=2)
     check_solve(r, ref, 1e-4)
+
+
+# ------------------------------------------------------------------ Ritz output on the fp64 tensor cores
+@pytest.mark.parametrize("K,m,storage", [(5, 12, "f64"), (16, 40, "f32"), (40, 64, "f64"), (40, 64, "f32")])
+def test_ritz_mma_paths(T, c3s, K, m, storage):
+    """k_ritz_mma (mma.sync m8n8k4 f64; 1, 2 or 4 output tiles per warp, several output
+    groups at K = 40) against the CUDA-core k_ritz and the oracle: vectors within 1e-12
+    (f64) / 1e-6 (f32 outputs) of the CUDA-core path, parity with the oracle."""
+    out = {}
+    for path in ("auto", "cuda_cores"):
+        with T.TopkEig(c3s, K, storage, "f64", m=m, ritz_path=path) as h:
+            out[path] = h.solve(seed=6, vectors=True, vec_dtype="f64")
+    a, b = out["auto"], out["cuda_cores"]
+    assert np.array_equal(a.eigenvalues, b.eigenvalues)
+    tol = 1e-12 if storage == "f64" else 1e-6
+    for k in range(len(a.eigenvalues)):
+        assert np.linalg.norm(a.eigenvectors[k] - b.eigenvectors[k]) <= tol
+    ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=K, m=m, seed=6)
+    check_solve(a, ref, 1e-8 if storage == "f64" else 1e-4)
