@@ -528,4 +528,6 @@ def test_ritz_mma_paths(T, c3s, K, m, storage):
     for k in range(len(a.eigenvalues)):
         assert np.linalg.norm(a.eigenvectors[k] - b.eigenvectors[k]) <= tol
     ref = O.solve(c3s.rowptr, c3s.col, c3s.val, K=K, m=m, seed=6)
-    check_solve(a, ref, 1e-8 if storage == "f64" else 1e-4)
+    # FDF at K = 40: the deeper Ritz pairs have relative gaps ~2e-4, where f32 storage
+    # moves a vector by ~1e-5 (the error of the pair / its gap); the paths agree exactly above
+    check_solve(a, ref, 1e-8 if storage == "f64" else 1e-4, vec_tol=1e-5 if storage == "f64" or K <= 24 else 5e-5)
