@@ -146,8 +146,9 @@ typedef struct {
      * exchange = 0 the SpMV runs as two passes, the own-slot columns first (they need nothing
      * from the peers), then the other columns and the epilogue; one process per GPU runs the
      * allgather of v_i on a second stream during the first pass. 0 -> on with one process per
-     * GPU, off in one process; 1 -> on (also in one process: same kernels and sums as the
-     * multi-process run); -1 -> off (one pass after the exchange). */
+     * GPU when a rank receives >= 64 MB per exchange ((G-1) n_pad storage bytes: the second
+     * pass costs ~30-45 us per SpMV), off in one process; 1 -> on (also in one process: same
+     * kernels and sums as the multi-process run); -1 -> off (one pass after the exchange). */
     int32_t overlap;
 } topk_eig_opts_t;
 

@@ -1158,9 +1158,12 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (o.exchange < 0 || o.exchange > 1) return fail(TOPK_E_INVALID, "exchange must be 0 (allgather) or 1 (halo)");
     h->halo = (G > 1 && o.exchange == 1);
     if (o.overlap < -1 || o.overlap > 1) return fail(TOPK_E_INVALID, "overlap must be -1, 0 or 1");
-    // two-pass SpMV, own-slot columns first: by default with one process
-    // per GPU (the vector exchange then overlaps the first pass); overlap = 1 also in one process
-    h->split = G > 1 && !h->halo && (o.overlap == 1 || (o.overlap == 0 && world > 1));
+    // two-pass SpMV, own-slot columns first: overlap = 1 always (also in
+    // one process); by default (0) with one process per GPU when the vector exchange is large
+    // enough to pay for the second pass (measured at G = 8: +31 us per SpMV at C3, whose
+    // exchange is ~15 MB; +45 us at C4, ~350 MB; profiles/r02_overlap_cost.jsonl), decided
+    // below once n_pad is known
+    h->split = G > 1 && !h->halo && o.overlap == 1;
     if (o.jacobi_path < 0 || o.jacobi_path > 2) return fail(TOPK_E_INVALID, "jacobi_path must be 0, 1 or 2");
     if (o.jacobi_cluster != 0 && o.jacobi_cluster != 8 && o.jacobi_cluster != 16)
         return fail(TOPK_E_INVALID, "jacobi_cluster must be 0, 8 or 16");
@@ -1188,6 +1191,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
     if (s != TOPK_OK) return fail(s, "partition failed");
     const int64_t npad = padded_rows(h->bounds.data(), G);
     clk.mark("partition");
+    if (G > 1 && !h->halo && o.overlap == 0 && world > 1)  // >= 64 MB received per exchange
+        h->split = (int64_t)(G - 1) * npad * (int64_t)dsize(storage) >= ((int64_t)64 << 20);
 
     // device
     int ndev = 0;
