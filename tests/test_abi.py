@@ -178,15 +178,18 @@ def test_physical_format_unpacks_to_logical(G):
 
 
 
-@pytest.mark.skipif(has_gpu(), reason="uses the no-device status to see that the symmetry check passed")
+def _sym_ok(T, A):
+    h = T.plan_symmetry(A, 0, A.n)  # the hash sums create uses (host-only, runs everywhere)
+    return bool(h[0] == h[2] and h[1] == h[3])
+
+
 def test_symmetry_check_hash_multiset():
     """Row a2 (reading Q17): the multiset-hash symmetry check accepts a symmetric
-    R-MAT and rejects one-bit, one-entry and swapped-value perturbations of it."""
+    R-MAT and rejects one-bit, one-entry and swapped-value perturbations of it, and
+    agrees with the oracle's exact check (O1, a search per entry) on every case."""
     import paper_2201_07498_b200 as T
     A = S.rmat(13, 60_000, 7)
-    with pytest.raises(T.TopkError) as e:
-        T.TopkEig(A, 4, "f64", "f64")
-    assert e.value.status == 8  # symmetric: passes the check, then no device
+    assert _sym_ok(T, A) and O.is_symmetric(A.n, A.rowptr, A.col, A.val)
 
     def variant(kind):
         rp, col, val = A.rowptr.copy(), A.col.copy(), A.val.copy()
@@ -205,6 +208,71 @@ def test_symmetry_check_hash_multiset():
         return S.CSR(A.n, rp, col, val)
 
     for kind in ("bit", "swap", "drop"):
-        with pytest.raises(T.TopkError) as e:
-            T.TopkEig(variant(kind), 4, "f64", "f64")
-        assert e.value.status == 3, kind
+        V = variant(kind)
+        assert not _sym_ok(T, V), kind
+        assert not O.is_symmetric(V.n, V.rowptr, V.col, V.val), kind
+    if not has_gpu():  # the same check inside create: rejected before any device work
+        for kind in ("bit", "swap", "drop"):
+            with pytest.raises(T.TopkError) as e:
+                T.TopkEig(variant(kind), 4, "f64", "f64")
+            assert e.value.status == 3, kind
+
+
+def test_symmetry_check_adversarial_vs_exact_oracle():
+    """Adversarial inputs for a multiset hash (reading Q17), each compared with the
+    oracle's exact check: value swaps between the two triangles that keep every
+    multiset statistic but one pairing, entries moved to the mirror position of
+    another entry, sign flips, stored +0.0 vs -0.0 (bitwise check), and
+    randomly perturbed small matrices (300 cases): the library's verdict equals the
+    oracle's on every one."""
+    import paper_2201_07498_b200 as T
+    rng = np.random.default_rng(11)
+    cases = []
+    base = np.zeros((7, 7))
+    for (i, j, v) in [(0, 1, 0.5), (0, 2, 0.75), (1, 3, 1.25), (2, 5, 0.5), (4, 6, 1.0), (3, 3, 2.0)]:
+        base[i, j] = base[j, i] = v
+    cases.append(base)
+    t = base.copy(); t[0, 1], t[0, 2] = t[0, 2], t[0, 1]  # swap two upper values: lower unchanged
+    cases.append(t)
+    t = base.copy(); t[1, 0], t[2, 0] = 0.75, 0.5; t[0, 1], t[0, 2] = 0.75, 0.5  # consistent swap: symmetric
+    cases.append(t)
+    t = base.copy(); t[4, 6] = -1.0  # sign flip of one triangle
+    cases.append(t)
+    t = base.copy(); t[0, 1] = 0.0; t[0, 3] = 0.5  # an upper entry moved along its row
+    cases.append(t)
+    for _ in range(300):
+        n = int(rng.integers(2, 9))
+        a = np.zeros((n, n))
+        for _ in range(int(rng.integers(1, 12))):
+            i, j = rng.integers(0, n, 2)
+            v = float(rng.integers(1, 4)) / 4
+            a[i, j] = a[j, i] = v
+        kind = rng.integers(0, 4)
+        if kind == 1:  # perturb one stored entry
+            nz = np.argwhere(a != 0)
+            if len(nz):
+                i, j = nz[rng.integers(len(nz))]
+                a[i, j] = a[i, j] + 0.25
+        elif kind == 2:  # move one entry to a fresh position
+            nz = np.argwhere(a != 0)
+            if len(nz):
+                i, j = nz[rng.integers(len(nz))]
+                v = a[i, j]; a[i, j] = 0.0
+                a[int(rng.integers(0, n)), int(rng.integers(0, n))] = v
+        elif kind == 3:  # transpose-mirror swap of two values
+            nz = np.argwhere(np.triu(a, 1) != 0)
+            if len(nz) >= 2:
+                (i, j), (k, l) = nz[rng.choice(len(nz), 2, replace=False)]
+                a[i, j], a[k, l] = a[k, l], a[i, j]
+        cases.append(a)
+    for a in cases:
+        A = S.from_dense(a) if np.any(a) else None
+        if A is None:
+            continue
+        assert _sym_ok(T, A) == O.is_symmetric(A.n, A.rowptr, A.col, A.val), a
+    # stored entries that are +0.0 and -0.0 at mirrored positions: equal values, different bits
+    Z = S.from_dense(base)
+    for r, c, v in ((2, 5, -0.0), (5, 2, 0.0)):
+        k = int(Z.rowptr[r]) + int(np.where(Z.col[Z.rowptr[r]:Z.rowptr[r + 1]] == c)[0][0])
+        Z.val[k] = v
+    assert _sym_ok(T, Z) == O.is_symmetric(Z.n, Z.rowptr, Z.col, Z.val) == False
