@@ -55,6 +55,9 @@ WORKLOADS = {
     "C4X": dict(desc="R-MAT S=27 (n=2^27 = 134,217,728, GAP-kron's n, PAPER.md:180), 2.0e9 samples, seed 28, "
                      "symmetric, deduplicated -> nnz ~2.2e9 > 2^31 (64-bit offsets, SURVEY 8(f) NEXT-4)",
                 K=16, m=16, storage="f32", compute="f64"),
+    "C6": dict(desc="weighted Laplacian of a 4096 x 4096 4-neighbour grid, 25 % of edges dropped, seed 6, "
+                    "row-major ids (n=16,777,216, nnz ~67M; mesh / road class of Table I, PAPER.md:167-177)",
+               K=24, m=24, storage="f32", compute="f64"),
 }
 
 

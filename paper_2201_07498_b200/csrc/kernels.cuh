@@ -226,7 +226,12 @@ __device__ __forceinline__ int ld_col_stream(const int32_t *p) {
     return v;
 }
 
-template <typename VT, typename ST, typename CT, bool LOCAL>
+template <typename VT, typename ST, typename CT, bool LOCAL, bool BIG, int GQ>
+// GQ: nonzeros per lane per group (the next group's col/val are in flight while the
+// current group's x gathers are).
+// BIG = false: a pass without big-row chunks (low-degree matrices: meshes, road
+// networks); the chunk path is compiled out, which frees registers for more resident
+// warps (the host picks the instantiation from the pass's chunk count).
 // LOCAL: the first pass of the two-pass SpMV: only the own-slot
 // columns, which do not wait for the vector exchange; unscaled fp64 row sums to
 // ypart, no alpha, no state writes. Otherwise the final (or only) pass, which adds
@@ -243,7 +248,7 @@ template <typename VT, typename ST, typename CT, bool LOCAL>
 #else
 #define TOPK_SPMV_BOUNDS __launch_bounds__(kSpmvNT)
 #endif
-__global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
+__device__ __forceinline__ void spmv_body(const SpmvArgs &a, int it) {
     __shared__ CT red[kSpmvNT / 32];
     __shared__ double redd[kSpmvNT / 32];
     __shared__ int sflag;
@@ -266,10 +271,8 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
     ST *__restrict__ y = reinterpret_cast<ST *>(a.y);
     CT alpha_acc = CT(0);
     const int nwork = a.nchunks + a.nitems;
-    constexpr int GQ = TOPK_SPMV_GQ;  // nonzeros per lane per group; the next group's col/val are in flight
-                           // while the current group's x gathers are
     for (int wi = gwarp; wi < nwork; wi += nwarps) {
-        if (wi < a.nchunks) {
+        if (BIG && wi < a.nchunks) {
             // ---- big-row chunk: lane stream k = zb + lane + 32 t, warp reduction
             const Chunk *Cp = a.chunks + wi;
             const int64_t zb = __ldg(&Cp->z0);
@@ -352,6 +355,19 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             const int ntot = (int)((Sl.x - base) / 32 + Sl.y);  // total width of the item
             int sl = I.x;
             int bound = (int)__ldg(a.sell + sl).y;  // t at which slice sl ends
+            // one slice ahead: the next slice's width, and this slice's epilogue inputs
+            // (u_i and the own-pass partial of its row), so that low-degree slices (a few
+            // entries each) do not wait on a dependent load at every slice end
+            int wnext = (sl + 1 < I.y) ? (int)__ldg(a.sell + sl + 1).y : 0;
+            int row = a.nbig + 32 * sl + lane;
+            ST ucur = ST(0);
+            double ypc = 0.0;
+            if constexpr (!LOCAL) {
+                if (row < a.nnonempty) {
+                    ucur = ld_noalloc<ST>(ui + row);
+                    if (yp) ypc = __ldcg(yp + row);
+                }
+            }
             CT acc = CT(0);
             int cc[GQ];
             VT vv[GQ];
@@ -383,21 +399,28 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
                     if (t < ntot) {
                         acc += cvt<CT>(vc[q]) * cvt<CT>(xg[q]);
                         if (t + 1 == bound) {  // warp-uniform: slice sl complete
-                            const int row = a.nbig + 32 * sl + lane;
                             if (row < a.nnonempty) {
                                 if constexpr (LOCAL) {
                                     a.ypart[row] = (double)acc;
                                 } else {
-                                    if (yp) acc += (CT)__ldcg(yp + row);
+                                    if (yp) acc += (CT)ypc;
                                     const CT yv = s * acc;
                                     y[row] = rnd_ct<ST, CT>(yv);
-                                    alpha_acc += yv * (s * cvt<CT>(ld_noalloc<ST>(ui + row)));
+                                    alpha_acc += yv * (s * cvt<CT>(ucur));
                                     if (a.y_dbg) a.y_dbg[row] = (double)acc;
                                 }
                             }
                             acc = CT(0);
                             ++sl;
-                            if (sl < I.y) bound += (int)__ldg(a.sell + sl).y;
+                            bound += wnext;
+                            wnext = (sl + 1 < I.y) ? (int)__ldg(a.sell + sl + 1).y : 0;
+                            row += 32;
+                            if constexpr (!LOCAL) {
+                                if (row < a.nnonempty) {
+                                    ucur = ld_noalloc<ST>(ui + row);
+                                    if (yp) ypc = __ldcg(yp + row);
+                                }
+                            }
                         }
                     }
                 }
@@ -415,6 +438,27 @@ __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
             *a.counter = 0u;
         }
     }
+}
+
+// The SpMV kernels: with the big-row chunk path (plain bound; measured above), and
+// SELL-only (a pass without chunks: low-degree matrices such as meshes and road
+// networks). Measured on C6 (tools/lab/spmv_ab.py, profiles/r02_mesh_spmv_ab.jsonl):
+// (min CTAs/SM, GQ) = (3, 8) 167-171 us, (4, 4) 172, (3, 6) 176, (6, 2) 186, (5, 4) 198,
+// (2, 16) 199, (4, 2) 226, (6, 4) 257 (spills): more resident warps do not beat
+// deeper per-warp groups; the stream marked L2 evict-first: 194 vs 172 (worse).
+#ifndef TOPK_SPMV_SELL_MINB
+#define TOPK_SPMV_SELL_MINB 3
+#endif
+#ifndef TOPK_SPMV_SELL_GQ
+#define TOPK_SPMV_SELL_GQ 8
+#endif
+template <typename VT, typename ST, typename CT, bool LOCAL>
+__global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
+    spmv_body<VT, ST, CT, LOCAL, true, TOPK_SPMV_GQ>(a, it);
+}
+template <typename VT, typename ST, typename CT, bool LOCAL>
+__global__ void __launch_bounds__(kSpmvNT, TOPK_SPMV_SELL_MINB) k_spmv_sell(SpmvArgs a, int it) {
+    spmv_body<VT, ST, CT, LOCAL, false, TOPK_SPMV_SELL_GQ>(a, it);
 }
 
 // ---------------------------------------------------------------------------

@@ -160,6 +160,7 @@ struct topk_eig_s {
     int conv_checks = 0;     // checks enqueued per solve
     int use_graph = 1;
     int nsm = 148;
+    int grid_spmv_v[2] = {0, 0};  // k_spmv without / with the big-row chunk path
     int grid_spmv = 0, grid_stream = 0, grid_step = 0, grid_corr = 0, grid_ritz = 0;
     int ritz_tn = 0;           // > 0: Ritz output pass on the fp64 tensor cores, 8 * ritz_tn outputs per warp
     bool use_gram = false;  // Ritz norms from the Gram matrix (reading Q24; no Ritz pass 0)
@@ -401,6 +402,15 @@ static void pass_args(SpmvArgs &a, const SpmvDev &d) {
     a.alpha_long = d.alpha_long; a.nlong = d.nlong;
 }
 
+template <typename VT, typename ST, typename CT, bool LOCAL>
+static void spmv_pass(topk_eig_s *h, const SpmvArgs &a, int it) {
+    if (a.nchunks > 0)
+        k_spmv<VT, ST, CT, LOCAL><<<h->grid_spmv_v[1], kSpmvNT, 0, h->stream>>>(a, it);
+    else
+        k_spmv_sell<VT, ST, CT, LOCAL><<<h->grid_spmv_v[0], kSpmvNT, 0, h->stream>>>(a, it);
+    CUDA_TRY(cudaGetLastError());
+}
+
 // a7. Two-pass SpMV (h->split): the own-slot columns first (they do
 // not need the vector exchange), then -- after the exchange, which one process per GPU
 // runs on the comm stream meanwhile -- the other columns plus the epilogue.
@@ -419,14 +429,12 @@ static void launch_spmv(topk_eig_s *h, Part &p, int it, double *y_dbg) {
     prof_begin(h, p, 1);
     if (p.ypart) {
         pass_args(a, p.own);
-        k_spmv<VT, ST, CT, true><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
-        CUDA_TRY(cudaGetLastError());
+        spmv_pass<VT, ST, CT, true>(h, a, it);
         h->launches++;
         exch_join(h);  // the remote columns need the exchanged vector
     }
     pass_args(a, p.sp);
-    k_spmv<VT, ST, CT, false><<<h->grid_spmv, kSpmvNT, 0, h->stream>>>(a, it);
-    CUDA_TRY(cudaGetLastError());
+    spmv_pass<VT, ST, CT, false>(h, a, it);
     prof_end(h, p);
     h->launches++;
 }
@@ -789,8 +797,14 @@ static void set_kernels(topk_eig_s *h) {
     // the SpMV uses no dynamic shared memory: the whole unified L1 caches x
     CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CUDA_TRY(cudaFuncSetAttribute(k_spmv<VT, ST, CT, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CUDA_TRY(cudaFuncSetAttribute(k_spmv_sell<VT, ST, CT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CUDA_TRY(cudaFuncSetAttribute(k_spmv_sell<VT, ST, CT, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<VT, ST, CT, false>, kSpmvNT, 0);
-    h->grid_spmv = h->nsm * std::max(1, occ);
+    h->grid_spmv_v[1] = h->nsm * std::max(1, occ);
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell<VT, ST, CT, false>, kSpmvNT, 0);
+    h->grid_spmv_v[0] = h->nsm * std::max(1, occ);
+    h->grid_spmv = std::max(h->grid_spmv_v[0], h->grid_spmv_v[1]);  // slot allocation
     int occ2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_step<ST, CT, kStepJB>, kNT, 0);
     h->grid_step = h->nsm * std::max(1, std::min(occ2, 8));

@@ -51,6 +51,9 @@ def _load():
                                 ctypes.c_double, ctypes.c_double, ctypes.c_uint64]
         lib.sg_tridiag.restype = ctypes.POINTER(_Csr)
         lib.sg_tridiag.argtypes = [ctypes.c_int, ctypes.c_int64]
+        lib.sg_grid2d.restype = ctypes.POINTER(_Csr)
+        lib.sg_grid2d.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                  ctypes.c_uint64]
         lib.sg_free.argtypes = [ctypes.POINTER(_Csr)]
         lib.sg_er_coo.restype = ctypes.c_int64
         lib.sg_er_coo.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64,
@@ -124,6 +127,20 @@ def path_laplacian(n: int) -> CSR:
 def cycle_laplacian(n: int) -> CSR:
     """Cycle Laplacian (n >= 3): eigenvalues 2 - 2 cos(2 pi k / n), k = 0..n-1."""
     return _take(_load().sg_tridiag(2, n))
+
+
+def grid_dirichlet(nx: int, ny: int) -> CSR:
+    """5-point Dirichlet Laplacian on an nx x ny grid (row-major ids): eigenvalues
+    4 - 2 cos(pi i / (nx+1)) - 2 cos(pi j / (ny+1)), i = 1..nx, j = 1..ny."""
+    return _take(_load().sg_grid2d(0, nx, ny, 0.0, 0))
+
+
+def grid_laplacian(nx: int, ny: int, drop: float, seed: int) -> CSR:
+    """Weighted graph Laplacian D - W of an nx x ny 4-neighbour grid with each edge
+    dropped with probability `drop` (mesh / road-network class of PAPER.md Table I);
+    weights k/128, k in [64, 191]; row-major ids (spatial locality); isolated
+    vertices are empty rows."""
+    return _take(_load().sg_grid2d(1, nx, ny, drop, seed))
 
 
 def er_coo(n: int, samples: int, seed: int) -> COO:
@@ -231,6 +248,10 @@ def config_matrix(name: str):
     C3S: R-MAT S=16 (n=65,536), 491,520 samples, seed 16 (C3 shape, oracle-fast).
     C4: R-MAT ids over 2^27 rejected if >= n = 100,000,000, 1,410,000,000 samples,
         seed 27 -> nnz ~ 1.5e9 (host RAM ~45 GB while generating).
+    C6: weighted Laplacian of a 4096 x 4096 grid, 25 % of edges dropped, seed 6 ->
+        n = 16,777,216, nnz ~ 67M (mesh / road class of Table I, e.g. hugetrace-00020:
+        16.0 M rows, 47.8 M nnz; row-major ids keep the spatial locality).
+    C6S: the same recipe on a 300 x 200 grid, seed 6 (oracle-fast).
     C4X: R-MAT S=27, n = 2^27 (GAP-kron's n), 2.0e9 samples, seed 28 ->
         nnz ~ 2.2e9 > 2^31 (host RAM ~70 GB while generating).
     """
@@ -246,6 +267,10 @@ def config_matrix(name: str):
         return rmat(16, 491_520, 16)
     if name == "C4":
         return rmat(27, 1_410_000_000, 27, n=100_000_000)
+    if name == "C6":
+        return grid_laplacian(4096, 4096, 0.25, 6)
+    if name == "C6S":
+        return grid_laplacian(300, 200, 0.25, 6)
     if name == "C4X":
         return rmat(27, 2_000_000_000, 28)
     raise KeyError(name)

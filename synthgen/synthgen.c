@@ -1,6 +1,6 @@
 /*
  * synthgen.c — seeded synthetic INPUT generators (ER, R-MAT, Dirichlet path,
- * path/cycle Laplacians).
+ * path/cycle Laplacians, 2-D grids).
  *
  * This module is input infrastructure shared by the oracle (oracle/) and the
  * CUDA path (paper_2201_07498_b200/). It holds none of the eigensolver's
@@ -293,5 +293,71 @@ sg_csr_t *sg_tridiag(int kind, int64_t n) {
     }
     m->rowptr[n] = k;
     m->nnz = k;
+    return m;
+}
+
+/* 2-D grid (mesh / road-network class of Table I: hugetrace-00020, venturiLevel3,
+ * *_osm, road_central). Vertex r = y * nx + x, 4-neighbour edges.
+ *   kind 0: Dirichlet 5-point Laplacian (diagonal 4, off-diagonal -1, no drops);
+ *           eigenvalues 4 - 2 cos(pi i/(nx+1)) - 2 cos(pi j/(ny+1)), i<=nx, j<=ny.
+ *   kind 1: weighted graph Laplacian D - W: each grid edge {u, v} is kept unless
+ *           U(h(seed, min, max)) < drop; weight k/128, k in [64, 191] from a second
+ *           hash of the same pair (so both triangles hold identical bits); diagonal =
+ *           sum of the kept weights (exact in f64/f32); isolated vertices have empty rows.
+ * Columns are ascending within a row (r - nx, r - 1, r, r + 1, r + nx). */
+static inline int grid_edge(uint64_t seed, double drop, int64_t u, int64_t v, double *w) {
+    const int64_t a = u < v ? u : v, b = u < v ? v : u;
+    if (sg_unit(sg_h3(seed, (uint64_t)a, (uint64_t)b)) < drop) return 0;
+    *w = (double)(64 + (int)(sg_h3(seed ^ 0x5bd1e995ull, (uint64_t)a, (uint64_t)b) % 128)) / 128.0;
+    return 1;
+}
+
+static int grid_row(int kind, int64_t nx, int64_t ny, double drop, uint64_t seed, int64_t r,
+                    int32_t *col, double *val) {
+    const int64_t x = r % nx, y = r / nx;
+    int64_t nb[4];
+    int c = 0;
+    if (y > 0) nb[c++] = r - nx;
+    if (x > 0) nb[c++] = r - 1;
+    const int lower = c;
+    if (x < nx - 1) nb[c++] = r + 1;
+    if (y < ny - 1) nb[c++] = r + nx;
+    int k = 0;
+    double diag = 0.0;
+    double wv[4];
+    int keep[4];
+    for (int i = 0; i < c; ++i) {
+        if (kind == 0) { keep[i] = 1; wv[i] = 1.0; }
+        else keep[i] = grid_edge(seed, drop, r, nb[i], &wv[i]);
+        if (keep[i]) diag += wv[i];
+    }
+    if (kind == 0) diag = 4.0;
+    for (int i = 0; i < lower; ++i)
+        if (keep[i]) { if (col) { col[k] = (int32_t)nb[i]; val[k] = -wv[i]; } ++k; }
+    if (kind == 0 || diag != 0.0) { if (col) { col[k] = (int32_t)r; val[k] = diag; } ++k; }
+    for (int i = lower; i < c; ++i)
+        if (keep[i]) { if (col) { col[k] = (int32_t)nb[i]; val[k] = -wv[i]; } ++k; }
+    return k;
+}
+
+sg_csr_t *sg_grid2d(int kind, int64_t nx, int64_t ny, double drop, uint64_t seed) {
+    if (nx < 1 || ny < 1 || nx * ny > 2147483647ll || (kind != 0 && kind != 1)) return NULL;
+    const int64_t n = nx * ny;
+    sg_csr_t *m = (sg_csr_t *)calloc(1, sizeof(sg_csr_t));
+    if (!m) return NULL;
+    m->n = n;
+    m->rowptr = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+    if (!m->rowptr) { sg_free(m); return NULL; }
+    m->rowptr[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n; ++r) m->rowptr[r + 1] = grid_row(kind, nx, ny, drop, seed, r, NULL, NULL);
+    for (int64_t r = 0; r < n; ++r) m->rowptr[r + 1] += m->rowptr[r];
+    m->nnz = m->rowptr[n];
+    m->col = (int32_t *)malloc((size_t)(m->nnz > 0 ? m->nnz : 1) * sizeof(int32_t));
+    m->val = (double *)malloc((size_t)(m->nnz > 0 ? m->nnz : 1) * sizeof(double));
+    if (!m->col || !m->val) { sg_free(m); return NULL; }
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n; ++r)
+        grid_row(kind, nx, ny, drop, seed, r, m->col + m->rowptr[r], m->val + m->rowptr[r]);
     return m;
 }

@@ -338,6 +338,50 @@ def test_p4_dirichlet_1M_closed_form():
     assert r.lanczos.beta[16] <= 1e-8
 
 
+# ---------------------------------------------------------------- P16 (O3-O9, 2-D)
+def test_p16_grid_dirichlet_closed_form():
+    """5-point Dirichlet Laplacian on a 300 x 200 grid (the mesh class of C6): it is
+    the Kronecker sum T_nx (+) T_ny, with eigenvectors sin(pi i x/(nx+1)) sin(pi j y/(ny+1))
+    and eigenvalues 4 - 2cos(pi i/(nx+1)) - 2cos(pi j/(ny+1)). v1 = sum of 8 such modes
+    with well-separated eigenvalues: the Krylov space is their span, so the 8 Ritz values
+    are those eigenvalues (the P4 argument in two dimensions). Modes with clustered
+    eigenvalues near the dense centre of this spectrum are avoided: there the rounding
+    error of the sine vectors (~1e-16 along the other 59,992 modes) is amplified by the
+    Krylov polynomial through small beta_i (measured: 12 modes including 3.9732/3.9739
+    leave beta_13 = 3.6e-3 and Ritz values 2e-6 off)."""
+    nx, ny = 300, 200
+    A = S.grid_dirichlet(nx, ny)
+    assert A.n == nx * ny and A.nnz == 5 * nx * ny - 2 * (nx + ny)
+    modes = [(1, 1), (300, 200), (40, 30), (260, 170), (100, 60), (200, 140), (150, 100), (120, 40)]
+    x = np.arange(1, nx + 1)
+    y = np.arange(1, ny + 1)
+    v1 = np.zeros(nx * ny)
+    for i, j in modes:  # vertex r = (y-1) * nx + (x-1)
+        v1 += np.outer(np.sin(np.pi * j * y / (ny + 1)), np.sin(np.pi * i * x / (nx + 1))).ravel()
+    lam = np.array([4 - 2 * np.cos(np.pi * i / (nx + 1)) - 2 * np.cos(np.pi * j / (ny + 1)) for i, j in modes])
+    assert np.min(np.diff(np.sort(lam))) > 1e-6
+    r = O.solve(A.rowptr, A.col, A.val, K=8, m=8, v1vec=v1, tau=0.0, want_vectors=False)
+    assert np.abs(np.sort(r.theta_all) - np.sort(lam)).max() <= 1e-12
+    assert r.lanczos.beta[8] <= 1e-9
+
+
+def test_grid_laplacian_generator_properties():
+    """The weighted grid Laplacian D - W (C6 recipe): symmetric bit for bit, zero row
+    sums, off-diagonals only between grid neighbours, and its kernel dimension equals
+    the number of connected components of the kept edges (graph theory)."""
+    nx, ny = 23, 17
+    A = S.grid_laplacian(nx, ny, 0.35, 11)
+    D = A.to_dense()
+    assert np.array_equal(D, D.T) and np.abs(D.sum(axis=1)).max() == 0.0
+    r, c = np.nonzero(D - np.diag(np.diag(D)))
+    d = np.abs(r - c)
+    assert np.all((d == 1) & (r // nx == c // nx) | (d == nx))
+    import scipy.sparse.csgraph as cg
+    ncomp, _ = cg.connected_components(sp.csr_matrix(D != 0))
+    ev = np.linalg.eigvalsh(D)
+    assert np.sum(np.abs(ev) <= 1e-10) == ncomp and ev.min() > -1e-10
+
+
 # ---------------------------------------------------------------- P5, P7 (O4-O10)
 @pytest.mark.parametrize("kind", ["dirichlet", "cycle"])
 def test_p5_kahan_bound_random_start(kind):
