@@ -9,7 +9,11 @@ CODE = r'''
 import os, sys, json
 sys.path.insert(0, %r)
 import torch, synthgen as S, paper_2201_07498_b200 as T
-A = S.config_matrix(os.environ.get("AB_WL", "C3"))
+if os.environ.get("AB_GRID"):  # nx,ny,drop: a weighted grid Laplacian instead of a named config
+    nx, ny, dr = os.environ["AB_GRID"].split(",")
+    A = S.grid_laplacian(int(nx), int(ny), float(dr), 6)
+else:
+    A = S.config_matrix(os.environ.get("AB_WL", "C3"))
 with T.TopkEig(A, 24, "f32", "f64", m=24, profile=True, check_symmetry=False) as h:
     for i in range(3): h.solve(seed=1, vectors=False)
     kt = h.kernel_times()
@@ -25,7 +29,8 @@ with T.TopkEig(A, 24, "f32", "f64", m=24, check_symmetry=False) as h:
     e1.record(st); h.sync()
     ms = e0.elapsed_time(e1) / 50
     r = h.solve(seed=1, vectors=False)
-print(json.dumps({"lib": os.environ.get("AB_NAME", "default"),
+print(json.dumps({"lib": os.environ.get("AB_NAME", "default"), "n": A.n, "nnz": A.nnz,
+                  "matrix": os.environ.get("AB_GRID") or os.environ.get("AB_WL", "C3"),
                   "spmv_us": round(kt["spmv"][0] / 24 * 1e3, 1), "solve_ms": round(ms, 4),
                   "top": r.eigenvalues[0]}))
 ''' % ROOT

@@ -5,7 +5,7 @@ selected through TOPK_LIB; the script's output lines are prefixed with the name.
 import os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from tools.build import build_variant  # noqa: E402
+from tools.build import build_variant, deps  # noqa: E402
 
 script = sys.argv[1]
 libs = [("default", None)]
@@ -13,7 +13,8 @@ os.makedirs(os.path.join(ROOT, "tools/lab/variants"), exist_ok=True)
 for spec in sys.argv[2:]:
     name, _, defs = spec.partition("=")
     out = os.path.join(ROOT, "tools/lab/variants", f"lib_{name}.so")
-    build_variant(out, [d for d in defs.split(",") if d])
+    if not (os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(f) for f in deps())):
+        build_variant(out, [d for d in defs.split(",") if d])  # else prebuilt here (travels with gpurun)
     libs.append((name, out))
 for name, lib in libs:
     env = dict(os.environ)
