@@ -72,22 +72,35 @@ topk_status_t canonicalize(const topk_matrix_t &A, Csr &out, std::string &err) {
         err = "values_dtype must be TOPK_F64 or TOPK_F32"; return TOPK_E_INVALID;
     }
     int bad_col = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad_col)
-    for (int64_t k = 0; k < nnz; ++k)
-        if (A.col_idx[k] < 0 || (int64_t)A.col_idx[k] >= n) bad_col = 1;
-    if (bad_col) { err = "column index out of range"; return TOPK_E_STRUCTURE; }
+    int unsorted = 1;
     if (A.format == TOPK_CSR) {
         if (!A.row_ptr) { err = "row_ptr is NULL"; return TOPK_E_INVALID; }
         if (A.row_ptr[0] != 0 || A.row_ptr[n] != nnz) { err = "row_ptr[0] must be 0 and row_ptr[n] must be nnz"; return TOPK_E_STRUCTURE; }
-        for (int64_t r = 0; r < n; ++r)
-            if (A.row_ptr[r + 1] < A.row_ptr[r]) { err = "row_ptr is not non-decreasing"; return TOPK_E_STRUCTURE; }
-        // fast path: columns already strictly increasing in every row (canonical
-        // input) -> one parallel copy, no regrouping
-        int unsorted = 0;
-#pragma omp parallel for schedule(dynamic, 4096) reduction(| : unsorted)
-        for (int64_t r = 0; r < n; ++r)
-            for (int64_t k = A.row_ptr[r] + 1; k < A.row_ptr[r + 1]; ++k)
-                if (A.col_idx[k] <= A.col_idx[k - 1]) { unsorted = 1; break; }
+        int bad_rp = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad_rp)
+        for (int64_t r = 0; r < n; ++r) bad_rp |= (A.row_ptr[r + 1] < A.row_ptr[r]);
+        if (bad_rp) { err = "row_ptr is not non-decreasing"; return TOPK_E_STRUCTURE; }
+        // one pass over the entries, row by row (row_ptr is monotonic from 0 to nnz, so
+        // the rows cover every entry once): range check, and whether the columns are
+        // already strictly increasing in every row (canonical input -> borrowed, no copy)
+        unsorted = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : bad_col, unsorted)
+        for (int64_t r = 0; r < n; ++r) {
+            int32_t prev = -1;
+            for (int64_t k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k) {
+                const int32_t c = A.col_idx[k];
+                bad_col |= (c < 0) | ((int64_t)c >= n);
+                unsorted |= (c <= prev);
+                prev = c;
+            }
+        }
+    } else {
+#pragma omp parallel for schedule(static) reduction(| : bad_col)
+        for (int64_t k = 0; k < nnz; ++k)
+            if (A.col_idx[k] < 0 || (int64_t)A.col_idx[k] >= n) bad_col = 1;
+    }
+    if (bad_col) { err = "column index out of range"; return TOPK_E_STRUCTURE; }
+    if (A.format == TOPK_CSR) {
         if (!unsorted) {
             out.n = n;
             out.rowptr = {A.row_ptr, (size_t)n + 1};
@@ -231,6 +244,7 @@ static int64_t parts_needed(const int64_t *rowptr, int64_t n, int64_t B, int64_t
 topk_status_t partition_rule_p(const int64_t *rowptr, int64_t n, int32_t G, int64_t *b) {
     if (G < 1 || n < G) return TOPK_E_INVALID;
     int64_t maxrow = 0;
+#pragma omp parallel for schedule(static) reduction(max : maxrow)
     for (int64_t r = 0; r < n; ++r) maxrow = std::max(maxrow, rowptr[r + 1] - rowptr[r]);
     int64_t lo = maxrow, hi = std::max(maxrow, rowptr[n]);
     while (lo < hi) {
@@ -283,7 +297,7 @@ double bf16_bits_to_double(uint16_t b) {
 
 
 
-void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos) {
+void degree_order(const Csr &m, const int64_t *b, int32_t G, hvec<int32_t> &pos) {
     // stable counting sort by degree, descending (ties keep ascending row index)
     pos.resize((size_t)m.n);
     auto deg = [&](int64_t r) { return m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r]; };
@@ -295,8 +309,10 @@ void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t
         const int64_t nb = dmax + 1;  // key = dmax - degree
         const int T = (nr >= (1 << 16) && nb <= (1 << 22)) ? std::max(1, omp_get_max_threads()) : 1;
         // per-thread histograms over contiguous row chunks; positions = (key, thread, row) order
-        std::vector<int64_t> cnt((size_t)T * (size_t)nb, 0);
+        hvec<int64_t> cnt((size_t)T * (size_t)nb);
         const int64_t per = (nr + T - 1) / T;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+        for (int t = 0; t < T; ++t) std::fill(cnt.data() + (size_t)t * nb, cnt.data() + (size_t)(t + 1) * nb, int64_t(0));
 #pragma omp parallel for schedule(static, 1) num_threads(T)
         for (int t = 0; t < T; ++t) {
             int64_t *c = cnt.data() + (size_t)t * nb;
@@ -321,8 +337,8 @@ void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t
 }
 
 
-std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos) {
-    std::vector<int32_t> cm((size_t)n);
+hvec<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos) {
+    hvec<int32_t> cm((size_t)n);
     for (int32_t q = 0; q < G; ++q) {
 #pragma omp parallel for schedule(static)
         for (int64_t c = b[q]; c < b[q + 1]; ++c) cm[(size_t)c] = (int32_t)(q * npad + pos[(size_t)c]);

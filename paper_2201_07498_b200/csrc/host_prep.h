@@ -12,12 +12,25 @@
 
 namespace topk {
 
+void *host_block_alloc(size_t bytes);  // mem_pool.cpp: cached large host blocks
+void host_block_free(void *p, size_t bytes);
+
 // Allocator that default-initialises (no zero fill) so large host buffers are
-// first touched by the parallel loops that fill them.
+// first touched by the parallel loops that fill them; blocks of >= 1 MB come from
+// the process-wide host block cache (mem_pool.h), so repeated creates reuse pages.
 template <class T> struct NoInitAlloc : std::allocator<T> {
     template <class U> struct rebind { using other = NoInitAlloc<U>; };
+    static constexpr size_t kBig = size_t(1) << 20;
     NoInitAlloc() = default;
     template <class U> NoInitAlloc(const NoInitAlloc<U> &) {}
+    T *allocate(size_t n) {
+        if (n * sizeof(T) >= kBig) return static_cast<T *>(host_block_alloc(n * sizeof(T)));
+        return std::allocator<T>::allocate(n);
+    }
+    void deallocate(T *p, size_t n) {
+        if (n * sizeof(T) >= kBig) host_block_free(p, n * sizeof(T));
+        else std::allocator<T>::deallocate(p, n);
+    }
     template <class U> void construct(U *p) noexcept { ::new ((void *)p) U; }
     template <class U, class... A> void construct(U *p, A &&...a) { ::new ((void *)p) U(std::forward<A>(a)...); }
 };
@@ -87,9 +100,9 @@ double bf16_bits_to_double(uint16_t b);
 // columns are the dense prefix of every slot, so the SpMV's plain L1-cached x
 // gathers keep them resident.
 // pos[r] = position of global row r inside its part's degree order.
-void degree_order(const Csr &m, const int64_t *b, int32_t G, std::vector<int32_t> &pos);
+void degree_order(const Csr &m, const int64_t *b, int32_t G, hvec<int32_t> &pos);
 // colmap[c] = device column entry of global column c (one lookup per nonzero).
-std::vector<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos);
+hvec<int32_t> column_map(int64_t n, const int64_t *b, int32_t G, int64_t npad, const int32_t *pos);
 
 // Halo exchange (reading Q27): part g's SpMV input
 // is a compact vector x_g = [own slot (n_pad) | the remote columns its rows touch,
@@ -145,8 +158,8 @@ struct LongRow {
 
 struct PartLayout {
     int64_t row0 = 0, nrows = 0, npad = 0, nnonempty = 0;
-    std::vector<int64_t> rowptr;    // nrows+1, logical CSR in degree order
-    std::vector<int32_t> perm;      // nrows: part-local original row at each position
+    hvec<int64_t> rowptr;           // nrows+1, logical CSR in degree order
+    hvec<int32_t> perm;             // nrows: part-local original row at each position
     // physical SpMV format
     int32_t nbig = 0;
     int64_t nphys = 0;              // physical entries (big-row CSR + padded SELL)

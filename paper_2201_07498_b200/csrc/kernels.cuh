@@ -1742,6 +1742,42 @@ __global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const in
     }
 }
 
+// big rows, single pass (MODE 0: every entry kept, so entry j of row p goes to
+// dbig[p] + j = the logical offset): warp per SpMV chunk (<= kChunkNnz entries), so a
+// hub row of ~10^5 entries is spread over many warps instead of one (k_layout_big's
+// warp per row took 3.5 ms on C3 for its longest row alone)
+template <typename VT>
+__global__ void __launch_bounds__(256) k_layout_big_chunks(const int64_t *srp, const int32_t *scol, const VT *sval,
+                                                           const int32_t *perm, const int64_t *drp, const Chunk *chunks,
+                                                           int nchunks, const int32_t *colmap, int32_t *pcol, VT *pval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t ci = w; ci < nchunks; ci += nw) {
+        const Chunk C = chunks[ci];
+        const int64_t src0 = srp[perm[C.row]] + (C.z0 - drp[C.row]);
+        constexpr int U = 8;
+        for (int e0 = 0; e0 < C.cnt; e0 += 32 * U) {
+            int32_t c[U];
+            VT v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + 32 * u + lane;
+                c[u] = e < C.cnt ? scol[src0 + e] : 0;
+                v[u] = e < C.cnt ? sval[src0 + e] : VT(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + 32 * u + lane;
+                if (e < C.cnt) {
+                    pcol[C.z0 + e] = colmap[c[u]];
+                    pval[C.z0 + e] = v[u];
+                }
+            }
+        }
+    }
+}
+
 // SELL slices: thread per slice row; the j-th kept entry to base + 32 j + i, then padding
 template <typename VT, int MODE>
 __global__ void __launch_bounds__(256) k_layout_sell(const int64_t *srp, const int32_t *scol, const VT *sval,

@@ -8,7 +8,12 @@
 #include <unordered_map>
 #include <utility>
 
+#include <cstdlib>
+#include <new>
+#include <vector>
+
 #include <omp.h>
+#include <sys/mman.h>
 
 namespace topk {
 
@@ -84,10 +89,80 @@ void pool_dev_free(void *p) {
     P.live.erase(it);
 }
 
+namespace {
+struct HostPool {
+    std::mutex mu;
+    std::multimap<size_t, void *> cached;  // rounded size -> block
+    size_t cached_bytes = 0;
+};
+HostPool &host_pool() {
+    static HostPool *p = new HostPool();
+    return *p;
+}
+constexpr size_t kHostGran = size_t(2) << 20;
+constexpr size_t kHostCacheMax = size_t(32) << 30;  // cached (unused) host bytes kept at most
+size_t host_round(size_t b) { return (b + kHostGran - 1) / kHostGran * kHostGran; }
+size_t trim_host_locked(HostPool &P) {
+    size_t freed = 0;
+    for (auto &kv : P.cached) {
+        std::free(kv.second);
+        freed += kv.first;
+    }
+    P.cached.clear();
+    P.cached_bytes = 0;
+    return freed;
+}
+}  // namespace
+
+void *host_block_alloc(size_t bytes) {
+    const size_t rb = host_round(std::max<size_t>(bytes, 1));
+    HostPool &P = host_pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto it = P.cached.find(rb);
+        if (it != P.cached.end()) {
+            void *p = it->second;
+            P.cached.erase(it);
+            P.cached_bytes -= rb;
+            return p;
+        }
+    }
+    void *p = std::aligned_alloc(kHostGran, rb);
+    if (!p) {
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            trim_host_locked(P);
+        }
+        p = std::aligned_alloc(kHostGran, rb);
+        if (!p) throw std::bad_alloc();
+    }
+    madvise(p, rb, MADV_HUGEPAGE);  // advisory: fewer, larger first-touch faults
+    return p;
+}
+
+void host_block_free(void *p, size_t bytes) {
+    if (!p) return;
+    const size_t rb = host_round(std::max<size_t>(bytes, 1));
+    HostPool &P = host_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.cached_bytes + rb > kHostCacheMax) {
+        std::free(p);
+        return;
+    }
+    P.cached.insert({rb, p});
+    P.cached_bytes += rb;
+}
+
 size_t pool_trim() {
+    size_t freed = 0;
+    {
+        HostPool &H = host_pool();
+        std::lock_guard<std::mutex> lk(H.mu);
+        freed += trim_host_locked(H);
+    }
     DevPool &P = dev_pool();
     std::lock_guard<std::mutex> lk(P.mu);
-    return trim_device_locked(P, -1);
+    return freed + trim_device_locked(P, -1);
 }
 
 void par_memcpy(void *dst, const void *src, size_t bytes) {

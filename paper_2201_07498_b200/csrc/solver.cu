@@ -112,9 +112,9 @@ struct Part {
     int nbig = 0;
     int64_t nnonempty = 0;
     int32_t *perm = nullptr;
-    std::vector<int32_t> h_perm;    // host copy: position -> part-local original row
+    hvec<int32_t> h_perm;           // host copy: position -> part-local original row
     int32_t *inv = nullptr;         // original part-local row -> position
-    std::vector<int64_t> h_rowptr;  // host copy (export_layout)
+    hvec<int64_t> h_rowptr;         // host copy (export_layout)
     SpmvDev sp;                     // the SpMV (final pass when split)
     SpmvDev own;                    // two-pass SpMV: own-slot columns first
     double *ypart = nullptr;        // own-slot row sums of the first pass (nullptr: one pass)
@@ -987,7 +987,13 @@ template <typename VT, int MODE>
 static void scatter_pass(topk_eig_s *h, Part &p, const PartLayout &L, const DevCsr &d, const int32_t *d_colmap,
                          const int64_t *d_drp, SpmvDev &dp) {
     const VT *sval = static_cast<const VT *>(d.sval);
-    if (L.nbig > 0) {
+    if (L.nbig > 0 && MODE == 0) {
+        if (dp.nchunks > 0) {
+            k_layout_big_chunks<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, dp.chunks, dp.nchunks,
+                                                                       d_colmap, dp.col, reinterpret_cast<VT *>(dp.val));
+            CUDA_TRY(cudaGetLastError());
+        }
+    } else if (L.nbig > 0) {
         int64_t *d_big = static_cast<int64_t *>(dalloc_or_throw(dp.h_bigptr.size() * 8));
         CUDA_TRY(scopy(h->stream, d_big, dp.h_bigptr.data(), dp.h_bigptr.size() * 8, cudaMemcpyHostToDevice));
         k_layout_big<VT, MODE><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_big, d_colmap, L.nbig,
@@ -1262,9 +1268,9 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 for (DevCsr &x : d) free_dev_csr(x);
             }
         } joiner{uploader, dcsr};
-        std::vector<int32_t> pos;
+        hvec<int32_t> pos;
         degree_order(csr, h->bounds.data(), G, pos);
-        const std::vector<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
+        const hvec<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
         clk.mark("degree order + column map");
         if (!select_kernels(h.get())) return fail(TOPK_E_INVALID, "unsupported (values, storage, compute) dtype combination");
         clk.mark("kernel attributes");
@@ -1366,11 +1372,6 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         int32_t *d_colmap = static_cast<int32_t *>(pool_dev_alloc((size_t)n * 4));
         if (!d_colmap) CUDA_TRY(cudaErrorMemoryAllocation);
         struct ColmapGuard { int32_t *p; ~ColmapGuard() { pool_dev_free(p); } } colmap_guard{d_colmap};
-        if (!h->halo) {
-            const char *cm = reinterpret_cast<const char *>(colmap.data());
-            CUDA_TRY(staged_h2d(d_colmap, (size_t)n * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },
-                                h->stream));
-        }
         h->parts.resize((size_t)nlocal);
         for (int lp = 0; lp < nlocal; ++lp) {
             Part &p = h->parts[(size_t)lp];
@@ -1381,8 +1382,6 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             clk.mark("layout tables");
             p.row0 = L.row0; p.nrows = L.nrows; p.npad = npad; p.nnz = (int64_t)L.rowptr.back();
             p.nbig = L.nbig; p.nnonempty = L.nnonempty;
-            p.h_rowptr = L.rowptr;
-            p.h_perm = L.perm;
             p.perm = h->alloc<int32_t>(L.perm.size());
             p.inv = h->alloc<int32_t>(L.perm.size());
             CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1394,6 +1393,11 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 CUDA_TRY(scopy(h->stream, p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
             }
             if (h->halo) setup_halo(h.get(), p, csr, npad, pos.data(), d_colmap);
+            if (lp == 0 && !h->halo) {  // after the first part's tables: the staging buffers are the uploader's until then
+                const char *cm = reinterpret_cast<const char *>(colmap.data());
+                CUDA_TRY(staged_h2d(d_colmap, (size_t)n * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },
+                                    h->stream));
+            }
             if (uploader.joinable()) {
                 uploader.join();
                 clk.mark("wait for CSR upload");
@@ -1401,6 +1405,8 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             }
             device_layout(h.get(), p, L, dcsr[(size_t)lp], d_colmap);
             free_dev_csr(dcsr[(size_t)lp]);
+            p.h_rowptr = std::move(L.rowptr);  // host copies for the exports
+            p.h_perm = std::move(L.perm);
             clk.mark("device layout");
             const size_t vsz = dsize(storage);
             p.V = h->alloc<char>((size_t)(m + 1) * npad * vsz);
@@ -1694,9 +1700,9 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
         s = partition_rule_p(csr.rowptr.data(), csr.n, G, b.data());
         if (s != TOPK_OK) return fail(s, "partition failed");
         const int64_t npad = padded_rows(b.data(), G);
-        std::vector<int32_t> pos;
+        hvec<int32_t> pos;
         degree_order(csr, b.data(), G, pos);
-        const std::vector<int32_t> colmap = column_map(csr.n, b.data(), G, npad, pos.data());
+        const hvec<int32_t> colmap = column_map(csr.n, b.data(), G, npad, pos.data());
         clk.mark("partition + order");
         PartLayout L;
         s = build_part(csr, b.data(), G, g, npad, pos.data(), colmap.data(), L, err);
@@ -1767,7 +1773,7 @@ topk_status_t topk_eig_plan_halo(const topk_matrix_t *A, int32_t G, int32_t g, i
         s = partition_rule_p(csr.rowptr.data(), csr.n, G, b.data());
         if (s != TOPK_OK) return fail(s, "partition failed");
         const int64_t npad = padded_rows(b.data(), G);
-        std::vector<int32_t> pp;
+        hvec<int32_t> pp;
         degree_order(csr, b.data(), G, pp);
         Halo H;
         build_halo(csr, b.data(), G, g, npad, pp.data(), H);

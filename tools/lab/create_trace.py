@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 os.environ["TOPK_TRACE"] = "1"
 import numpy as np
 import synthgen as S, paper_2201_07498_b200 as T
-A = S.config_matrix("C3")
+A = S.config_matrix(sys.argv[1] if len(sys.argv) > 1 else "C3")
 for rep in range(5):
     t0 = time.perf_counter()
     h = T.TopkEig(A, 24, "f32", "f64")  # default options (symmetry check on)
