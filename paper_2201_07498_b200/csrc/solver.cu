@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <thread>
+
+#include <omp.h>
 #include <type_traits>
 #include <cstdio>
 #include <cstring>
@@ -1243,8 +1245,18 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
         const int nloc = (world > 1) ? 1 : G;
         std::vector<DevCsr> dcsr((size_t)nloc);
         std::string up_err;
+        // the host cores are split between the uploader and this thread while both run
+        // (two full OpenMP teams oversubscribe the cores: C3 create 57-60 ms with both at
+        // all cores, 49-50 ms split in halves, 71-78 ms with a quarter for the upload)
+        const int omp_all = omp_get_max_threads();
+        const int omp_half = std::max(1, omp_all / 2);
+        struct OmpRestore {
+            int n;
+            ~OmpRestore() { omp_set_num_threads(n); }
+        } omp_restore{omp_all};
         std::thread uploader([&] {
             cudaStream_t st = nullptr;
+            omp_set_num_threads(omp_half);
             try {
                 CUDA_TRY(cudaSetDevice(h->device));
                 CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1268,6 +1280,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 for (DevCsr &x : d) free_dev_csr(x);
             }
         } joiner{uploader, dcsr};
+        omp_set_num_threads(std::max(1, omp_all - omp_half));
         hvec<int32_t> pos;
         degree_order(csr, h->bounds.data(), G, pos);
         const hvec<int32_t> colmap = column_map(n, h->bounds.data(), G, npad, pos.data());
@@ -1400,6 +1413,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             }
             if (uploader.joinable()) {
                 uploader.join();
+                omp_set_num_threads(omp_all);
                 clk.mark("wait for CSR upload");
                 if (!up_err.empty()) throw CudaFail(up_err);
             }
