@@ -250,8 +250,10 @@ topk_status_t topk_eig_plan_layout(const topk_matrix_t *A, int32_t G, int32_t g,
 
 /* Memory runtime (mem_pool.h): device blocks freed by topk_eig_destroy are cached
  * per device and reused by later handles (no cudaMalloc/cudaFree on the create/
- * destroy path after the first handle). Returns every cached, unused block to the
- * driver; returns the bytes released. Thread-safe; live handles are unaffected. */
+ * destroy path after the first handle); large host blocks of the create-time layout
+ * arrays are cached the same way (no page faults on fresh memory per create).
+ * Returns every cached, unused device and host block to the driver / the C heap;
+ * returns the bytes released. Thread-safe; live handles are unaffected. */
 size_t topk_eig_trim_pool(void);
 
 /* Host-only: the symmetry check's four wrapping 64-bit hash sums over rows [r0, r1) of

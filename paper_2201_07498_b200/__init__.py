@@ -117,7 +117,7 @@ def nccl_id() -> bytes:
 
 
 def trim_pool() -> int:
-    """Return the library's cached device blocks to the driver (topk_eig_trim_pool)."""
+    """Return the library's cached device and host blocks (topk_eig_trim_pool)."""
     return int(_lib.topk_eig_trim_pool())
 
 

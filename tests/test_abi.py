@@ -134,6 +134,57 @@ def test_plan_layout_parallel_degree_order_vs_oracle(G):
         assert np.array_equal(L["rowptr"], orp) and np.array_equal(L["col"], ocol)
 
 
+def test_csr_validation_and_canonicalisation_paths():
+    """Row a1's one-pass CSR check (range, monotonic row pointers, strictly increasing
+    columns): a canonical CSR is borrowed, a CSR with unsorted / duplicated columns in a
+    row takes the regrouping path and lays out exactly like the oracle's canonical form
+    (duplicates summed in input order), and malformed input is E_STRUCTURE."""
+    A = S.rmat(12, 40_000, 3)
+    rng = np.random.default_rng(1)
+    col, val = A.col.copy(), A.val.copy()
+    for r in rng.choice(A.n, 200, replace=False):  # shuffle some rows' entries
+        a, b = A.rowptr[r], A.rowptr[r + 1]
+        if b - a > 1:
+            o = rng.permutation(b - a)
+            col[a:b], val[a:b] = col[a:b][o], val[a:b][o]
+    U = S.CSR(A.n, A.rowptr, col, val)
+    rows = np.repeat(np.arange(A.n), np.diff(A.rowptr))
+    crp, ccol, cval = O.coo_to_csr(A.n, rows, col, val)
+    for G in (1, 2):
+        b = O.partition(crp, G)
+        for g in range(G):
+            L = T.plan_layout(U, G, g, "f64")
+            orp, ocol, oval, onpad = O.layout(crp, ccol, cval, G, b, g, "f64")
+            assert np.array_equal(L["rowptr"], orp) and np.array_equal(L["col"], ocol)
+            assert np.array_equal(L["val"].view(np.uint64), oval.view(np.uint64))
+    # a duplicated entry inside a row (unsorted by equality): summed like COO
+    r = int(np.argmax(np.diff(A.rowptr) > 2))
+    a = A.rowptr[r]
+    col2 = A.col.copy(); col2[a + 1] = col2[a]
+    D = S.CSR(A.n, A.rowptr, col2, A.val)
+    rp3, c3, v3 = O.coo_to_csr(A.n, rows, col2, A.val)
+    L = T.plan_layout(D, 1, 0, "f64")
+    orp, ocol, oval, _ = O.layout(rp3, c3, v3, 1, O.partition(rp3, 1), 0, "f64")
+    assert np.array_equal(L["rowptr"], orp) and np.array_equal(L["col"], ocol)
+    # malformed: column out of range, decreasing row pointer
+    bad = A.col.copy(); bad[5] = A.n
+    dec = A.rowptr.copy(); k = int(np.argmax(np.diff(A.rowptr) > 0)); dec[k + 1] = dec[k] - 1 if dec[k] > 0 else dec[k + 2] + 1
+    for M in (S.CSR(A.n, A.rowptr, bad, A.val), S.CSR(A.n, dec, A.col, A.val)):
+        with pytest.raises(T.TopkError) as e:
+            T.plan_layout(M, 1, 0, "f64")
+        assert e.value.status == 2
+
+
+def test_host_block_cache_trim():
+    """The create-time layout arrays (>= 1 MB) come from the library's host block cache
+    (mem_pool.h): after a host-only layout the cached blocks are released by
+    topk_eig_trim_pool, and a second trim finds nothing."""
+    A = S.rmat(16, 500_000, 2)
+    T.plan_layout(A, 1, 0, "f32")
+    assert T.trim_pool() >= A.n * 4
+    assert T.trim_pool() == 0
+
+
 @pytest.mark.parametrize("G", [1, 3])
 def test_physical_format_unpacks_to_logical(G):
     """The SpMV physical format (big-row CSR chunks + SELL-32 slices, host_prep.h)
