@@ -100,7 +100,7 @@ HostPool &host_pool() {
     return *p;
 }
 constexpr size_t kHostGran = size_t(2) << 20;
-constexpr size_t kHostCacheMax = size_t(32) << 30;  // cached (unused) host bytes kept at most
+constexpr size_t kHostCacheMax = size_t(8) << 30;  // cached (unused) host bytes kept at most
 size_t host_round(size_t b) { return (b + kHostGran - 1) / kHostGran * kHostGran; }
 size_t trim_host_locked(HostPool &P) {
     size_t freed = 0;

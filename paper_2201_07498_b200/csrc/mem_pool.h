@@ -6,7 +6,8 @@
 //  * a caching host allocator for large blocks (>= 1 MB; the host-side layout arrays of
 //    topk_eig_create): freed blocks are kept and reused, new ones are 2 MB aligned with
 //    transparent huge pages requested, so repeated creates do not pay a page fault per
-//    4 KB of fresh memory (measured on C3: 120 -> ~80 ms per create);
+//    4 KB of fresh memory (measured on C3: 120 -> ~80 ms per create); at most 8 GB
+//    of unused blocks are kept;
 //  * staged host<->device copies through two pinned chunks: the host side of chunk
 //    i+1 (a parallel memcpy or an element conversion) overlaps the DMA of chunk i,
 //    so pageable caller buffers and the host-side layout move at pinned-copy speed.
