@@ -121,6 +121,29 @@ def test_spmv_parity(T, c1, c3s, name, storage, vals, G):
     assert np.all(np.abs(y - yr) <= bound + 1e-300), np.max(np.abs(y - yr) / (bound + 1e-300))
 
 
+# ------------------------------------------------------------------ create: symmetry check on the device path
+def test_create_rejects_asymmetric_on_device_host(T, c3s):
+    """Row a2 through create on a GPU host: a one-entry value change, a dropped mirror
+    entry and an asymmetric pattern are E_NOT_SYMMETRIC at G = 1 and 3, no handle is
+    created, and the next create/solve in the same process is unaffected."""
+    A = c3s
+    r = int(np.argmax(np.diff(A.rowptr) > 3))
+    k = A.rowptr[r] + 1
+    val = A.val.copy(); val[k] += 2.0 ** -20
+    drop_rp = A.rowptr.copy(); drop_rp[r + 1:] -= 1
+    variants = [S.CSR(A.n, A.rowptr, A.col, val),
+                S.CSR(A.n, drop_rp, np.delete(A.col, k), np.delete(A.val, k)),
+                S.from_dense(np.array([[1.0, 2.0], [0.0, 1.0]]))]
+    for V in variants:
+        for G in (1, 3):
+            with pytest.raises(T.TopkError) as e:
+                T.TopkEig(V, 1, "f32", "f64", parts=min(G, V.n))
+            assert e.value.status == 3
+    ref = O.solve(A.rowptr, A.col, A.val, K=8, m=16, seed=2)
+    res = T.solve(A, 8, storage="f64", compute="f64", m=16, seed=2)
+    assert normwise(res.eigenvalues, ref.eigenvalues) <= 1e-8
+
+
 # ------------------------------------------------------------------ small exact cases
 def test_spec_examples(T, golden):
     for key in ("two_by_two", "antidiag_tie", "diag54321_top2"):
