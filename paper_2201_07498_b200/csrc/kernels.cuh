@@ -1749,7 +1749,9 @@ __global__ void __launch_bounds__(256) k_layout_big(const int64_t *srp, const in
 template <typename VT>
 __global__ void __launch_bounds__(256) k_layout_big_chunks(const int64_t *srp, const int32_t *scol, const VT *sval,
                                                            const int32_t *perm, const int64_t *drp, const Chunk *chunks,
-                                                           int nchunks, const int32_t *colmap, int32_t *pcol, VT *pval) {
+                                                           int nchunks, const int32_t *colmap, int64_t nphys, int32_t *pcol,
+                                                           VT *pval) {
+    (void)nphys;
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1770,6 +1772,8 @@ __global__ void __launch_bounds__(256) k_layout_big_chunks(const int64_t *srp, c
             for (int u = 0; u < U; ++u) {
                 const int e = e0 + 32 * u + lane;
                 if (e < C.cnt) {
+                    TOPK_DCHECK(C.z0 + e < nphys && C.z0 + e >= drp[C.row] && C.z0 + e < drp[C.row + 1],
+                                "big-row chunk scatter destination");
                     pcol[C.z0 + e] = colmap[c[u]];
                     pval[C.z0 + e] = v[u];
                 }

@@ -992,7 +992,7 @@ static void scatter_pass(topk_eig_s *h, Part &p, const PartLayout &L, const DevC
     if (L.nbig > 0 && MODE == 0) {
         if (dp.nchunks > 0) {
             k_layout_big_chunks<VT><<<h->nsm * 8, 256, 0, h->stream>>>(d.srp, d.scol, sval, p.perm, d_drp, dp.chunks, dp.nchunks,
-                                                                       d_colmap, dp.col, reinterpret_cast<VT *>(dp.val));
+                                                                       d_colmap, dp.nphys, dp.col, reinterpret_cast<VT *>(dp.val));
             CUDA_TRY(cudaGetLastError());
         }
     } else if (L.nbig > 0) {
