@@ -243,6 +243,9 @@ template <typename VT, typename ST, typename CT, bool LOCAL, bool BIG, int GQ>
 #ifndef TOPK_SPMV_GQ
 #define TOPK_SPMV_GQ 8
 #endif
+#ifndef TOPK_SPMV_SELL_PIPE3
+#define TOPK_SPMV_SELL_PIPE3 1
+#endif
 #ifdef TOPK_SPMV_MINB
 #define TOPK_SPMV_BOUNDS __launch_bounds__(kSpmvNT, TOPK_SPMV_MINB)
 #else
@@ -369,6 +372,70 @@ __device__ __forceinline__ void spmv_body(const SpmvArgs &a, int it) {
                 }
             }
             CT acc = CT(0);
+          if constexpr (!BIG && TOPK_SPMV_SELL_PIPE3) {
+            // SELL-only kernel: three-stage software pipeline -- col/val loads two groups
+            // ahead, x gathers one group ahead of the multiply-adds, so a gather never
+            // waits on a column index loaded in the same step (low-degree slices have
+            // little else to overlap; profiles/r02_mesh_spmv_ab.jsonl)
+            int cB[GQ], cC[GQ];
+            VT vA[GQ], vB[GQ], vC[GQ];
+            ST xA[GQ], xB[GQ];
+#pragma unroll
+            for (int q = 0; q < GQ; ++q) {
+                const int64_t k = base + lane + 32 * q;
+                const int c0 = q < ntot ? ld_col_stream(col + k) : 0;
+                vA[q] = q < ntot ? ld_val_stream<VT>(val + k) : VT(0);
+                const int t1 = GQ + q;
+                cB[q] = t1 < ntot ? ld_col_stream(col + k + 32 * GQ) : 0;
+                vB[q] = t1 < ntot ? ld_val_stream<VT>(val + k + 32 * GQ) : VT(0);
+                TOPK_DCHECK(q >= ntot || (c0 >= 0 && c0 < a.xlen), "SpMV SELL gather out of x");
+                xA[q] = q < ntot ? __ldg(x + c0) : ST(0);
+            }
+            for (int t0 = 0; t0 < ntot; t0 += GQ) {
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) {
+                    const int t1 = t0 + GQ + q, t2 = t0 + 2 * GQ + q;
+                    TOPK_DCHECK(t1 >= ntot || (cB[q] >= 0 && cB[q] < a.xlen), "SpMV SELL gather out of x");
+                    xB[q] = t1 < ntot ? __ldg(x + cB[q]) : ST(0);
+                    const int64_t k = base + lane + 32 * t2;
+                    cC[q] = t2 < ntot ? ld_col_stream(col + k) : 0;
+                    vC[q] = t2 < ntot ? ld_val_stream<VT>(val + k) : VT(0);
+                }
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) {
+                    const int t = t0 + q;
+                    if (t < ntot) {
+                        acc += cvt<CT>(vA[q]) * cvt<CT>(xA[q]);
+                        if (t + 1 == bound) {  // warp-uniform: slice sl complete
+                            if (row < a.nnonempty) {
+                                if constexpr (LOCAL) {
+                                    a.ypart[row] = (double)acc;
+                                } else {
+                                    if (yp) acc += (CT)ypc;
+                                    const CT yv = s * acc;
+                                    y[row] = rnd_ct<ST, CT>(yv);
+                                    alpha_acc += yv * (s * cvt<CT>(ucur));
+                                    if (a.y_dbg) a.y_dbg[row] = (double)acc;
+                                }
+                            }
+                            acc = CT(0);
+                            ++sl;
+                            bound += wnext;
+                            wnext = (sl + 1 < I.y) ? (int)__ldg(a.sell + sl + 1).y : 0;
+                            row += 32;
+                            if constexpr (!LOCAL) {
+                                if (row < a.nnonempty) {
+                                    ucur = ld_noalloc<ST>(ui + row);
+                                    if (yp) ypc = __ldcg(yp + row);
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < GQ; ++q) { xA[q] = xB[q]; vA[q] = vB[q]; vB[q] = vC[q]; cB[q] = cC[q]; }
+            }
+          } else {
             int cc[GQ];
             VT vv[GQ];
 #pragma unroll
@@ -425,6 +492,7 @@ __device__ __forceinline__ void spmv_body(const SpmvArgs &a, int it) {
                     }
                 }
             }
+          }
         }
     }
     if constexpr (LOCAL) return;
@@ -442,22 +510,24 @@ __device__ __forceinline__ void spmv_body(const SpmvArgs &a, int it) {
 
 // The SpMV kernels: with the big-row chunk path (plain bound; measured above), and
 // SELL-only (a pass without chunks: low-degree matrices such as meshes and road
-// networks). Measured on C6 (tools/lab/spmv_ab.py, profiles/r02_mesh_spmv_ab.jsonl):
-// (min CTAs/SM, GQ) = (3, 8) 167-171 us, (4, 4) 172, (3, 6) 176, (6, 2) 186, (5, 4) 198,
-// (2, 16) 199, (4, 2) 226, (6, 4) 257 (spills): more resident warps do not beat
-// deeper per-warp groups; the stream marked L2 evict-first: 194 vs 172 (worse).
+// networks). Measured on C6 (tools/lab/spmv_ab.py, profiles/r02_mesh_spmv_ab.jsonl),
+// two-stage loop: (min CTAs/SM, GQ) = (3, 8) 167-171 us, (4, 4) 172, (3, 6) 176,
+// (6, 2) 186, (5, 4) 198, (2, 16) 199, (4, 2) 226, (6, 4) 257 (spills); the stream marked
+// L2 evict-first: 194 vs 172 (worse). Three-stage loop (adopted): (4, 4) 161.6-161.7 us,
+// (3, 8) 164.5, (3, 6) 170, (5, 3) 183 and (6, 2) 211 (spills).
 #ifndef TOPK_SPMV_SELL_MINB
-#define TOPK_SPMV_SELL_MINB 3
+#define TOPK_SPMV_SELL_MINB 4
 #endif
 #ifndef TOPK_SPMV_SELL_GQ
-#define TOPK_SPMV_SELL_GQ 8
+#define TOPK_SPMV_SELL_GQ 4
 #endif
 template <typename VT, typename ST, typename CT, bool LOCAL>
 __global__ void TOPK_SPMV_BOUNDS k_spmv(SpmvArgs a, int it) {
     spmv_body<VT, ST, CT, LOCAL, true, TOPK_SPMV_GQ>(a, it);
 }
 template <typename VT, typename ST, typename CT, bool LOCAL>
-__global__ void __launch_bounds__(kSpmvNT, TOPK_SPMV_SELL_MINB) k_spmv_sell(SpmvArgs a, int it) {
+__global__ void __launch_bounds__(kSpmvNT, (sizeof(VT) == 8 || sizeof(ST) == 8) ? 3 : TOPK_SPMV_SELL_MINB)
+    k_spmv_sell(SpmvArgs a, int it) {  // fp64 storage: 3 CTAs/SM (the 4-CTA bound spills)
     spmv_body<VT, ST, CT, LOCAL, false, TOPK_SPMV_SELL_GQ>(a, it);
 }
 
