@@ -1,6 +1,8 @@
 """Ritz output pass: position order + un-permute vs the direct row-order pass
 (k_ritz_mma DIRECT) on C3 / C6 (FDF, K = m = 24): kernel times per solve and
-whether both give the same eigenvectors bit for bit."""
+whether both give the same eigenvectors bit for bit. The direct variant and its
+ritz_path values ("tc_unpermute", "tc_direct") were removed after this measurement
+(slower, profiles/r02_ritz_direct_ab.jsonl); the script documents the run."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
