@@ -297,6 +297,33 @@ double bf16_bits_to_double(uint16_t b) {
 
 
 
+// a[i] <- a[0] + ... + a[i] (parallel: per-thread chunk sums, a serial scan over the
+// threads' totals, then each chunk offset; identical to the serial running sum)
+static void prefix_sum_inplace(int64_t *a, int64_t n) {
+    const int T = n >= (1 << 20) ? std::max(1, omp_get_max_threads()) : 1;
+    if (T == 1) {
+        for (int64_t i = 1; i < n; ++i) a[i] += a[i - 1];
+        return;
+    }
+    std::vector<int64_t> tot((size_t)T + 1, 0);
+    const int64_t per = (n + T - 1) / T;
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int t = 0; t < T; ++t) {
+        const int64_t i0 = std::min(n, (int64_t)t * per), i1 = std::min(n, i0 + per);
+        int64_t run = 0;
+        for (int64_t i = i0; i < i1; ++i) { run += a[i]; a[i] = run; }
+        tot[(size_t)t + 1] = run;
+    }
+    for (int t = 0; t < T; ++t) tot[(size_t)t + 1] += tot[(size_t)t];
+#pragma omp parallel for schedule(static, 1) num_threads(T)
+    for (int t = 0; t < T; ++t) {
+        const int64_t i0 = std::min(n, (int64_t)t * per), i1 = std::min(n, i0 + per);
+        const int64_t off = tot[(size_t)t];
+        if (off)
+            for (int64_t i = i0; i < i1; ++i) a[i] += off;
+    }
+}
+
 void degree_order(const Csr &m, const int64_t *b, int32_t G, hvec<int32_t> &pos) {
     // stable counting sort by degree, descending (ties keep ascending row index)
     pos.resize((size_t)m.n);
@@ -404,12 +431,13 @@ topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32
         const int64_t r = r0 + out.perm[(size_t)p];
         out.rowptr[(size_t)p + 1] = m.rowptr[(size_t)r + 1] - m.rowptr[(size_t)r];
     }
+    // lengths are non-increasing in degree order: the non-empty rows are a prefix
     int64_t nne = 0;
-    for (int64_t p = 0; p < ng; ++p) {
-        if (out.rowptr[(size_t)p + 1] > 0) nne = p + 1;
-        out.rowptr[(size_t)p + 1] += out.rowptr[(size_t)p];
-    }
+#pragma omp parallel for schedule(static) reduction(max : nne)
+    for (int64_t p = 0; p < ng; ++p)
+        if (out.rowptr[(size_t)p + 1] > 0) nne = std::max(nne, p + 1);
     out.nnonempty = nne;
+    prefix_sum_inplace(out.rowptr.data() + 1, ng);
     hp_mark("perm + rowptr");
     // physical format: big rows (CSR prefix, chunked), then SELL-32 slices
     int64_t nbig = 0;
@@ -429,14 +457,21 @@ topk_status_t build_part_tables(const Csr &m, const int64_t *b, int32_t G, int32
     const int64_t zbig = out.rowptr[(size_t)nbig];
     const int64_t nsl = (nne - nbig + 31) / 32;
     out.sell.assign((size_t)(2 * nsl), 0);
-    int64_t phys = zbig;
+    // slice widths in parallel, bases = zbig + 32 * (exclusive prefix of the widths)
+    hvec<int64_t> span((size_t)nsl);
+#pragma omp parallel for schedule(static)
     for (int64_t sl = 0; sl < nsl; ++sl) {
         const int64_t p0 = nbig + 32 * sl;
-        const int64_t w = out.rowptr[(size_t)p0 + 1] - out.rowptr[(size_t)p0];
-        out.sell[(size_t)(2 * sl)] = phys;
-        out.sell[(size_t)(2 * sl + 1)] = w;
-        phys += 32 * w;
+        span[(size_t)sl] = 32 * (out.rowptr[(size_t)p0 + 1] - out.rowptr[(size_t)p0]);
     }
+    prefix_sum_inplace(span.data(), nsl);
+#pragma omp parallel for schedule(static)
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        const int64_t incl = span[(size_t)sl], prev = sl ? span[(size_t)sl - 1] : 0;
+        out.sell[(size_t)(2 * sl)] = zbig + prev;
+        out.sell[(size_t)(2 * sl + 1)] = (incl - prev) / 32;
+    }
+    const int64_t phys = zbig + (nsl ? span[(size_t)nsl - 1] : 0);
     out.items.clear();
     for (int64_t sl = 0; sl < nsl;) {
         int64_t e = sl, width = 0;

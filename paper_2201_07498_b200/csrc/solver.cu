@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -924,7 +925,10 @@ static void *dalloc_or_throw(size_t bytes) {
     if (!q) CUDA_TRY(cudaErrorMemoryAllocation);
     return q;
 }
-static void upload_csr_slice(const Csr &csr, int64_t r0, int64_t ng, topk_dtype_t ms, DevCsr &d, cudaStream_t st) {
+// nthreads: OpenMP threads of the fills, read before every 32 MB chunk (the creating
+// thread raises it once its own host work is done)
+static void upload_csr_slice(const Csr &csr, int64_t r0, int64_t ng, topk_dtype_t ms, DevCsr &d, cudaStream_t st,
+                             const std::atomic<int> &nthreads) {
     const int64_t z0 = csr.rowptr[(size_t)r0], z = csr.rowptr[(size_t)(r0 + ng)] - z0;
     const size_t es = dsize(ms);
     d.srp = static_cast<int64_t *>(dalloc_or_throw((size_t)(ng + 1) * 8));
@@ -932,6 +936,7 @@ static void upload_csr_slice(const Csr &csr, int64_t r0, int64_t ng, topk_dtype_
     d.sval = dalloc_or_throw((size_t)z * es);
     const int64_t *srp = csr.rowptr.data() + r0;
     auto fill_srp = [&](char *dst, size_t off, size_t nb) {
+        omp_set_num_threads(nthreads.load());
         const size_t i0 = off / 8, cnt = nb / 8;
         int64_t *dd = reinterpret_cast<int64_t *>(dst);
 #pragma omp parallel for schedule(static)
@@ -939,9 +944,13 @@ static void upload_csr_slice(const Csr &csr, int64_t r0, int64_t ng, topk_dtype_
     };
     CUDA_TRY(staged_h2d(d.srp, (size_t)(ng + 1) * 8, fill_srp, st));
     const char *sc = reinterpret_cast<const char *>(csr.col.data() + z0);
-    CUDA_TRY(staged_h2d(d.scol, (size_t)z * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, sc + off, nb); }, st));
+    CUDA_TRY(staged_h2d(d.scol, (size_t)z * 4, [&](char *dst, size_t off, size_t nb) {
+        omp_set_num_threads(nthreads.load());
+        par_memcpy(dst, sc + off, nb);
+    }, st));
     const double *sv = csr.val.data() + z0;
     auto fill_val = [&](char *dst, size_t off, size_t nb) {
+        omp_set_num_threads(nthreads.load());
         const size_t k0 = off / es, cnt = nb / es;
 #pragma omp parallel for schedule(static)
         for (size_t k = 0; k < cnt; ++k) {
@@ -1254,16 +1263,16 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
             int n;
             ~OmpRestore() { omp_set_num_threads(n); }
         } omp_restore{omp_all};
+        std::atomic<int> up_threads{omp_half};
         std::thread uploader([&] {
             cudaStream_t st = nullptr;
-            omp_set_num_threads(omp_half);
             try {
                 CUDA_TRY(cudaSetDevice(h->device));
                 CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
                 for (int lp = 0; lp < nloc; ++lp) {
                     const int g = (world > 1) ? h->rank : lp;
                     upload_csr_slice(csr, h->bounds[(size_t)g], h->bounds[(size_t)g + 1] - h->bounds[(size_t)g], ms,
-                                     dcsr[(size_t)lp], st);
+                                     dcsr[(size_t)lp], st, up_threads);
                 }
             } catch (CudaFail &e) {
                 up_err = e.msg;
@@ -1406,6 +1415,7 @@ static topk_status_t create_impl(topk_eig_t *out, const topk_matrix_t *A, int32_
                 CUDA_TRY(scopy(h->stream, p.inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
             }
             if (h->halo) setup_halo(h.get(), p, csr, npad, pos.data(), d_colmap);
+            if (lp + 1 == nlocal) up_threads.store(omp_all);  // this thread's host work is done: the upload takes every core
             if (lp == 0 && !h->halo) {  // after the first part's tables: the staging buffers are the uploader's until then
                 const char *cm = reinterpret_cast<const char *>(colmap.data());
                 CUDA_TRY(staged_h2d(d_colmap, (size_t)n * 4, [&](char *dst, size_t off, size_t nb) { par_memcpy(dst, cm + off, nb); },

@@ -5,7 +5,7 @@ os.environ["TOPK_TRACE"] = "1"
 import numpy as np
 import synthgen as S, paper_2201_07498_b200 as T
 A = S.config_matrix(sys.argv[1] if len(sys.argv) > 1 else "C3")
-for rep in range(5):
+for rep in range(int(os.environ.get("REPS", "5"))):
     t0 = time.perf_counter()
     h = T.TopkEig(A, 24, "f32", "f64")  # default options (symmetry check on)
     t1 = time.perf_counter()
