@@ -442,6 +442,7 @@ def main():
                     "bytes_per_iteration": int(info["bytes_nvlink"]) // max(1, m),
                     "gbs_if_spread_over_lanczos_phase": round(info["bytes_nvlink"] / max(info["ms_lanczos"], 1e-9) / 1e6, 1),
                     "nvlink5_gbs_per_direction": 900,
+                    "frac_of_nvlink5": round(info["bytes_nvlink"] / max(info["ms_lanczos"], 1e-9) / 1e6 / 900, 4),
                     "note": "modelled bytes (topk_eig_info_t.bytes_nvlink); the exchange is not timed separately"},
                 "solve_info": {k: info[k] for k in ("k_found", "iterations", "breakdown", "jacobi_sweeps",
                                                     "jacobi_converged")},
